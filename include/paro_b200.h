@@ -1,0 +1,201 @@
+/*
+ * paro_b200.h -- C ABI of the B200-native PAROAttention hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ library API on the hot
+ * path (reference proj/include/paro/ headers). Plain pointers
+ * and sizes only; no exceptions cross it. Every call returns a status:
+ *
+ *   PARO_OK (0) or an error class whose tens digit is the reference exit code
+ *   (proj/include/paro/error.hpp:11-40): 2x = ConfigError/ShapeError/InputError,
+ *   3x = FormatError/IoError, 4x = InvariantError, 5x = CUDA runtime failure
+ *   (no reference counterpart). paro_last_error() returns the thread-local
+ *   message of the last failing call on the calling thread.
+ *
+ * Supported hot-path configuration (anything else is rejected with
+ * PARO_E_CONFIG, never served by a CPU fallback): block = 64, d in {64, 128},
+ * P/V bits in {4, 8}, dense_prefix = 0, 2-D (H,W) or 3-D (F,H,W) token grids.
+ *
+ * Threading: one paro_ctx per GPU, used from one host thread; layers belong to
+ * the context they were created on. Device pointers are caller-owned unless a
+ * function says otherwise; all device work is enqueued on the given stream.
+ */
+#ifndef PARO_B200_H
+#define PARO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARO_OK 0
+#define PARO_E_CONFIG 20    /* ConfigError    (error.hpp:21-23) */
+#define PARO_E_SHAPE 21     /* ShapeError     (error.hpp:24-26) */
+#define PARO_E_INPUT 22     /* InputError     (error.hpp:27-29) */
+#define PARO_E_FORMAT 30    /* FormatError    (error.hpp:30-32) */
+#define PARO_E_IO 31        /* IoError        (error.hpp:33-35) */
+#define PARO_E_INVARIANT 40 /* InvariantError (error.hpp:36-38) */
+#define PARO_E_CUDA 50      /* CUDA runtime error (new) */
+
+#define PARO_BLOCK 64
+
+typedef void* paro_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+typedef struct paro_ctx paro_ctx;
+typedef struct paro_layer paro_layer;
+
+const char* paro_last_error(void);
+const char* paro_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Host-side integer stages (no GPU needed).
+ * ------------------------------------------------------------------------- */
+
+/* parse_grid("F:13,H:30,W:45") -- replaces paro::parse_grid + TokenGrid
+ * validation (tensor.cpp:320-341, 389-408). labels/extents hold >= 3 slots. */
+int paro_parse_grid(const char* text, int* ndim, char* labels, uint32_t* extents);
+
+/* make_perm(grid, order) -- replaces paro::make_perm (reorder.hpp:32,
+ * reorder.cpp:49-72). forward[old] = new, inverse[new] = old, N entries each. */
+int paro_make_perm(int ndim, const char* labels, const uint32_t* extents, const char* order, uint32_t* forward,
+                   uint32_t* inverse);
+
+/* enumerate_perms(grid) orders -- replaces paro::enumerate_perms
+ * (reorder.cpp:74-91): identity first, then lexicographic. `orders` receives
+ * count*ndim chars (no terminators); count = ndim! (<= 6). */
+int paro_enumerate_orders(int ndim, const char* labels, char* orders, int* count);
+
+/* PMSK blob decode -- replaces paro::deserialize_mask (mask.hpp:74,
+ * mask.cpp:217-244). bits (k_rows*k_cols bytes, row-major) may be NULL to
+ * query the header; consumed may be NULL. */
+int paro_deserialize_mask(const uint8_t* data, size_t size, uint32_t* k_rows, uint32_t* k_cols, uint32_t* block,
+                          uint8_t* bits, size_t* consumed);
+
+/* PMSK blob encode -- replaces paro::serialize_mask (mask.cpp:197-215).
+ * out may be NULL to query *size. */
+int paro_serialize_mask(const uint8_t* bits, uint32_t k_rows, uint32_t k_cols, uint32_t block, uint8_t* out,
+                        size_t* size);
+
+/* PSCH schedule lookup -- replaces load_schedule(path).at(t)
+ * (mask.cpp:132-140, 267-305) on an in-memory PSCH image. bits may be NULL. */
+int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_rows, uint32_t* k_cols,
+                     uint32_t* block, uint8_t* bits);
+
+/* gen_mask(sums, density, block, guard) -- host restatement of the offline mask
+ * producer paro::gen_mask (mask.cpp:56-130), used to build bench/demo masks.
+ * sums: k_rows*k_cols doubles; bits: k_rows*k_cols bytes out. */
+int paro_gen_mask(const double* sums, uint32_t k_rows, uint32_t k_cols, double density, uint32_t block,
+                  uint32_t guard_blocks, uint8_t* bits, uint32_t* repaired_rows);
+
+/* Synthetic N(0,1) fp32 inputs: MT19937-64, u = (x>>11)*2^-53, Box-Muller on
+ * (1-u1, u2), the generator documented in synth.cpp:20-22,173-182. */
+int paro_synth_randn(uint64_t seed, size_t count, float* out);
+
+/* ---------------------------------------------------------------------------
+ * Device context.
+ * ------------------------------------------------------------------------- */
+int paro_ctx_create(int device, paro_ctx** out);
+int paro_ctx_destroy(paro_ctx* ctx);
+int paro_ctx_num_sms(const paro_ctx* ctx, int* out);
+
+/* pinned host buffers for the e2e path (cudaHostAlloc / cudaFreeHost) */
+int paro_host_alloc(size_t bytes, void** out);
+int paro_host_free(void* p);
+/* device buffers (cudaMalloc / cudaFree) for C callers without another allocator */
+int paro_device_alloc(size_t bytes, void** out);
+int paro_device_free(void* p);
+int paro_memcpy(void* dst, const void* src, size_t bytes, paro_stream_t stream); /* cudaMemcpyDefault, async */
+int paro_stream_sync(paro_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Standalone device stages (bit-exact with the reference functions they name).
+ * ------------------------------------------------------------------------- */
+
+/* apply_perm_rows on the GPU -- replaces paro::apply_perm_rows
+ * (reorder.cpp:93-101): out.row(i) = in.row(inverse[i]); fp32 [rows, cols]. */
+int paro_apply_perm_rows_device(paro_ctx* ctx, paro_stream_t stream, const float* in, uint32_t rows, uint32_t cols,
+                                const uint32_t* inverse, float* out);
+
+/* quantize(m, {bits, Symmetric, PerBlock, 64}) on the GPU -- replaces
+ * paro::quantize (quant.cpp:60-104) for the hot path's Q/K configuration.
+ * codes: int8 [rows, cols] row-major; scales: ceil(rows/64)*ceil(cols/64) fp32
+ * in the reference's group order (quant.cpp:45-56). cols must be <= 128. */
+int paro_quantize_sym_device(paro_ctx* ctx, paro_stream_t stream, const float* in, uint32_t rows, uint32_t cols,
+                             int bits, int8_t* codes, float* scales);
+
+/* ---------------------------------------------------------------------------
+ * Layer: the per-head chain of cmd_run (proj/tools/main.cpp:276-305) for H
+ * heads at once -- per-head PARO permutation, block-mask application,
+ * Q/K INT8 + P/V INT8|INT4 quantized block-sparse attention, inverse
+ * permutation of the output. Q/K/V/O are fp32 [H, N, d] in ORIGINAL token
+ * order; N must equal the grid's token count.
+ * ------------------------------------------------------------------------- */
+
+/* orders: H*ndim chars (head h's axis order at orders[h*ndim]), or NULL for
+ * the identity plan of every head (plan_for_head without a plan file,
+ * main.cpp:118-120). */
+int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text, const char* orders,
+                      paro_layer** out);
+int paro_layer_destroy(paro_layer* layer);
+
+/* Masks: H*k*k bytes (BlockMask::bits per head, mask.hpp:15-32), k = ceil(N/64);
+ * NULL = every block kept (quantized_blocked_attention(in, nullptr, ...)).
+ * Runs K2 (mask -> per q-block-pair kept lists + LPT work order) on `stream`.
+ * The _device variant reads device bytes. */
+int paro_layer_set_masks(paro_layer* layer, paro_stream_t stream, const uint8_t* host_bits);
+int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const uint8_t* device_bits);
+
+/* K1: permuted gather + per-block quantization into layer-owned buffers. */
+int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,
+                                const float* v, int v_bits);
+
+/* K3: block-sparse quantized attention from the layer-owned codes; writes
+ * out [H,N,d] in original token order and zeroed [H,N] bytes (1 = row had no
+ * kept block, indexed by ORIGINAL token; may be NULL). scale 0 -> 1/sqrt(d)
+ * (AttnInputs::effective_scale, attention.cpp:26-28). pv_bits must equal the
+ * v_bits of the preceding reorder_quantize. */
+int paro_layer_attention(paro_layer* layer, paro_stream_t stream, float scale, int pv_bits, float* out,
+                         uint8_t* zeroed);
+
+/* K1 + K3 on device buffers. */
+int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
+                       float scale, int pv_bits, float* out, uint8_t* zeroed);
+
+/* End to end from HOST buffers (pinned for full speed): H2D of Q/K/V, K1, K3,
+ * D2H of O (and zeroed if non-NULL), synchronised before returning. */
+int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
+                            float scale, int pv_bits, float* out, uint8_t* zeroed);
+
+/* ---- introspection for parity tests ---- */
+/* Device buffers owned by the layer (kb = ceil(N/64), kb2 = kb rounded up to
+ * even, rows per head = kb2*64; all codes in PERMUTED token order, zero-padded). */
+typedef struct {
+    uint32_t heads, tokens, head_dim, kblocks, kblocks_padded; /* kblocks_padded = kb2 */
+    uint32_t groups;   /* head_dim/64 column groups of Q/K */
+    int8_t* q_codes;   /* [H, kb2*64, d] int8 */
+    int8_t* k_codes;   /* [H, kb2*64, d] int8 */
+    int8_t* v_codes;   /* [H, kb2*64, d] int8 (within +-qmax of the v_bits used) */
+    float* q_scales;   /* [H, kb2, groups] */
+    float* tile_meta;  /* [H, kb2, 4+d]: k_scale[g0], k_scale[g1] (0 if d=64), v_scale, 0,
+                          v_colsum[d] (exact integers in fp32) */
+    uint32_t* inverse; /* [H, N] device perm tables (filled at create) */
+    uint32_t* forward; /* [H, N] */
+} paro_layer_buffers;
+int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out);
+
+/* K2 output: per head, per q-block kept-count (kept[H*k]), total kept tiles */
+int paro_layer_mask_stats(paro_layer* layer, uint32_t* kept_per_qblock, uint64_t* total_kept);
+
+/* Debug: int32 QK^T accumulators of (head, q-block, k-block) tiles through the
+ * same tcgen05 path K3 uses. tiles: n_tiles*3 uint32 (device); S: n_tiles *
+ * groups * 64 * 64 int32 (device), [tile][group][row][col]. */
+int paro_layer_debug_qk(paro_layer* layer, paro_stream_t stream, uint32_t n_tiles, const uint32_t* tiles, int32_t* S);
+
+/* Launch accounting: number of kernels the last forward launched, and the
+ * last K3 kernel's grid size. */
+int paro_layer_last_launches(const paro_layer* layer, int* kernels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARO_B200_H */

@@ -1,0 +1,864 @@
+// host.cpp -- C-ABI implementation of include/paro_b200.h.
+//
+// Host-side integer stages restate the reference's TokenGrid / make_perm /
+// PMSK / PSCH / gen_mask contracts (cited per function); the device stages
+// launch the sm_100a kernels in prep_kernels.cu and attention_kernel.cu.
+// There is no CPU fallback for any device stage: without a usable sm_100
+// device every device call fails with PARO_E_CUDA.
+#include "../../include/paro_b200.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "layer.cuh"
+
+namespace paro {
+cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits, cudaStream_t st);
+cudaError_t launch_quantize_sym(const float* in, uint32_t rows, uint32_t cols, int bits, int8_t* codes,
+                                float* scales, cudaStream_t st);
+cudaError_t launch_apply_perm_rows(const float* in, uint32_t rows, uint32_t cols, const uint32_t* inverse, float* out,
+                                   cudaStream_t st);
+cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uint32_t* fwd, uint32_t* inv,
+                               cudaStream_t st);
+cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st);
+cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                      float scale_log2, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st);
+cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
+                            const uint32_t* tiles, int32_t* S, cudaStream_t st);
+} // namespace paro
+
+using paro::LayerDev;
+using paro::PermDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(PARO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PARO_OK;
+    } catch (const Fail& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return PARO_E_INVARIANT;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PARO_E_INVARIANT;
+    }
+}
+
+// ---------------------------------------------------------------- grid
+struct Grid {
+    int ndim = 0;
+    char labels[3] = {0, 0, 0};
+    uint32_t ext[3] = {0, 0, 0};
+    size_t tokens() const {
+        size_t n = 1;
+        for (int a = 0; a < ndim; ++a)
+            n *= ext[a];
+        return n;
+    }
+    int axis_index(char c) const {
+        for (int a = 0; a < ndim; ++a)
+            if (labels[a] == c)
+                return a;
+        fail(PARO_E_INPUT, std::string("grid has no axis labeled '") + c + "'"); // tensor.cpp:350-355
+    }
+};
+
+// TokenGrid constructor rules (tensor.cpp:320-341)
+void validate_grid(const Grid& g) {
+    if (g.ndim != 2 && g.ndim != 3)
+        fail(PARO_E_CONFIG, "token grid must have 2 or 3 axes, got " + std::to_string(g.ndim));
+    unsigned seen = 0;
+    for (int a = 0; a < g.ndim; ++a) {
+        unsigned bit;
+        switch (g.labels[a]) {
+        case 'F': bit = 1; break;
+        case 'H': bit = 2; break;
+        case 'W': bit = 4; break;
+        default: fail(PARO_E_CONFIG, std::string("unknown grid axis label '") + g.labels[a] + "'");
+        }
+        if (seen & bit)
+            fail(PARO_E_CONFIG, std::string("duplicate grid axis label '") + g.labels[a] + "'");
+        seen |= bit;
+        if (g.ext[a] == 0)
+            fail(PARO_E_CONFIG, std::string("grid axis '") + g.labels[a] + "' has zero extent");
+    }
+    if (g.ndim == 2 && (seen & 1))
+        fail(PARO_E_CONFIG, "2D grids use labels H and W only");
+}
+
+// parse_grid (tensor.cpp:389-408)
+Grid parse_grid_text(const char* text) {
+    if (!text)
+        fail(PARO_E_CONFIG, "null grid text");
+    Grid g;
+    std::string s(text);
+    size_t pos = 0;
+    std::vector<std::string> parts;
+    while (true) {
+        size_t c = s.find(',', pos);
+        parts.push_back(s.substr(pos, c == std::string::npos ? std::string::npos : c - pos));
+        if (c == std::string::npos)
+            break;
+        pos = c + 1;
+    }
+    if (s.empty())
+        parts.clear();
+    if (parts.size() > 3)
+        fail(PARO_E_CONFIG, "token grid must have 2 or 3 axes, got " + std::to_string(parts.size()));
+    for (const auto& part : parts) {
+        const size_t colon = part.find(':');
+        if (colon != 1 || part.size() < 3)
+            fail(PARO_E_CONFIG, "bad grid axis '" + part + "', expected LABEL:EXTENT (e.g. F:13)");
+        unsigned long v = 0;
+        try {
+            size_t used = 0;
+            v = std::stoul(part.substr(2), &used);
+            (void)used;
+        } catch (const std::exception&) {
+            fail(PARO_E_CONFIG, "bad grid extent in '" + part + "'");
+        }
+        g.labels[g.ndim] = part[0];
+        g.ext[g.ndim] = static_cast<uint32_t>(v);
+        ++g.ndim;
+    }
+    validate_grid(g);
+    return g;
+}
+
+Grid grid_from(int ndim, const char* labels, const uint32_t* extents) {
+    if (ndim < 0 || ndim > 3)
+        fail(PARO_E_CONFIG, "token grid must have 2 or 3 axes, got " + std::to_string(ndim));
+    Grid g;
+    g.ndim = ndim;
+    for (int a = 0; a < ndim; ++a) {
+        g.labels[a] = labels[a];
+        g.ext[a] = extents[a];
+    }
+    validate_grid(g);
+    return g;
+}
+
+// Per-head permutation descriptor for `order` (make_perm, reorder.cpp:49-72):
+// new index = row-major index of the old coordinates re-listed in `order`.
+PermDesc perm_desc(const Grid& g, const std::string& order) {
+    if ((int)order.size() != g.ndim)
+        fail(PARO_E_CONFIG, "permutation order '" + order + "' does not cover the grid axes");
+    uint32_t stride[3];
+    uint32_t s = 1;
+    for (int a = g.ndim; a-- > 0;) {
+        stride[a] = s;
+        s *= g.ext[a];
+    }
+    PermDesc pd{{1, 1, 1}, {0, 0, 0}};
+    const int off = 3 - g.ndim;
+    for (int a = 0; a < g.ndim; ++a) {
+        const int src = g.axis_index(order[a]);
+        pd.pext[off + a] = g.ext[src];
+        pd.ostride[off + a] = stride[src];
+    }
+    // a repeated label would make this a non-bijection; make_perm builds a
+    // TokenGrid from the re-listed axes, which rejects duplicates (tensor.cpp:333-334)
+    unsigned seen = 0;
+    for (int a = 0; a < g.ndim; ++a) {
+        const unsigned bit = 1u << g.axis_index(order[a]);
+        if (seen & bit)
+            fail(PARO_E_CONFIG, std::string("duplicate grid axis label '") + order[a] + "'");
+        seen |= bit;
+    }
+    return pd;
+}
+
+// ---------------------------------------------------------------- PMSK helpers (mask.cpp:179-244)
+uint32_t get_u32(const uint8_t* p) {
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+void put_u32(uint8_t* p, uint32_t v) {
+    p[0] = (uint8_t)(v & 0xff);
+    p[1] = (uint8_t)((v >> 8) & 0xff);
+    p[2] = (uint8_t)((v >> 16) & 0xff);
+    p[3] = (uint8_t)((v >> 24) & 0xff);
+}
+
+size_t decode_pmsk(const uint8_t* data, size_t size, uint32_t* kr, uint32_t* kc, uint32_t* block, uint8_t* bits) {
+    if (size < 18)
+        fail(PARO_E_FORMAT, "mask blob truncated: need 18 header bytes, have " + std::to_string(size));
+    if (std::memcmp(data, "PMSK", 4) != 0)
+        fail(PARO_E_FORMAT, "bad mask magic, expected \"PMSK\" (at byte offset 0)");
+    if (data[4] != 1)
+        fail(PARO_E_FORMAT, "unsupported mask version " + std::to_string(data[4]) + " (at byte offset 4)");
+    const uint32_t r = get_u32(data + 6), c = get_u32(data + 10), b = get_u32(data + 14);
+    if (r == 0 || c == 0 || b == 0)
+        fail(PARO_E_FORMAT, "mask dimensions must be nonzero");
+    const size_t row_bytes = (c + 7) / 8;
+    const size_t need = 18 + (size_t)r * row_bytes;
+    if (size < need)
+        fail(PARO_E_FORMAT, "mask blob truncated: need " + std::to_string(need) + " bytes, have " + std::to_string(size));
+    if (kr)
+        *kr = r;
+    if (kc)
+        *kc = c;
+    if (block)
+        *block = b;
+    if (bits)
+        for (size_t i = 0; i < r; ++i) {
+            const uint8_t* row = data + 18 + i * row_bytes;
+            for (size_t j = 0; j < c; ++j)
+                bits[i * c + j] = (row[j / 8] >> (j % 8)) & 1u;
+        }
+    return need;
+}
+
+} // namespace
+
+// ============================================================================
+// device context / layer objects
+// ============================================================================
+struct paro_ctx {
+    int device = 0;
+    int num_sms = 0;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+};
+
+struct paro_layer {
+    paro_ctx* ctx = nullptr;
+    Grid grid;
+    LayerDev L{};
+    std::vector<PermDesc> perm_host;
+    uint32_t* fwd = nullptr; // [H][N]
+    uint32_t* inv = nullptr; // [H][N]
+    uint8_t* mask_dev = nullptr;
+    bool masks_set = false;
+    int last_v_bits = 0;
+    int last_launches = 0;
+    CUtensorMap tm_q, tm_k, tm_v;
+    // e2e staging
+    float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+    uint8_t* dzero = nullptr;
+};
+
+namespace {
+
+void set_device(const paro_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
+
+template <typename T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    return static_cast<T*>(p);
+}
+
+void encode_codes_map(paro_ctx* ctx, CUtensorMap* m, int8_t* base, uint32_t D, uint64_t rows, uint32_t box_rows) {
+    cuuint64_t dims[2] = {D, rows};
+    cuuint64_t strides[1] = {D};
+    cuuint32_t box[2] = {D, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = ctx->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             D == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(PARO_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+void free_layer(paro_layer* l) {
+    cudaFree(l->L.perm);
+    cudaFree(l->L.q);
+    cudaFree(l->L.k);
+    cudaFree(l->L.v);
+    cudaFree(l->L.qsc);
+    cudaFree(l->L.meta);
+    cudaFree(l->L.items);
+    cudaFree(l->L.pair_count);
+    cudaFree(l->L.qb_count);
+    cudaFree(l->L.order);
+    cudaFree(l->L.work_counter);
+    cudaFree(l->fwd);
+    cudaFree(l->inv);
+    cudaFree(l->mask_dev);
+    cudaFree(l->dq);
+    cudaFree(l->dk);
+    cudaFree(l->dv);
+    cudaFree(l->dout);
+    cudaFree(l->dzero);
+}
+
+void check_bits(int bits) {
+    if (bits != 4 && bits != 8)
+        fail(PARO_E_CONFIG, "quantization bitwidth must be 4 or 8, got " + std::to_string(bits)); // quant.cpp:15-17
+}
+
+void check_layer(const paro_layer* l) {
+    if (!l)
+        fail(PARO_E_CONFIG, "null layer");
+}
+
+void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, float* out, uint8_t* zeroed) {
+    check_bits(pv_bits);
+    if (!l->masks_set)
+        fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before attention");
+    if (pv_bits != l->last_v_bits)
+        fail(PARO_E_CONFIG, "pv_bits " + std::to_string(pv_bits) + " does not match the V codes (" +
+                                std::to_string(l->last_v_bits) + " bits); rerun reorder_quantize");
+    if (!out)
+        fail(PARO_E_CONFIG, "null output");
+    // AttnInputs::effective_scale (attention.cpp:26-28), folded with log2(e) for ex2
+    const double eff = scale != 0.0f ? (double)scale : 1.0 / std::sqrt((double)l->L.D);
+    const float scale_log2 = (float)(eff * 1.4426950408889634);
+    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, scale_log2, pv_bits, out, zeroed, l->ctx->num_sms, st),
+               "k3_attention launch");
+}
+
+} // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* paro_last_error(void) { return g_last_error.c_str(); }
+const char* paro_version(void) { return "paro_b200 0.1 (sm_100a)"; }
+
+int paro_parse_grid(const char* text, int* ndim, char* labels, uint32_t* extents) {
+    return guarded([&] {
+        Grid g = parse_grid_text(text);
+        *ndim = g.ndim;
+        for (int a = 0; a < g.ndim; ++a) {
+            labels[a] = g.labels[a];
+            extents[a] = g.ext[a];
+        }
+    });
+}
+
+int paro_make_perm(int ndim, const char* labels, const uint32_t* extents, const char* order, uint32_t* forward,
+                   uint32_t* inverse) {
+    return guarded([&] {
+        Grid g = grid_from(ndim, labels, extents);
+        PermDesc pd = perm_desc(g, order ? std::string(order) : std::string());
+        const size_t n = g.tokens();
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t old = paro::perm_src(pd, (uint32_t)i);
+            inverse[i] = old;
+            forward[old] = (uint32_t)i;
+        }
+    });
+}
+
+int paro_enumerate_orders(int ndim, const char* labels, char* orders, int* count) {
+    return guarded([&] {
+        if (ndim != 2 && ndim != 3)
+            fail(PARO_E_CONFIG, "token grid must have 2 or 3 axes, got " + std::to_string(ndim));
+        // reorder.cpp:74-91: identity first, then the remaining orders in lexicographic order
+        std::string ident(labels, labels + ndim);
+        std::string perm = ident;
+        std::sort(perm.begin(), perm.end());
+        std::vector<std::string> out{ident};
+        do {
+            if (perm != ident)
+                out.push_back(perm);
+        } while (std::next_permutation(perm.begin(), perm.end()));
+        *count = (int)out.size();
+        for (size_t i = 0; i < out.size(); ++i)
+            std::memcpy(orders + i * ndim, out[i].data(), ndim);
+    });
+}
+
+int paro_deserialize_mask(const uint8_t* data, size_t size, uint32_t* k_rows, uint32_t* k_cols, uint32_t* block,
+                          uint8_t* bits, size_t* consumed) {
+    return guarded([&] {
+        const size_t used = decode_pmsk(data, size, k_rows, k_cols, block, bits);
+        if (consumed)
+            *consumed = used;
+    });
+}
+
+int paro_serialize_mask(const uint8_t* bits, uint32_t k_rows, uint32_t k_cols, uint32_t block, uint8_t* out,
+                        size_t* size) {
+    return guarded([&] {
+        const size_t row_bytes = (k_cols + 7) / 8;
+        const size_t total = 18 + (size_t)k_rows * row_bytes;
+        *size = total;
+        if (!out)
+            return;
+        std::memcpy(out, "PMSK", 4);
+        out[4] = 1;
+        out[5] = 0;
+        put_u32(out + 6, k_rows);
+        put_u32(out + 10, k_cols);
+        put_u32(out + 14, block);
+        std::memset(out + 18, 0, total - 18);
+        for (size_t i = 0; i < k_rows; ++i)
+            for (size_t j = 0; j < k_cols; ++j)
+                if (bits[i * k_cols + j])
+                    out[18 + i * row_bytes + j / 8] |= (uint8_t)(1u << (j % 8)); // LSB first
+    });
+}
+
+int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_rows, uint32_t* k_cols,
+                     uint32_t* block, uint8_t* bits) {
+    return guarded([&] {
+        // PSCH (mask.cpp:267-305): magic, u32 timesteps, u32 distinct (= T/2),
+        // (u32 t, PMSK) x distinct, shared PMSK; at(t) (mask.cpp:132-140)
+        if (size < 12)
+            fail(PARO_E_FORMAT, "truncated schedule header (at byte offset " + std::to_string(size) + ")");
+        if (std::memcmp(data, "PSCH", 4) != 0)
+            fail(PARO_E_FORMAT, "bad magic, expected \"PSCH\" (at byte offset 0)");
+        const uint32_t T = get_u32(data + 4), nd = get_u32(data + 8);
+        if (nd != T / 2)
+            fail(PARO_E_FORMAT, "schedule declares " + std::to_string(nd) + " distinct masks, expected " +
+                                    std::to_string(T / 2));
+        size_t off = 12;
+        const uint8_t* want = nullptr;
+        size_t want_size = 0;
+        for (uint32_t i = 0; i < nd; ++i) {
+            if (size < off + 4)
+                fail(PARO_E_FORMAT, "truncated distinct entry (schedule parse position " + std::to_string(off) + ")");
+            const uint32_t ti = get_u32(data + off);
+            off += 4;
+            const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
+            if (ti == t && t < T / 2) {
+                want = data + off;
+                want_size = used;
+            }
+            off += used;
+        }
+        const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
+        const uint8_t* shared = data + off;
+        off += used;
+        if (off != size)
+            fail(PARO_E_FORMAT, std::to_string(size - off) + " trailing bytes (at byte offset " + std::to_string(off) + ")");
+        if (t >= T)
+            fail(PARO_E_INPUT, "timestep " + std::to_string(t) + " out of range, schedule covers " + std::to_string(T));
+        if (t >= T / 2) {
+            want = shared;
+            want_size = used;
+        } else if (!want) {
+            fail(PARO_E_FORMAT, "schedule has no distinct mask for timestep " + std::to_string(t));
+        }
+        decode_pmsk(want, want_size, k_rows, k_cols, block, bits);
+    });
+}
+
+int paro_gen_mask(const double* sums, uint32_t kr, uint32_t kc, double density, uint32_t block, uint32_t guard,
+                  uint8_t* bits, uint32_t* repaired_rows) {
+    return guarded([&] {
+        // gen_mask (mask.cpp:56-130)
+        if (!(density > 0.0 && density <= 1.0))
+            fail(PARO_E_CONFIG, "density must be in (0,1], got " + std::to_string(density));
+        const size_t total = (size_t)kr * kc;
+        const size_t target = (size_t)std::ceil(density * (double)total);
+        auto guarded_blk = [&](size_t i, size_t j) { return i < guard || j < guard; };
+        size_t guard_count = 0;
+        if (guard > 0) {
+            const size_t gr = std::min<size_t>(guard, kr), gc = std::min<size_t>(guard, kc);
+            guard_count = total - (kr - gr) * (kc - gc);
+        }
+        if (guard_count > target)
+            fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
+                                    " blocks but the dense prefix alone occupies " + std::to_string(guard_count));
+        if (guard == 0 && target < kr)
+            fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
+                                    " blocks, fewer than the " + std::to_string(kr) + " rows that each need one");
+        struct Ref {
+            double sum;
+            uint32_t row, col;
+        };
+        std::vector<Ref> cand;
+        cand.reserve(total - guard_count);
+        for (uint32_t i = 0; i < kr; ++i)
+            for (uint32_t j = 0; j < kc; ++j)
+                if (!guarded_blk(i, j))
+                    cand.push_back({sums[(size_t)i * kc + j], i, j});
+        // keep-preference: larger sum, then smaller (row, col) -- a strict total order
+        std::sort(cand.begin(), cand.end(), [](const Ref& a, const Ref& b) {
+            if (a.sum != b.sum)
+                return a.sum > b.sum;
+            if (a.row != b.row)
+                return a.row < b.row;
+            return a.col < b.col;
+        });
+        std::memset(bits, 0, total);
+        for (size_t i = 0; i < kr; ++i)
+            for (size_t j = 0; j < kc; ++j)
+                if (guarded_blk(i, j))
+                    bits[i * kc + j] = 1;
+        for (size_t c = 0; c < target - guard_count; ++c)
+            bits[(size_t)cand[c].row * kc + cand[c].col] = 1;
+        std::vector<size_t> row_kept(kr, 0);
+        for (size_t i = 0; i < kr; ++i)
+            for (size_t j = 0; j < kc; ++j)
+                row_kept[i] += bits[i * kc + j];
+        uint32_t repaired = 0;
+        for (size_t i = 0; i < kr; ++i) {
+            if (row_kept[i] > 0)
+                continue;
+            size_t best = 0;
+            for (size_t j = 1; j < kc; ++j)
+                if (sums[i * kc + j] > sums[i * kc + best])
+                    best = j;
+            bits[i * kc + best] = 1;
+            ++row_kept[i];
+            ++repaired;
+            bool dropped = false;
+            for (size_t c = cand.size(); c-- > 0;) {
+                const Ref& cb = cand[c];
+                if (bits[(size_t)cb.row * kc + cb.col] && row_kept[cb.row] >= 2) {
+                    bits[(size_t)cb.row * kc + cb.col] = 0;
+                    --row_kept[cb.row];
+                    dropped = true;
+                    break;
+                }
+            }
+            if (!dropped)
+                fail(PARO_E_CONFIG, "cannot repair empty mask row " + std::to_string(i) + " at density " +
+                                        std::to_string(density));
+        }
+        if (repaired_rows)
+            *repaired_rows = repaired;
+    });
+}
+
+int paro_synth_randn(uint64_t seed, size_t count, float* out) {
+    return guarded([&] {
+        std::mt19937_64 rng(seed);
+        auto unit = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+        for (size_t i = 0; i < count; ++i) {
+            const double u1 = 1.0 - unit();
+            const double u2 = unit();
+            out[i] = static_cast<float>(std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2));
+        }
+    });
+}
+
+int paro_ctx_create(int device, paro_ctx** out) {
+    return guarded([&] {
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n)
+            fail(PARO_E_CONFIG, "device " + std::to_string(device) + " out of range (" + std::to_string(n) + " visible)");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            fail(PARO_E_CUDA, std::string("device ") + prop.name + " is sm_" + std::to_string(prop.major) +
+                                  std::to_string(prop.minor) + "; these kernels are built for sm_100a only");
+        auto* c = new paro_ctx;
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn) {
+            delete c;
+            fail(PARO_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+        }
+        c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        *out = c;
+    });
+}
+
+int paro_ctx_destroy(paro_ctx* ctx) {
+    return guarded([&] { delete ctx; });
+}
+
+int paro_ctx_num_sms(const paro_ctx* ctx, int* out) {
+    return guarded([&] { *out = ctx->num_sms; });
+}
+
+int paro_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { cuda_check(cudaHostAlloc(out, bytes, cudaHostAllocDefault), "cudaHostAlloc"); });
+}
+int paro_host_free(void* p) {
+    return guarded([&] { cuda_check(cudaFreeHost(p), "cudaFreeHost"); });
+}
+int paro_device_alloc(size_t bytes, void** out) {
+    return guarded([&] { cuda_check(cudaMalloc(out, bytes), "cudaMalloc"); });
+}
+int paro_device_free(void* p) {
+    return guarded([&] { cuda_check(cudaFree(p), "cudaFree"); });
+}
+int paro_memcpy(void* dst, const void* src, size_t bytes, paro_stream_t stream) {
+    return guarded([&] {
+        cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream), "cudaMemcpyAsync");
+    });
+}
+int paro_stream_sync(paro_stream_t stream) {
+    return guarded([&] { cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize"); });
+}
+
+int paro_apply_perm_rows_device(paro_ctx* ctx, paro_stream_t stream, const float* in, uint32_t rows, uint32_t cols,
+                                const uint32_t* inverse, float* out) {
+    return guarded([&] {
+        set_device(ctx);
+        if (rows == 0)
+            return;
+        cuda_check(paro::launch_apply_perm_rows(in, rows, cols, inverse, out, (cudaStream_t)stream), "apply_perm_rows");
+    });
+}
+
+int paro_quantize_sym_device(paro_ctx* ctx, paro_stream_t stream, const float* in, uint32_t rows, uint32_t cols,
+                             int bits, int8_t* codes, float* scales) {
+    return guarded([&] {
+        check_bits(bits);
+        if (cols != 64 && cols != 128)
+            fail(PARO_E_CONFIG, "device quantize supports 64 or 128 columns, got " + std::to_string(cols));
+        set_device(ctx);
+        if (rows == 0)
+            return;
+        cuda_check(paro::launch_quantize_sym(in, rows, cols, bits, codes, scales, (cudaStream_t)stream), "quantize");
+    });
+}
+
+int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text, const char* orders,
+                      paro_layer** out) {
+    return guarded([&] {
+        if (!ctx)
+            fail(PARO_E_CONFIG, "null context");
+        if (head_dim != 64 && head_dim != 128)
+            fail(PARO_E_CONFIG, "head dim must be 64 or 128 on the B200 path, got " + std::to_string(head_dim));
+        if (heads == 0 || heads > 65535)
+            fail(PARO_E_CONFIG, "heads must be in [1, 65535]");
+        Grid g = parse_grid_text(grid_text);
+        const size_t N = g.tokens();
+        if (N == 0 || N > (size_t)16383 * 64)
+            fail(PARO_E_CONFIG, "token count " + std::to_string(N) + " out of range");
+        set_device(ctx);
+        auto* l = new paro_layer;
+        l->ctx = ctx;
+        l->grid = g;
+        try {
+            for (uint32_t h = 0; h < heads; ++h) {
+                std::string ord = orders ? std::string(orders + (size_t)h * g.ndim, g.ndim)
+                                         : std::string(g.labels, g.labels + g.ndim);
+                l->perm_host.push_back(perm_desc(g, ord));
+            }
+            LayerDev& L = l->L;
+            L.H = heads;
+            L.N = (uint32_t)N;
+            L.D = head_dim;
+            L.G = head_dim / 64;
+            L.kb = (L.N + 63) / 64;
+            L.kb2 = (L.kb + 1) & ~1u;
+            L.np = L.kb2 / 2;
+            const size_t rows = (size_t)heads * L.kb2 * 64;
+            L.perm = dalloc<PermDesc>(heads);
+            L.q = dalloc<int8_t>(rows * head_dim);
+            L.k = dalloc<int8_t>(rows * head_dim);
+            L.v = dalloc<int8_t>(rows * head_dim);
+            L.qsc = dalloc<float>((size_t)heads * L.kb2 * L.G);
+            L.meta = dalloc<float>((size_t)heads * L.kb2 * paro::meta_stride(head_dim));
+            L.items = dalloc<uint16_t>((size_t)heads * L.np * L.kb);
+            L.pair_count = dalloc<uint32_t>((size_t)heads * L.np);
+            L.qb_count = dalloc<uint32_t>((size_t)heads * L.kb2);
+            L.order = dalloc<uint32_t>((size_t)heads * L.np);
+            L.work_counter = dalloc<uint32_t>(1);
+            l->fwd = dalloc<uint32_t>((size_t)heads * N);
+            l->inv = dalloc<uint32_t>((size_t)heads * N);
+            cuda_check(cudaMemset(L.q, 0, rows * head_dim), "cudaMemset");
+            cuda_check(cudaMemset(L.k, 0, rows * head_dim), "cudaMemset");
+            cuda_check(cudaMemset(L.v, 0, rows * head_dim), "cudaMemset");
+            cuda_check(cudaMemcpy(L.perm, l->perm_host.data(), heads * sizeof(PermDesc), cudaMemcpyHostToDevice),
+                       "cudaMemcpy perm");
+            cuda_check(paro::launch_perm_tables(L.perm, heads, L.N, l->fwd, l->inv, 0), "perm tables");
+            encode_codes_map(ctx, &l->tm_q, L.q, head_dim, rows, 128);
+            encode_codes_map(ctx, &l->tm_k, L.k, head_dim, rows, 64);
+            encode_codes_map(ctx, &l->tm_v, L.v, head_dim, rows, 64);
+            cuda_check(cudaDeviceSynchronize(), "layer init");
+        } catch (...) {
+            free_layer(l);
+            delete l;
+            throw;
+        }
+        *out = l;
+    });
+}
+
+int paro_layer_destroy(paro_layer* layer) {
+    return guarded([&] {
+        if (!layer)
+            return;
+        set_device(layer->ctx);
+        free_layer(layer);
+        delete layer;
+    });
+}
+
+static void set_masks_impl(paro_layer* l, cudaStream_t st, const uint8_t* bits, bool host) {
+    check_layer(l);
+    set_device(l->ctx);
+    const uint8_t* dbits = nullptr;
+    const size_t bytes = (size_t)l->L.H * l->L.kb * l->L.kb;
+    if (bits) {
+        if (host) {
+            if (!l->mask_dev)
+                l->mask_dev = dalloc<uint8_t>(bytes);
+            cuda_check(cudaMemcpyAsync(l->mask_dev, bits, bytes, cudaMemcpyHostToDevice, st), "mask upload");
+            dbits = l->mask_dev;
+        } else {
+            dbits = bits;
+        }
+    }
+    cuda_check(paro::launch_k2(l->L, dbits, st), "k2 launch");
+    l->masks_set = true;
+}
+
+int paro_layer_set_masks(paro_layer* layer, paro_stream_t stream, const uint8_t* host_bits) {
+    return guarded([&] { set_masks_impl(layer, (cudaStream_t)stream, host_bits, true); });
+}
+
+int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const uint8_t* device_bits) {
+    return guarded([&] { set_masks_impl(layer, (cudaStream_t)stream, device_bits, false); });
+}
+
+int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,
+                                const float* v, int v_bits) {
+    return guarded([&] {
+        check_layer(layer);
+        check_bits(v_bits);
+        if (!q || !k || !v)
+            fail(PARO_E_CONFIG, "null Q/K/V");
+        set_device(layer->ctx);
+        cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, (cudaStream_t)stream), "k1 launch");
+        layer->last_v_bits = v_bits;
+    });
+}
+
+int paro_layer_attention(paro_layer* layer, paro_stream_t stream, float scale, int pv_bits, float* out,
+                         uint8_t* zeroed) {
+    return guarded([&] {
+        check_layer(layer);
+        set_device(layer->ctx);
+        run_attention(layer, (cudaStream_t)stream, scale, pv_bits, out, zeroed);
+    });
+}
+
+int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
+                       float scale, int pv_bits, float* out, uint8_t* zeroed) {
+    return guarded([&] {
+        check_layer(layer);
+        check_bits(pv_bits);
+        if (!layer->masks_set)
+            fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
+        set_device(layer->ctx);
+        cudaStream_t st = (cudaStream_t)stream;
+        cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, st), "k1 launch");
+        layer->last_v_bits = pv_bits;
+        run_attention(layer, st, scale, pv_bits, out, zeroed);
+        layer->last_launches = 2;
+    });
+}
+
+int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
+                            float scale, int pv_bits, float* out, uint8_t* zeroed) {
+    return guarded([&] {
+        check_layer(layer);
+        check_bits(pv_bits);
+        if (!layer->masks_set)
+            fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
+        set_device(layer->ctx);
+        cudaStream_t st = (cudaStream_t)stream;
+        const LayerDev& L = layer->L;
+        const size_t elems = (size_t)L.H * L.N * L.D;
+        if (!layer->dq) {
+            layer->dq = dalloc<float>(elems);
+            layer->dk = dalloc<float>(elems);
+            layer->dv = dalloc<float>(elems);
+            layer->dout = dalloc<float>(elems);
+            layer->dzero = dalloc<uint8_t>((size_t)L.H * L.N);
+        }
+        cuda_check(cudaMemcpyAsync(layer->dq, q, elems * 4, cudaMemcpyHostToDevice, st), "H2D q");
+        cuda_check(cudaMemcpyAsync(layer->dk, k, elems * 4, cudaMemcpyHostToDevice, st), "H2D k");
+        cuda_check(cudaMemcpyAsync(layer->dv, v, elems * 4, cudaMemcpyHostToDevice, st), "H2D v");
+        cuda_check(paro::launch_k1(L, layer->dq, layer->dk, layer->dv, pv_bits, st), "k1 launch");
+        layer->last_v_bits = pv_bits;
+        run_attention(layer, st, scale, pv_bits, layer->dout, zeroed ? layer->dzero : nullptr);
+        cuda_check(cudaMemcpyAsync(out, layer->dout, elems * 4, cudaMemcpyDeviceToHost, st), "D2H out");
+        if (zeroed)
+            cuda_check(cudaMemcpyAsync(zeroed, layer->dzero, (size_t)L.H * L.N, cudaMemcpyDeviceToHost, st), "D2H zeroed");
+        cuda_check(cudaStreamSynchronize(st), "forward_host sync");
+        layer->last_launches = 2;
+    });
+}
+
+int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out) {
+    return guarded([&] {
+        check_layer(layer);
+        const LayerDev& L = layer->L;
+        out->heads = L.H;
+        out->tokens = L.N;
+        out->head_dim = L.D;
+        out->kblocks = L.kb;
+        out->kblocks_padded = L.kb2;
+        out->groups = L.G;
+        out->q_codes = L.q;
+        out->k_codes = L.k;
+        out->v_codes = L.v;
+        out->q_scales = L.qsc;
+        out->tile_meta = L.meta;
+        out->inverse = layer->inv;
+        out->forward = layer->fwd;
+    });
+}
+
+int paro_layer_mask_stats(paro_layer* layer, uint32_t* kept_per_qblock, uint64_t* total_kept) {
+    return guarded([&] {
+        check_layer(layer);
+        if (!layer->masks_set)
+            fail(PARO_E_CONFIG, "masks not set");
+        set_device(layer->ctx);
+        const LayerDev& L = layer->L;
+        std::vector<uint32_t> buf((size_t)L.H * L.kb2);
+        cuda_check(cudaMemcpy(buf.data(), L.qb_count, buf.size() * 4, cudaMemcpyDeviceToHost), "D2H qb_count");
+        uint64_t tot = 0;
+        for (uint32_t h = 0; h < L.H; ++h)
+            for (uint32_t b = 0; b < L.kb; ++b) {
+                const uint32_t c = buf[(size_t)h * L.kb2 + b];
+                tot += c;
+                if (kept_per_qblock)
+                    kept_per_qblock[(size_t)h * L.kb + b] = c;
+            }
+        if (total_kept)
+            *total_kept = tot;
+    });
+}
+
+int paro_layer_debug_qk(paro_layer* layer, paro_stream_t stream, uint32_t n_tiles, const uint32_t* tiles, int32_t* S) {
+    return guarded([&] {
+        check_layer(layer);
+        set_device(layer->ctx);
+        cuda_check(paro::launch_debug_qk(layer->L, layer->tm_q, layer->tm_k, n_tiles, tiles, S, (cudaStream_t)stream),
+                   "debug_qk launch");
+    });
+}
+
+int paro_layer_last_launches(const paro_layer* layer, int* kernels) {
+    return guarded([&] { *kernels = layer->last_launches; });
+}
+
+} // extern "C"

@@ -1,0 +1,57 @@
+// layer.cuh -- HBM layout shared by the host orchestration and the kernels.
+//
+// All per-layer device state for H heads of N tokens, head dim D in {64,128},
+// block 64, kb = ceil(N/64) key/query blocks, kb2 = kb rounded up to even (q
+// blocks are processed in pairs, A = 2p and B = 2p+1, so K3 can run M = 128
+// tcgen05 MMAs over the union of the pair's kept key blocks).
+//
+//   codes  q/k/v  int8 [H][kb2*64][D]  PERMUTED token order, zero-padded rows
+//   qsc          fp32 [H][kb2][G]     Q scale per (block, 64-column group), G = D/64
+//   meta         fp32 [H][kb2][4 + D] per key block: {ksc[0], ksc[1], vsc, 0, colsum[D]}
+//                                      (colsum = sum of V codes per column, exact in fp32)
+//   perm         PermDesc [H]          permuted index -> original token (div/mod form)
+//   items        u16  [H][np][kb]       per q-block pair: union of kept key blocks,
+//                                      bits 0..13 = key block, bit 14 = A keeps, bit 15 = B keeps
+//   pair_count   u32  [H][np]          entries used in items
+//   qb_count     u32  [H][kb2]         kept key blocks per q block (0 => zeroed rows)
+//   order        u32  [H*np]           work items (h << 16 | p), longest first (LPT)
+#pragma once
+#include <cstdint>
+
+namespace paro {
+
+constexpr int kBlock = 64;
+
+// Permuted index i -> original token: decompose i row-major over the permuted
+// extents (pext), then recombine with the original strides of those axes.
+// Equals PermPlan::inverse[i] of make_perm (reorder.cpp:49-72). 2-D grids use
+// pext[0] = 1, ostride[0] = 0.
+struct PermDesc {
+    uint32_t pext[3];
+    uint32_t ostride[3];
+};
+
+__host__ __device__ inline uint32_t perm_src(const PermDesc& pd, uint32_t i) {
+    const uint32_t c2 = i % pd.pext[2];
+    const uint32_t t = i / pd.pext[2];
+    const uint32_t c1 = t % pd.pext[1];
+    const uint32_t c0 = t / pd.pext[1];
+    return c0 * pd.ostride[0] + c1 * pd.ostride[1] + c2 * pd.ostride[2];
+}
+
+struct LayerDev {
+    uint32_t H, N, D, G, kb, kb2, np;
+    PermDesc* perm;
+    int8_t *q, *k, *v;
+    float* qsc;
+    float* meta;
+    uint16_t* items;
+    uint32_t* pair_count;
+    uint32_t* qb_count;
+    uint32_t* order;
+    uint32_t* work_counter;
+};
+
+__host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }
+
+} // namespace paro

@@ -1,0 +1,412 @@
+// prep_kernels.cu -- K1 (PARO reorder gather + per-block quantization), K2
+// (block mask -> per q-block-pair kept lists + LPT work order) and the small
+// standalone stages (device permutation tables, apply_perm_rows, quantize).
+//
+// K1 is HBM-bound: per head it reads 3*N*D*4 bytes of fp32 Q/K/V once and
+// writes 3*N*D bytes of int8 codes plus per-block scales/colsums. One CTA
+// owns one 64-token block (permuted order) of one head for all three tensors;
+// each thread issues all its 16-byte gather loads up front (MLP) before the
+// block reductions. The quantizer arithmetic is IEEE-exact (this TU is built
+// with -fmad=false, explicit __fdiv_rn) so codes/scales are bit-identical to
+// quantize() / the engine's V tile quantizer.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layer.cuh"
+
+namespace paro {
+
+// ---------------------------------------------------------------------------
+// quant_affine(x, 0, scale, -qmax, qmax) of kernels_scalar.cpp:78-85:
+// (x - 0)/scale in IEEE fp32, clamp to [-qmax, qmax] BEFORE rounding, round
+// half away from zero (std::round). x - 0.0f == x for every finite x.
+__device__ __forceinline__ int quant_sym(float x, float scale, float qmax) {
+    float q = __fdiv_rn(x, scale);
+    q = fminf(qmax, fmaxf(-qmax, q));
+    float t = truncf(q);
+    if (fabsf(__fsub_rn(q, t)) >= 0.5f)
+        t = __fadd_rn(t, copysignf(1.0f, q));
+    return static_cast<int>(t);
+}
+
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float amax4(float4 v) {
+    return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+    return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+           ((uint32_t)(d & 0xff) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// K1. grid (kb2, H), 256 threads. D/4 threads cover one row (float4 each);
+// a pass covers 256/(D/4) rows, PASSES passes cover the 64-row block.
+//   Q, K: quantize(.., {8, Symmetric, PerBlock, 64}) (quant.cpp:60-104): one
+//         group per 64x64 tile, scale = amax/127 (0 -> 1).
+//   V   : engine V-tile quantizer (attention.cpp:104-126): one group per key
+//         block over all D columns, scale = amax==0 ? 1 : amax/qmax, colsum.
+// Rows i >= N (block padding) read as zero and write zero codes; an all-zero
+// row never changes amax (max starts at 0) or colsum, so groups keep the
+// reference's true-extent semantics.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const float* __restrict__ q,
+                                                           const float* __restrict__ k, const float* __restrict__ v,
+                                                           int v_bits) {
+    constexpr int F4 = D / 4;        // float4 per row
+    constexpr int RPP = 256 / F4;    // rows per pass
+    constexpr int PASSES = 64 / RPP; // 4 (D=64) or 8 (D=128)
+    constexpr int G = D / 64;
+    const uint32_t b = blockIdx.x, h = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c4 = tid % F4;
+    const int r0 = tid / F4;
+    const int grp = (c4 * 4) / 64;
+
+    __shared__ float s_amax[3][8][2];
+    __shared__ int s_colsum[8][D];
+
+    const PermDesc pd = L.perm[h];
+    const size_t head_in = (size_t)h * L.N * D;
+    float4 xq[PASSES], xk[PASSES], xv[PASSES];
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const uint32_t i = b * 64 + r0 + RPP * j;
+        if (i < L.N) {
+            const size_t off = head_in + (size_t)perm_src(pd, i) * D + c4 * 4;
+            xq[j] = ld_stream(q + off);
+            xk[j] = ld_stream(k + off);
+            xv[j] = ld_stream(v + off);
+        } else {
+            xq[j] = xk[j] = xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+
+    // per-thread amax: Q/K per column group, V over everything
+    float aq = 0.f, ak = 0.f, av = 0.f;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        aq = fmaxf(aq, amax4(xq[j]));
+        ak = fmaxf(ak, amax4(xk[j]));
+        av = fmaxf(av, amax4(xv[j]));
+    }
+    // warp reduce. D=64: the whole warp is one group. D=128: lanes 0-15 are
+    // group 0, 16-31 group 1 (one row per warp) -> reduce within 16 lanes.
+#pragma unroll
+    for (int o = (G == 2 ? 8 : 16); o > 0; o >>= 1) {
+        aq = fmaxf(aq, __shfl_xor_sync(0xffffffffu, aq, o));
+        ak = fmaxf(ak, __shfl_xor_sync(0xffffffffu, ak, o));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, o));
+    if (lane == 0 || (G == 2 && lane == 16)) {
+        const int g = (G == 2 && lane == 16) ? 1 : 0;
+        s_amax[0][warp][g] = aq;
+        s_amax[1][warp][g] = ak;
+        if (g == 0)
+            s_amax[2][warp][0] = av;
+    }
+    __syncthreads();
+    float gq = 0.f, gk = 0.f, gv = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        gq = fmaxf(gq, s_amax[0][w][grp]);
+        gk = fmaxf(gk, s_amax[1][w][grp]);
+        gv = fmaxf(gv, s_amax[2][w][0]);
+    }
+    float sq = __fdiv_rn(gq, 127.0f);
+    if (sq == 0.0f)
+        sq = 1.0f;
+    float sk = __fdiv_rn(gk, 127.0f);
+    if (sk == 0.0f)
+        sk = 1.0f;
+    const float vq = v_bits == 4 ? 7.0f : 127.0f;
+    const float sv = gv == 0.0f ? 1.0f : __fdiv_rn(gv, vq);
+
+    const size_t head_codes = (size_t)h * L.kb2 * 64 * D;
+    int cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const size_t off = head_codes + (size_t)(b * 64 + r0 + RPP * j) * D + c4 * 4;
+        const float4 a = xq[j], c = xk[j], e = xv[j];
+        *reinterpret_cast<uint32_t*>(L.q + off) =
+            pack4(quant_sym(a.x, sq, 127.f), quant_sym(a.y, sq, 127.f), quant_sym(a.z, sq, 127.f),
+                  quant_sym(a.w, sq, 127.f));
+        *reinterpret_cast<uint32_t*>(L.k + off) =
+            pack4(quant_sym(c.x, sk, 127.f), quant_sym(c.y, sk, 127.f), quant_sym(c.z, sk, 127.f),
+                  quant_sym(c.w, sk, 127.f));
+        const int v0 = quant_sym(e.x, sv, vq), v1 = quant_sym(e.y, sv, vq), v2 = quant_sym(e.z, sv, vq),
+                  v3 = quant_sym(e.w, sv, vq);
+        *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
+        cs0 += v0;
+        cs1 += v1;
+        cs2 += v2;
+        cs3 += v3;
+    }
+    if (G == 1) { // lanes l and l^16 hold the same columns
+        cs0 += __shfl_xor_sync(0xffffffffu, cs0, 16);
+        cs1 += __shfl_xor_sync(0xffffffffu, cs1, 16);
+        cs2 += __shfl_xor_sync(0xffffffffu, cs2, 16);
+        cs3 += __shfl_xor_sync(0xffffffffu, cs3, 16);
+    }
+    if (G == 2 || lane < 16) {
+        s_colsum[warp][c4 * 4 + 0] = cs0;
+        s_colsum[warp][c4 * 4 + 1] = cs1;
+        s_colsum[warp][c4 * 4 + 2] = cs2;
+        s_colsum[warp][c4 * 4 + 3] = cs3;
+    }
+    __syncthreads();
+    float* meta = L.meta + ((size_t)h * L.kb2 + b) * meta_stride(D);
+    if (tid < D) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+            s += s_colsum[w][tid];
+        meta[4 + tid] = (float)s;
+    }
+    if (tid == 0) {
+        meta[0] = sk;
+        meta[2] = sv;
+        meta[3] = 0.f;
+        L.qsc[((size_t)h * L.kb2 + b) * G + 0] = sq;
+    }
+    if (tid == F4 - 1) { // a thread of the last column group
+        if (G == 2) {
+            meta[1] = sk;
+            L.qsc[((size_t)h * L.kb2 + b) * G + 1] = sq;
+        } else {
+            meta[1] = 0.f;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Standalone quantize(m, {bits, Symmetric, PerBlock, 64}) for cols in {64,128}
+// (same arithmetic as K1's Q/K path, identity row order).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_quantize_sym(const float* __restrict__ in, uint32_t rows, int bits,
+                                                      int8_t* __restrict__ codes, float* __restrict__ scales) {
+    constexpr int F4 = D / 4, RPP = 256 / F4, PASSES = 64 / RPP, G = D / 64;
+    const uint32_t b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c4 = tid % F4, r0 = tid / F4, grp = (c4 * 4) / 64;
+    __shared__ float s_amax[8][2];
+    float4 x[PASSES];
+    float a = 0.f;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const uint32_t i = b * 64 + r0 + RPP * j;
+        x[j] = i < rows ? ld_stream(in + (size_t)i * D + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        a = fmaxf(a, amax4(x[j]));
+    }
+#pragma unroll
+    for (int o = (G == 2 ? 8 : 16); o > 0; o >>= 1)
+        a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0 || (G == 2 && lane == 16))
+        s_amax[warp][(G == 2 && lane == 16) ? 1 : 0] = a;
+    __syncthreads();
+    float g = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+        g = fmaxf(g, s_amax[w][grp]);
+    const float qmax = bits == 4 ? 7.0f : 127.0f;
+    float s = __fdiv_rn(g, qmax);
+    if (s == 0.0f)
+        s = 1.0f;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const uint32_t i = b * 64 + r0 + RPP * j;
+        if (i < rows)
+            *reinterpret_cast<uint32_t*>(codes + (size_t)i * D + c4 * 4) =
+                pack4(quant_sym(x[j].x, s, qmax), quant_sym(x[j].y, s, qmax), quant_sym(x[j].z, s, qmax),
+                      quant_sym(x[j].w, s, qmax));
+    }
+    if (tid == 0)
+        scales[(size_t)b * G] = s;
+    if (G == 2 && tid == F4 - 1)
+        scales[(size_t)b * G + 1] = s;
+}
+
+// apply_perm_rows: out.row(i) = in.row(inverse[i]) (reorder.cpp:93-101)
+__global__ void k_apply_perm_rows(const float* __restrict__ in, uint32_t rows, uint32_t cols,
+                                  const uint32_t* __restrict__ inverse, float* __restrict__ out) {
+    const uint32_t i = blockIdx.x;
+    if (i >= rows)
+        return;
+    const float* src = in + (size_t)inverse[i] * cols;
+    float* dst = out + (size_t)i * cols;
+    for (uint32_t c = threadIdx.x; c < cols; c += blockDim.x)
+        dst[c] = src[c];
+}
+
+// device permutation tables from the per-head descriptors (bit-exact with make_perm)
+__global__ void k_perm_tables(const PermDesc* __restrict__ perm, uint32_t H, uint32_t N, uint32_t* __restrict__ fwd,
+                              uint32_t* __restrict__ inv) {
+    const uint32_t h = blockIdx.y;
+    const PermDesc pd = perm[h];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const uint32_t old = perm_src(pd, i);
+        inv[(size_t)h * N + i] = old;
+        fwd[(size_t)h * N + old] = i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2a. One CTA (128 threads) per (head, q-block pair). Walks the two mask rows
+// (BlockMask::bits, one byte per block, mask.hpp:15-32) and writes the union of
+// kept key blocks in ascending order with per-q-block keep flags; also the
+// per-q-block kept counts (a row block with 0 kept blocks is zeroed and
+// flagged, attention.cpp:242-247). bits == nullptr means all blocks kept.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k2_pair_lists(LayerDev L, const uint8_t* __restrict__ bits) {
+    const uint32_t p = blockIdx.x, h = blockIdx.y;
+    const uint32_t A = 2 * p, B = 2 * p + 1;
+    const bool hasB = B < L.kb;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ uint32_t s_warp[4][3];
+    __shared__ uint32_t s_base[3];
+    if (tid == 0)
+        s_base[0] = s_base[1] = s_base[2] = 0;
+    __syncthreads();
+    const uint8_t* rowA = bits ? bits + ((size_t)h * L.kb + A) * L.kb : nullptr;
+    const uint8_t* rowB = (bits && hasB) ? bits + ((size_t)h * L.kb + B) * L.kb : nullptr;
+    uint16_t* out = L.items + ((size_t)h * L.np + p) * L.kb;
+    for (uint32_t c0 = 0; c0 < L.kb; c0 += 128) {
+        const uint32_t j = c0 + tid;
+        bool a = false, bb = false;
+        if (j < L.kb) {
+            a = rowA ? rowA[j] != 0 : true;
+            bb = hasB ? (rowB ? rowB[j] != 0 : true) : false;
+        }
+        const bool any = a || bb;
+        const uint32_t mu = __ballot_sync(0xffffffffu, any);
+        const uint32_t ma = __ballot_sync(0xffffffffu, a);
+        const uint32_t mb = __ballot_sync(0xffffffffu, bb);
+        if (lane == 0) {
+            s_warp[warp][0] = __popc(mu);
+            s_warp[warp][1] = __popc(ma);
+            s_warp[warp][2] = __popc(mb);
+        }
+        __syncthreads();
+        uint32_t off = s_base[0];
+        for (int w = 0; w < warp; ++w)
+            off += s_warp[w][0];
+        if (any) {
+            const uint32_t pos = off + __popc(mu & ((1u << lane) - 1u));
+            out[pos] = (uint16_t)(j | (a ? 0x4000u : 0u) | (bb ? 0x8000u : 0u));
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 0; w < 4; ++w) {
+                s_base[0] += s_warp[w][0];
+                s_base[1] += s_warp[w][1];
+                s_base[2] += s_warp[w][2];
+            }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        L.pair_count[(size_t)h * L.np + p] = s_base[0];
+        L.qb_count[(size_t)h * L.kb2 + A] = s_base[1];
+        L.qb_count[(size_t)h * L.kb2 + B] = s_base[2];
+    }
+}
+
+// K2b. Single CTA: counting sort of the H*np work items by union length,
+// longest first (LPT order for K3's cyclic distribution). Ties are ordered
+// by (h, p) via a stable in-bucket rank, so the order is deterministic.
+__global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
+    extern __shared__ uint32_t s_hist[]; // kb + 1 buckets
+    const uint32_t total = L.H * L.np;
+    for (uint32_t i = threadIdx.x; i <= L.kb; i += blockDim.x)
+        s_hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x)
+        atomicAdd(&s_hist[L.pair_count[i]], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) { // exclusive offsets, descending key
+        uint32_t run = 0;
+        for (int key = (int)L.kb; key >= 0; --key) {
+            const uint32_t c = s_hist[key];
+            s_hist[key] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // stable placement by one warp walking the items in (h, p) order
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t i = base + lane;
+            const bool valid = i < total;
+            const uint32_t key = valid ? L.pair_count[i] : 0xffffffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+            const uint32_t pos = valid ? s_hist[key] + rank : 0;
+            __syncwarp();
+            if (valid && lane == (uint32_t)(__ffs(peers) - 1))
+                s_hist[key] += __popc(peers);
+            __syncwarp();
+            if (valid)
+                L.order[pos] = ((i / L.np) << 16) | (i % L.np);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits,
+                      cudaStream_t st) {
+    dim3 grid(L.kb2, L.H);
+    if (L.D == 64)
+        k1_reorder_quantize<64><<<grid, 256, 0, st>>>(L, q, k, v, v_bits);
+    else
+        k1_reorder_quantize<128><<<grid, 256, 0, st>>>(L, q, k, v, v_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_sym(const float* in, uint32_t rows, uint32_t cols, int bits, int8_t* codes,
+                                float* scales, cudaStream_t st) {
+    const uint32_t nb = (rows + 63) / 64;
+    if (cols == 64)
+        k_quantize_sym<64><<<nb, 256, 0, st>>>(in, rows, bits, codes, scales);
+    else
+        k_quantize_sym<128><<<nb, 256, 0, st>>>(in, rows, bits, codes, scales);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_perm_rows(const float* in, uint32_t rows, uint32_t cols, const uint32_t* inverse, float* out,
+                                   cudaStream_t st) {
+    k_apply_perm_rows<<<rows, 128, 0, st>>>(in, rows, cols, inverse, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uint32_t* fwd, uint32_t* inv,
+                               cudaStream_t st) {
+    dim3 grid((N + 255) / 256, H);
+    k_perm_tables<<<grid, 256, 0, st>>>(perm, H, N, fwd, inv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
+    dim3 grid(L.np, L.H);
+    k2_pair_lists<<<grid, 128, 0, st>>>(L, bits);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return e;
+    k2_work_order<<<1, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    return cudaGetLastError();
+}
+
+} // namespace paro
