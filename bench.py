@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py -- PARO sparse-quantized attention layer on B200 (BASELINE.json metric).
+
+Metric: "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)".
+  value        = effective TOPS over the whole job (all ranks): algorithmic ops of
+                 the kept tiles (4*d*rows*cols per kept 64x64 block, padding
+                 excluded) / max-over-ranks device time of one layer step.
+  ms_per_step  = ms/layer.
+A step = one pass of the hot path over one layer: K2 (mask -> kept lists, masks
+resident in HBM) + K1 (PARO gather + Q/K/V quantize) + K3 (block-sparse INT8
+attention + inverse permute). Heads are sharded across ranks (no collective on
+the data path; "scaling": "strong" -- the layer is fixed, ranks split heads).
+e2e: the same metric through the C-ABI host call paro_layer_forward_host (pinned
+host Q/K/V in, O out; H2D/D2H inside the timed region).
+
+--impl reference: the reference's own CPU implementation of the path
+(quantized_blocked_attention + permutes, compiled from the reference sources into
+oracle/_ref) on the host cores, bounded sample of heads, same metric.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (grid, heads, d, density, pv_bits, description)
+    "c1": ("F:2,H:8,W:8", 2, 64, 0.3, 8, "small synthetic F2xH8xW8, 2 heads, d=64, 30% (block 64 -> 50%), INT8/INT8"),
+    "c2": ("F:13,H:30,W:45", 48, 64, 0.3, 8, "CogVideoX-5B N=17550 (13x30x45), 48 heads, d=64, density 0.3, INT8 QK / INT8 PV"),
+    "c3": ("F:13,H:30,W:45", 48, 64, 0.2, 4, "CogVideoX-5B N=17550, 48 heads, d=64, density 0.2, INT8 QK / INT4 PV"),
+    "c4": ("H:64,W:64", 24, 128, 0.3, 8, "Flux.1-dev N=4096 (64x64), 24 heads, d=128, density 0.3, INT8/INT8"),
+    "c4i4": ("H:64,W:64", 24, 128, 0.3, 4, "Flux.1-dev N=4096 (64x64), 24 heads, d=128, density 0.3, INT8/INT4"),
+    "c5": ("F:21,H:45,W:80", 40, 128, 0.2, 4, "Wan-2.1-14B N=75600 (21x45x80), 40 heads, d=128, density 0.2, INT8 QK / INT4 PV"),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / baseline / clocks)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workload
+def head_orders(paro, grid, heads):
+    """Per-head order = enumerate_perms(grid)[head % ndim!]."""
+    orders = paro.enumerate_orders(grid)
+    return [orders[h % len(orders)] for h in range(heads)]
+
+
+def head_inputs(paro, h, N, d):
+    """Seeded N(0,1): MT19937-64 + Box-Muller, seed 1000 + 3*head + {0,1,2}."""
+    return [paro.synth_randn(1000 + 3 * h + i, N * d).reshape(N, d) for i in range(3)]
+
+
+def head_mask(paro, h, kb, density, family):
+    rng = np.random.default_rng(7919 * (h + 1))
+    if family == "random":  # M1: U[0,1) + 2*I (test_mask.cpp:28-37 shape)
+        sums = rng.random((kb, kb)) + 2.0 * np.eye(kb)
+    else:  # M2: exp(-|i-j|/w) + 0.05*U, w = density*k/2
+        w = max(density * kb / 2.0, 1.0)
+        i = np.arange(kb)
+        sums = np.exp(-np.abs(i[:, None] - i[None, :]) / w) + 0.05 * rng.random((kb, kb))
+    return paro.gen_mask(sums, density, 64)[0].bits
+
+
+def kept_ops(mask, N, d):
+    """4*d*sum over kept blocks of true rows x true cols."""
+    kb = mask.shape[0]
+    ext = np.full(kb, 64, np.int64)
+    ext[-1] = N - 64 * (kb - 1)
+    return int(4 * d * (ext[:, None] * ext[None, :] * (mask != 0)).sum())
+
+
+def build_inputs(paro, heads, N, d, density, family, threads=8):
+    from concurrent.futures import ThreadPoolExecutor
+
+    kb = (N + 63) // 64
+    q = np.empty((len(heads), N, d), np.float32)
+    k = np.empty_like(q)
+    v = np.empty_like(q)
+    masks = np.empty((len(heads), kb, kb), np.uint8)
+
+    def one(i):
+        h = heads[i]
+        q[i], k[i], v[i] = head_inputs(paro, h, N, d)
+        masks[i] = head_mask(paro, h, kb, density, family)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(len(heads))))
+    return q, k, v, masks
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), float(mp["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- CPU baseline (reference)
+def cpu_reference_sample(cfg_name, threads, max_heads=None):
+    """The reference's own CPU chain (oracle/_ref) on a bounded sample of heads."""
+    from oracle.pyoracle import Reference, have_reference
+
+    import paro_b200 as paro
+
+    if not have_reference():
+        return None
+    grid_text, H, d, density, bits, _ = CONFIGS[cfg_name]
+    g = paro.parse_grid(grid_text)
+    N = g.token_count()
+    ref = Reference()
+    ref.select_kernels("auto")
+    threads = threads or os.cpu_count() or 1
+    # bounded sample: about one head per thread, sized for ~10-30 s of CPU work
+    per_head_ops = None
+    n_run = min(H, max_heads or threads)
+    heads = list(range(n_run))
+    q, k, v, masks = build_inputs(paro, heads, N, d, density, "random")
+    orders = head_orders(paro, g, H)[:n_run]
+    _, secs = ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
+    ops = sum(kept_ops(masks[i], N, d) for i in range(n_run))
+    per_head_ops = ops / n_run
+    return {
+        "value": ops / secs / 1e12,
+        "unit": "TOPS",
+        "cores": threads,
+        "kind": "reference",
+        "sample": f"{n_run} of {H} heads ({cfg_name}) on {threads} threads, {secs:.1f} s wall; "
+                  f"layer time extrapolated {H * per_head_ops / (ops / secs):.1f} s",
+        "seconds": secs,
+        "layer_seconds_extrapolated": H * per_head_ops / (ops / secs),
+    }
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    grid_text, H, d, density, pv_bits, desc = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_sample(args.config, args.cpu_threads, None)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparo_ref.so not built"}))
+            return
+        line = {
+            "impl": "reference", "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
+            "value": r["value"], "unit": "TOPS", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "ms_per_step": r["layer_seconds_extrapolated"] * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp64 QK / int8 P,V (reference CPU semantics)", "data": "synthetic",
+            "config": {"workload": desc, "heads": H, "grid": grid_text, "head_dim": d, "density": density,
+                       "pv_bits": pv_bits, "mask_family": "random"},
+            "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    import paro_b200 as paro
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ctx = paro.Context(local_rank)
+    g = paro.parse_grid(grid_text)
+    N = g.token_count()
+    kb = (N + 63) // 64
+    if H % world:
+        raise SystemExit(f"{H} heads do not split over {world} ranks")
+    hpr = H // world
+    my_heads = list(range(rank * hpr, (rank + 1) * hpr))
+    orders_all = head_orders(paro, g, H)
+    q, k, v, masks = build_inputs(paro, my_heads, N, d, density, args.mask_family)
+    my_ops = sum(kept_ops(masks[i], N, d) for i in range(hpr))
+    total_ops = my_ops
+    if dist:
+        t = torch.tensor([my_ops], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        total_ops = float(t.item())
+
+    layer = paro.Layer(ctx, hpr, d, g, [orders_all[h] for h in my_heads])
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    dq = torch.from_numpy(q).cuda()
+    dk = torch.from_numpy(k).cuda()
+    dv = torch.from_numpy(v).cuda()
+    dmask = torch.from_numpy(masks).cuda()
+    dout = torch.empty_like(dq)
+    dzero = torch.empty((hpr, N), dtype=torch.uint8, device="cuda")
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(events=None):
+        if events:
+            events[0].record(stream)
+        layer.set_masks_device(dmask.data_ptr(), sp)
+        if events:
+            events[1].record(stream)
+        layer.reorder_quantize(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), pv_bits, sp)
+        if events:
+            events[2].record(stream)
+        layer.attention(0.0, pv_bits, dout.data_ptr(), dzero.data_ptr(), sp)
+        if events:
+            events[3].record(stream)
+
+    for _ in range(max(args.warmup, 3 if not args.profile else 1)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.2)
+    # timed region: K steps, barrier + synchronize on both sides, per-kernel events
+    per = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = ev(), ev()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(per[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    k2_ms = sum(e[0].elapsed_time(e[1]) for e in per) / args.steps
+    k1_ms = sum(e[1].elapsed_time(e[2]) for e in per) / args.steps
+    k3_ms = sum(e[2].elapsed_time(e[3]) for e in per) / args.steps
+    ms_step = ms_total / args.steps
+    if dist:
+        t = torch.tensor([ms_step, k1_ms, k2_ms, k3_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, k1_ms, k2_ms, k3_ms = [float(x) for x in t.tolist()]
+    clk = clocks.stop() if not args.profile else None
+
+    # e2e through the public C-ABI host call (pinned host buffers)
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        hq, hk, hv = (paro.HostBuffer(q.shape, np.float32) for _ in range(3))
+        hq.array[...] = q
+        hk.array[...] = k
+        hv.array[...] = v
+        hout = paro.HostBuffer(q.shape, np.float32)
+        hz = paro.HostBuffer((hpr, N), np.uint8)
+        layer.set_masks_device(dmask.data_ptr(), sp)
+        for _ in range(2):
+            layer.forward_host(hq.array, hk.array, hv.array, 0.0, pv_bits, hout.array, hz.array, sp)
+        e_steps = max(3, min(args.steps, 10))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(e_steps):
+            layer.set_masks_device(dmask.data_ptr(), sp)
+            layer.forward_host(hq.array, hk.array, hv.array, 0.0, pv_bits, hout.array, hz.array, sp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / e_steps
+        if dist:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": total_ops / (e_ms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_layer": e_ms,
+               "h2d_bytes_per_step": int(3 * q.nbytes) * world, "d2h_bytes_per_step": int(q.nbytes + hz.array.nbytes) * world}
+
+    # rooflines (rank-0 numbers; per launch = per layer shard)
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    int8_peak = 2.0 * bf16_peak  # kind::i8 issues at 2x the kind::f16 rate on tcgen05
+    k3_tops = my_ops / (k3_ms * 1e-3) / 1e12
+    k1_bytes = hpr * (3 * N * d * 4 + 3 * kb * 64 * d + kb * (4 + d) * 4 + kb * 4 * (d // 64))
+    k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
+    density_kept = float(np.mean([m.mean() for m in masks]))
+
+    line = {
+        "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
+        "value": total_ops / (ms_step * 1e-3) / 1e12,
+        "unit": "TOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int8 (QK s8*s8->s32, PV u8*s8->s32 on tcgen05; fp32 softmax/dequant)",
+        "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), gen_mask masks",
+        "config": {
+            "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
+            "kept_density": round(density_kept, 5), "pv_bits": pv_bits, "mask_family": args.mask_family,
+            "parallelism": f"head-shard x{world} (no data-path collective)",
+            "l2": f"inputs {3 * q.nbytes * world / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
+        },
+        "ms_per_layer": ms_step,
+        "kernels_ms": {"k2_mask_lists": k2_ms, "k1_reorder_quantize": k1_ms, "k3_attention": k3_ms},
+        "roofline": {
+            "bound": "tensor", "kernel": "k3_attention", "achieved": k3_tops, "peak": int8_peak, "unit": "TOPS",
+            "frac": k3_tops / int8_peak, "traffic": None,
+            "peak_source": f"2x bf16_tflops {bf16_peak} ({peak_src}, MEASURED_PEAKS.json): dense INT8 tcgen05 rate",
+            "algorithmic_ops_per_launch": my_ops,
+        },
+        "roofline_k1": {"bound": "hbm", "kernel": "k1_reorder_quantize", "achieved": k1_gbs, "peak": hbm_peak,
+                        "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        try:
+            cb = cpu_reference_sample(args.config, args.cpu_threads)
+        except Exception as ex:  # the baseline must not kill the bench line
+            cb = {"error": str(ex)}
+        if cb is not None:
+            line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample") if k_ in cb} \
+                if "error" not in cb else cb
+    if rank == 0:
+        print(json.dumps(line))
+    layer.close()
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -215,9 +215,11 @@ static double dot_f(const float* a, const float* b, size_t n) {
     return acc;
 }
 
-int oracle_stream_engine(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
-                         size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode, float* out,
-                         uint8_t* zeroed) {
+/* Rows of q-blocks [qb_begin, qb_end) only (the engine is independent per
+ * q-tile, attention.cpp:134); other output rows are left untouched. */
+int oracle_stream_engine_range(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
+                               size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode,
+                               size_t qb_begin, size_t qb_end, float* out, uint8_t* zeroed) {
     if (n == 0 || d == 0 || block < 1)
         return ORACLE_CONFIG;
     if (dense_prefix > n)
@@ -257,9 +259,7 @@ int oracle_stream_engine(const float* q, const float* k, const float* v, size_t 
     double* s = (double*)malloc(block * block * sizeof(double));
     float* ptile = (float*)malloc(block * block * sizeof(float));
     int32_t* pcodes = (int32_t*)malloc(block * sizeof(int32_t));
-    memset(zeroed, 0, n);
-
-    for (size_t qs0 = 0; qs0 < n; qs0 += block) {
+    for (size_t qs0 = qb_begin * block; qs0 < n && qs0 < qb_end * block; qs0 += block) {
         const size_t qe = qs0 + block < n ? qs0 + block : n;
         const size_t qn = qe - qs0;
         const size_t qb = qs0 / block;
@@ -368,6 +368,7 @@ int oracle_stream_engine(const float* q, const float* k, const float* v, size_t 
         }
         for (size_t r = 0; r < qn; ++r) {
             float* o = out + (qs0 + r) * d;
+            zeroed[qs0 + r] = 0;
             if (row_sum[r] == 0.0) {
                 zeroed[qs0 + r] = 1;
                 memset(o, 0, d * sizeof(float));
@@ -391,6 +392,13 @@ int oracle_stream_engine(const float* q, const float* k, const float* v, size_t 
     free(vscale);
     free(vcolsum);
     return ORACLE_OK;
+}
+
+int oracle_stream_engine(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
+                         size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode, float* out,
+                         uint8_t* zeroed) {
+    return oracle_stream_engine_range(q, k, v, n, d, scale_in, dense_prefix, block, mask, pv_bits, qk_mode, 0,
+                                      (n + block - 1) / block, out, zeroed);
 }
 
 /* ------------------------------------------------------------------------- */

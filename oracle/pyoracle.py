@@ -104,6 +104,26 @@ class Oracle:
             raise ValueError(f"oracle_stream_engine rc={rc}")
         return out, zeroed.astype(bool)
 
+    def stream_engine_range(self, q, k, v, qb_begin, qb_end, mask=None, pv_bits=8, qk_mode=1, scale=0.0):
+        """Engine output rows of q-blocks [qb_begin, qb_end) only (rows [qb_begin*64, ...))."""
+        q = np.ascontiguousarray(q, np.float32)
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        n, d = q.shape
+        out = np.zeros((n, d), np.float32)
+        zeroed = np.zeros(n, np.uint8)
+        mp = None
+        if mask is not None:
+            mask = np.ascontiguousarray(mask, np.uint8)
+            mp = _ptr(mask)
+        rc = self.lib.oracle_stream_engine_range(_ptr(q), _ptr(k), _ptr(v), SZ(n), SZ(d), ctypes.c_float(scale), SZ(0),
+                                                 SZ(64), mp, ctypes.c_int(pv_bits), ctypes.c_int(qk_mode),
+                                                 SZ(qb_begin), SZ(qb_end), _ptr(out), _ptr(zeroed))
+        if rc:
+            raise ValueError(f"oracle_stream_engine_range rc={rc}")
+        r0, r1 = qb_begin * 64, min(n, qb_end * 64)
+        return out[r0:r1], zeroed[r0:r1].astype(bool)
+
     def paro_head(self, q, k, v, fwd, inv, mask=None, pv_bits=8, qk_mode=1, scale=0.0):
         """cmd_run's chain for one head (main.cpp:276-305). zeroed in PERMUTED order."""
         q = np.ascontiguousarray(q, np.float32)

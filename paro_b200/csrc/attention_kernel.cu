@@ -293,54 +293,84 @@ __global__ void __launch_bounds__(320, 1)
                     ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
                     ptx::tc_fence_after();
                     const float* meta = reinterpret_cast<const float*>(smem + C::OFF_META + s * C::META_BYTES);
+                    const bool is_tail = (tail != 0) && (bj == L.kb - 1);
+                    // y[j] <- log2-domain argument p_j = 2^y[j], computed so that the only
+                    // roundings are the fp32 scale and one FMA (P codes are sensitive to
+                    // relative errors in p: SURVEY Appendix A.4)
                     float y[64];
-                    {
-                        uint32_t raw[32];
-                        // group 0
-                        float c0 = __uint_as_float(__float_as_uint(cq[0] * meta[0]) & 0xFFFFFFFCu);
-                        float b0 = -12582912.0f * c0;
+                    float m_new, gamma;
+                    if (G == 1) {
+                        const float c0 = cq[0] * meta[0];
+                        int32_t sraw[64];
 #pragma unroll
                         for (int h2 = 0; h2 < 2; ++h2) {
+                            uint32_t raw[32];
                             ptx::tmem_ld32(tmem + lane_base + C::TM_S + b * C::S_COLS + h2 * 32, raw);
                             ptx::tmem_ld_wait();
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
-                                y[h2 * 32 + j] = fmaf(i2f_magic(raw[j]), c0, b0);
+                                sraw[h2 * 32 + j] = (int32_t)raw[j];
                         }
-                        if (G == 2) {
-                            float c1 = __uint_as_float(__float_as_uint(cq[G - 1] * meta[1]) & 0xFFFFFFFCu);
-                            float b1 = -12582912.0f * c1;
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            ptx::mbar_arrive(bar(BR::SEMPTY + b));
+                        if (is_tail) {
 #pragma unroll
-                            for (int h2 = 0; h2 < 2; ++h2) {
-                                ptx::tmem_ld32(tmem + lane_base + C::TM_S + b * C::S_COLS + 64 + h2 * 32, raw);
-                                ptx::tmem_ld_wait();
-#pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    y[h2 * 32 + j] += fmaf(i2f_magic(raw[j]), c1, b1);
-                            }
+                            for (int j = 0; j < 64; ++j)
+                                if ((uint32_t)j >= tail)
+                                    sraw[j] = -(1 << 30);
                         }
-                    }
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0)
-                        ptx::mbar_arrive(bar(BR::SEMPTY + b));
-                    const bool is_tail = (tail != 0) && (bj == L.kb - 1);
-                    if (is_tail) {
+                        int32_t smax = sraw[0];
+#pragma unroll
+                        for (int j = 1; j < 64; ++j)
+                            smax = max(smax, sraw[j]);
+                        // exact logit order: c0 > 0, so argmax S == argmax logit
+                        const float tm = __int2float_rn(smax) * c0;
+                        m_new = fmaxf(m, tm);
+                        const float dmax = (m_new == tm) ? 0.f : fmaf(__int2float_rn(smax), c0, -m_new);
+                        gamma = l > 0.f ? ex2(m - m_new) : 1.0f;
 #pragma unroll
                         for (int j = 0; j < 64; ++j)
-                            if ((uint32_t)j >= tail)
-                                y[j] = -INFINITY;
-                    }
-                    float ymax = y[0];
+                            y[j] = fmaf(__int2float_rn(sraw[j] - smax), c0, dmax);
+                    } else {
+                        const float c0 = cq[0] * meta[0];
+                        const float c1 = cq[G - 1] * meta[1];
 #pragma unroll
-                    for (int j = 1; j < 64; ++j)
-                        ymax = fmaxf(ymax, y[j]);
-                    const float m_new = fmaxf(m, ymax);
-                    const float gamma = l > 0.f ? ex2(m - m_new) : 1.0f;
+                        for (int h2 = 0; h2 < 2; ++h2) {
+                            uint32_t r0[32], r1[32];
+                            ptx::tmem_ld32(tmem + lane_base + C::TM_S + b * C::S_COLS + h2 * 32, r0);
+                            ptx::tmem_ld32(tmem + lane_base + C::TM_S + b * C::S_COLS + 64 + h2 * 32, r1);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                y[h2 * 32 + j] =
+                                    fmaf(__int2float_rn((int32_t)r1[j]), c1, __int2float_rn((int32_t)r0[j]) * c0);
+                        }
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            ptx::mbar_arrive(bar(BR::SEMPTY + b));
+                        if (is_tail) {
+#pragma unroll
+                            for (int j = 0; j < 64; ++j)
+                                if ((uint32_t)j >= tail)
+                                    y[j] = -INFINITY;
+                        }
+                        float ymax = y[0];
+#pragma unroll
+                        for (int j = 1; j < 64; ++j)
+                            ymax = fmaxf(ymax, y[j]);
+                        m_new = fmaxf(m, ymax);
+                        gamma = l > 0.f ? ex2(m - m_new) : 1.0f;
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            y[j] = y[j] - m_new;
+                    }
                     float sum = 0.f, pmin = INFINITY, pmax = 0.f;
 #pragma unroll
                     for (int j = 0; j < 64; ++j) {
-                        y[j] = ex2(y[j] - m_new);
+                        y[j] = ex2(y[j]);
                         sum += y[j];
                         pmax = fmaxf(pmax, y[j]);
                         pmin = (is_tail && (uint32_t)j >= tail) ? pmin : fminf(pmin, y[j]);
@@ -363,16 +393,22 @@ __global__ void __launch_bounds__(320, 1)
                     float pscale = __fdiv_rn(hi - lo, P.p_qmax);
                     if (pscale == 0.f)
                         pscale = 1.f;
+                    // code = round-half-away(q), q = fp32 (p - lo) / pscale (quant_affine,
+                    // kernels_scalar.cpp:78-85; q >= 0 here, so half-away == floor(q + 0.5)).
+                    // q is formed in fp32 like the reference (division as x * RN(1/pscale));
+                    // floor(q + 0.5) is exact via two round-down adds: RD(q + 0.5) never
+                    // crosses an integer upward, and RD(t + 2^23) leaves floor(t) in the mantissa.
                     const float inv = __frcp_rn(pscale);
-                    const float nb = -lo * inv;
                     // codes -> 16 packed words -> 4 swizzled 16B chunks of row `row`
                     uint32_t w[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         uint32_t bb[4];
 #pragma unroll
-                        for (int k2 = 0; k2 < 4; ++k2)
-                            bb[k2] = __float_as_uint(fmaf(y[4 * c + k2], inv, nb) + 12582912.0f);
+                        for (int k2 = 0; k2 < 4; ++k2) {
+                            const float qv = __fmul_rn(__fsub_rn(y[4 * c + k2], lo), inv);
+                            bb[k2] = __float_as_uint(__fadd_rd(__fadd_rd(qv, 0.5f), 8388608.0f));
+                        }
                         w[c] = __byte_perm(__byte_perm(bb[0], bb[1], 0x0040), __byte_perm(bb[2], bb[3], 0x0040),
                                            0x5410);
                     }

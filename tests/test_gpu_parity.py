@@ -1,0 +1,219 @@
+"""GPU parity: every stage of the B200 path against the CPU oracle on the same inputs.
+
+Bar (BASELINE north_star): bit-exact for permutation indices, kept lists, quantized
+integer tensors (+ scales) and int32 QK^T accumulators; max|dO|/max|O| <= 1e-3 for
+the attention output against the restated INT8-QK engine (oracle/paro_oracle.c).
+"""
+import numpy as np
+import pytest
+
+from conftest import randn, rel_err
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL = 1e-3  # max|dO| / max|O| (north_star)
+
+# (grid, heads, d, orders) -- c1 from BASELINE.configs[0] plus ragged / 2-D / d=128 shapes
+CASES = [
+    ("F:2,H:8,W:8", 2, 64, ["HWF", "WFH"]),
+    ("F:3,H:7,W:11", 3, 64, ["FHW", "WHF", "HFW"]),  # N=231: ragged tail (39 rows), odd kb=4? -> kb=4
+    ("H:20,W:33", 2, 128, ["HW", "WH"]),  # N=660: kb=11 (odd: unpaired last q-block), tail 20
+    ("F:5,H:9,W:14", 2, 128, ["WFH", "FWH"]),  # N=630
+]
+
+
+def permuted(x, inv):
+    return np.ascontiguousarray(x[inv])
+
+
+def make_inputs(H, N, d, seed):
+    return randn(seed, (H, N, d)), randn(seed + 1, (H, N, d)), randn(seed + 2, (H, N, d))
+
+
+def random_masks(H, kb, density, seed, empty_row=None):
+    rng = np.random.default_rng(seed)
+    m = (rng.random((H, kb, kb)) < density).astype(np.uint8)
+    for h in range(H):
+        np.fill_diagonal(m[h], 1)
+    if empty_row is not None:
+        m[:, empty_row, :] = 0
+    return m
+
+
+@pytest.mark.parametrize("grid,H,d,orders", CASES)
+def test_perm_tables_bit_exact(paro, ctx, oracle, grid, H, d, orders):
+    g = paro.parse_grid(grid)
+    layer = paro.Layer(ctx, H, d, g, orders)
+    b = layer.buffers()
+    for h in range(H):
+        fwd, inv = oracle.make_perm(g.labels, g.extents, orders[h])
+        assert np.array_equal(b["inverse"][h], inv)
+        assert np.array_equal(b["forward"][h], fwd)
+    layer.close()
+
+
+@pytest.mark.parametrize("grid,H,d,orders", CASES)
+@pytest.mark.parametrize("v_bits", [8, 4])
+def test_reorder_quantize_bit_exact(paro, ctx, oracle, grid, H, d, orders, v_bits):
+    g = paro.parse_grid(grid)
+    N = g.token_count()
+    q, k, v = make_inputs(H, N, d, 11)
+    layer = paro.Layer(ctx, H, d, g, orders)
+    dq, dk, dv = (paro.DeviceBuffer.from_array(x) for x in (q, k, v))
+    layer.reorder_quantize(dq.ptr, dk.ptr, dv.ptr, v_bits)
+    paro.stream_sync()
+    b = layer.buffers()
+    kb = (N + 63) // 64
+    G = d // 64
+    for h in range(H):
+        _, inv = oracle.make_perm(g.labels, g.extents, orders[h])
+        for name, x, sc in (("q", q, b["q_scales"][h]), ("k", k, b["meta"][h][:, :G])):
+            codes, scales, _ = oracle.quantize(permuted(x[h], inv), 8, 1, 64)
+            assert np.array_equal(b[name][h][:N].astype(np.int32), codes), name
+            assert np.all(b[name][h][N:] == 0)
+            assert np.array_equal(sc[:kb].reshape(-1).view(np.uint32), scales.view(np.uint32)), name
+        vc, vs, vcs = oracle.quant_v(permuted(v[h], inv), v_bits)
+        assert np.array_equal(b["v"][h][:N].astype(np.int32), vc)
+        assert np.array_equal(b["meta"][h][:kb, 2].view(np.uint32), vs.view(np.uint32))
+        assert np.array_equal(b["meta"][h][:kb, 4:].astype(np.int64), vcs)
+    layer.close()
+
+
+@pytest.mark.parametrize("grid,H,d,orders", CASES)
+def test_mask_lists(paro, ctx, grid, H, d, orders):
+    g = paro.parse_grid(grid)
+    kb = (g.token_count() + 63) // 64
+    masks = random_masks(H, kb, 0.3, 5, empty_row=kb - 1)
+    layer = paro.Layer(ctx, H, d, g, orders)
+    layer.set_masks(masks)
+    kept, total = layer.mask_stats()
+    assert np.array_equal(kept, masks.sum(axis=2).astype(np.uint32))
+    assert total == int(masks.sum())
+    layer.close()
+
+
+@pytest.mark.parametrize("grid,H,d,orders", CASES)
+def test_qk_int32_accumulators_bit_exact(paro, ctx, grid, H, d, orders):
+    g = paro.parse_grid(grid)
+    N = g.token_count()
+    kb = (N + 63) // 64
+    q, k, v = make_inputs(H, N, d, 23)
+    layer = paro.Layer(ctx, H, d, g, orders)
+    dq, dk, dv = (paro.DeviceBuffer.from_array(x) for x in (q, k, v))
+    layer.reorder_quantize(dq.ptr, dk.ptr, dv.ptr, 8)
+    paro.stream_sync()
+    b = layer.buffers()
+    rng = np.random.default_rng(3)
+    tiles = np.array([[h, qb, bj] for h in range(H) for qb in range(kb) for bj in range(kb)], np.uint32)
+    if len(tiles) > 200:
+        tiles = tiles[rng.choice(len(tiles), 200, replace=False)]
+    S = layer.debug_qk(tiles)
+    G = d // 64
+    for t, (h, qb, bj) in enumerate(tiles):
+        Q = b["q"][h][qb * 64:(qb + 1) * 64].astype(np.int64)
+        K = b["k"][h][bj * 64:(bj + 1) * 64].astype(np.int64)
+        for gi in range(G):
+            ref = Q[:, gi * 64:(gi + 1) * 64] @ K[:, gi * 64:(gi + 1) * 64].T
+            assert np.array_equal(S[t, gi].astype(np.int64), ref), (h, qb, bj, gi)
+    layer.close()
+
+
+def run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv_bits, seed, scale=0.0):
+    g = paro.parse_grid(grid)
+    N = g.token_count()
+    q, k, v = make_inputs(H, N, d, seed)
+    layer = paro.Layer(ctx, H, d, g, orders)
+    layer.set_masks(masks)
+    out, zeroed = layer.forward_host(q, k, v, scale, pv_bits)
+    layer.close()
+    worst = 0.0
+    for h in range(H):
+        fwd, inv = oracle.make_perm(g.labels, g.extents, orders[h])
+        ref, zref_perm = oracle.paro_head(q[h], k[h], v[h], fwd, inv, None if masks is None else masks[h], pv_bits,
+                                          qk_mode=1, scale=scale)
+        zref = np.zeros(N, bool)
+        zref[inv[zref_perm]] = True  # permuted index -> original token
+        assert np.array_equal(zeroed[h].astype(bool), zref)
+        assert np.all(out[h][zref] == 0)
+        worst = max(worst, rel_err(out[h], ref))
+    print(f"[attn] {grid} H={H} d={d} pv={pv_bits} masks={'none' if masks is None else 'yes'}: max|dO|/max|O| = {worst:.3e}")
+    return worst
+
+
+@pytest.mark.parametrize("grid,H,d,orders", CASES)
+@pytest.mark.parametrize("pv_bits", [8, 4])
+def test_attention_matches_oracle(paro, ctx, oracle, grid, H, d, orders, pv_bits):
+    kb = (paro.parse_grid(grid).token_count() + 63) // 64
+    masks = random_masks(H, kb, 0.4, 7)
+    err = run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv_bits, 31)
+    assert err <= OUT_TOL, err
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_attention_dense_and_zeroed_rows(paro, ctx, oracle, d):
+    grid, H, orders = "F:4,H:10,W:12", 2, ["HWF", "FWH"]  # N=480, kb=8
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, None, 8, 41) <= OUT_TOL
+    masks = random_masks(H, 8, 0.3, 9, empty_row=3)
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, 8, 43) <= OUT_TOL
+
+
+def test_single_head_api_matches_oracle(paro, ctx, oracle):
+    n, d = 300, 64
+    q, k, v = randn(1, (n, d)), randn(2, (n, d)), randn(3, (n, d))
+    kb = (n + 63) // 64
+    mask = paro.BlockMask(kb, kb, 64, random_masks(1, kb, 0.5, 4)[0])
+    res = ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v), mask, paro.QuantConfig(8))
+    ref, z = oracle.stream_engine(q, k, v, mask.bits, 8, qk_mode=1)
+    assert rel_err(res.output, ref) <= OUT_TOL
+    assert res.zeroed_rows == list(np.nonzero(z)[0])
+
+
+def test_device_and_host_paths_identical(paro, ctx):
+    grid, H, d = "F:3,H:8,W:8", 2, 64
+    N = 192
+    q, k, v = make_inputs(H, N, d, 50)
+    masks = random_masks(H, 3, 0.5, 1)
+    layer = paro.Layer(ctx, H, d, grid, ["WHF", "HFW"])
+    layer.set_masks(masks)
+    out_h, z_h = layer.forward_host(q, k, v, 0.0, 8)
+    dq, dk, dv = (paro.DeviceBuffer.from_array(x) for x in (q, k, v))
+    dout = paro.DeviceBuffer(q.nbytes)
+    dz = paro.DeviceBuffer(H * N)
+    layer.forward(dq.ptr, dk.ptr, dv.ptr, 0.0, 8, dout.ptr, dz.ptr)
+    paro.stream_sync()
+    assert np.array_equal(dout.download(q.shape, np.float32), out_h)
+    assert np.array_equal(dz.download((H, N), np.uint8), z_h)
+    # deterministic across runs
+    out_h2, _ = layer.forward_host(q, k, v, 0.0, 8)
+    assert np.array_equal(out_h, out_h2)
+    layer.close()
+
+
+def test_device_apply_perm_rows_and_quantize(paro, ctx, oracle):
+    g = paro.parse_grid("F:13,H:30,W:45")
+    plan = paro.make_perm(g, "WHF")
+    m = randn(8, (g.token_count(), 64))
+    got = ctx.apply_perm_rows(m, plan)
+    assert np.array_equal(got, m[plan.inverse])
+    for cols in (64, 128):
+        for bits in (4, 8):
+            x = randn(9 + cols + bits, (1000, cols)) * 3
+            qt = ctx.quantize(x, paro.QuantConfig(bits, paro.SYMMETRIC, paro.PER_BLOCK, 64))
+            codes, scales, _ = oracle.quantize(x, bits, 1, 64)
+            assert np.array_equal(qt.codes, codes)
+            assert np.array_equal(qt.scales.view(np.uint32), scales.view(np.uint32))
+
+
+def test_gpu_errors(paro, ctx):
+    with pytest.raises(paro.ConfigError):
+        paro.Layer(ctx, 2, 96, "H:8,W:8")
+    layer = paro.Layer(ctx, 1, 64, "H:8,W:8")
+    layer.set_masks(None)
+    q = randn(0, (1, 64, 64))
+    with pytest.raises(paro.ConfigError):
+        layer.forward_host(q, q, q, 0.0, 6)
+    with pytest.raises(paro.ShapeError):
+        layer.forward_host(q[:, :32], q[:, :32], q[:, :32], 0.0, 8)
+    layer.close()
+    with pytest.raises(paro.ConfigError):
+        ctx.quantized_blocked_attention(paro.AttnInputs(q[0], q[0], q[0]), None, paro.QuantConfig(16))
