@@ -52,3 +52,21 @@ def randn(seed, shape):
 def rel_err(a, b):
     """max|a-b| / max|b| -- the north-star output metric."""
     return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64))) / max(np.max(np.abs(b)), 1e-30))
+
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="session")
+def c1():
+    return np.load(os.path.join(GOLD, "golden_c1.npz"))
+
+
+@pytest.fixture(scope="session")
+def rnd():
+    return np.load(os.path.join(GOLD, "golden_rand.npz"))
+
+
+@pytest.fixture(scope="session")
+def kat():
+    return np.load(os.path.join(GOLD, "golden_kat.npz"))
