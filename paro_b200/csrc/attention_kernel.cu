@@ -19,21 +19,23 @@
 // P codes follow the reference's fp32 quantizer exactly given p (round half
 // away, fp32 (p - lo) then * 1/pscale).
 //
-// Work unit: one (head, q-block pair) -- rows 0..63 = q-block 2p, 64..127 =
-// 2p+1 -- so each MMA is M = 128 over the union of the pair's kept key blocks;
-// a q-block's warps skip tiles its own mask row drops (no softmax work, the
-// garbage half of the MMA output is never read). Units are LPT-sorted by K2
-// and dealt to persistent CTAs in snake order.
+// Work unit: two q-blocks A, B of one head (paired by K2 with similar kept
+// counts), each running its OWN kept list through independent M = 64 MMAs:
+// A's accumulators sit in TMEM lanes 0-15 of each 32-lane quadrant, B's in
+// lanes 16-31 (the M=64 datapath layout at lane offset 0 / 16). Step t runs
+// tile A.list[t] and tile B.list[t] side by side, so every softmax lane works
+// on a kept tile (no union of mask rows) and the pair costs max(nA, nB) steps.
+// Units are LPT-sorted by K2 and dealt to persistent CTAs in snake order.
 //
 // Warp roles (320 threads; 2 CTAs/SM at d=64, 1 at d=128):
-//   warp 0     TMA producer: Q pair tile, K/V tiles + per-block meta (NS-stage ring)
+//   warp 0     TMA producer: Q tiles, per step the K/V tiles + meta of A and B
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5  softmax: TMEM S -> two passes (row extremes, then p / codes)
 //              -> P codes (u8) into swizzled smem; per-tile column offsets
 //   warps 6-9  epilogue: TMEM int32 PV -> dequant + rescale into fp32 registers,
 //              final normalisation + inverse-permuted row store
-// Warp w owns TMEM lanes 32*(w%4)..+31 (hardware lane-quadrant rule), i.e.
-// rows of one q-block: quadrants 0,1 -> q-block A, 2,3 -> q-block B.
+// A thread of quadrant q (= warp % 4), lane i owns row 16q + (i & 15) of
+// q-block (i < 16 ? A : B).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -47,34 +49,35 @@ namespace paro {
 template <int D>
 struct K3Cfg {
     static constexpr int G = D / 64;
-    static constexpr int NS = 4;
+    static constexpr int NS = 3;
     static constexpr int MINB = D == 64 ? 2 : 1; // CTAs per SM
-    static constexpr uint32_t Q_BYTES = 128 * D;
+    static constexpr uint32_t QT_BYTES = 64 * D; // one q-block tile
     static constexpr uint32_t KV_BYTES = 64 * D;
     static constexpr uint32_t META_BYTES = (4 + D) * 4; // multiple of 16
-    static constexpr uint32_t P_BYTES = 128 * 64;
+    static constexpr uint32_t STAGE_BYTES = (4 * KV_BYTES + 2 * META_BYTES + 1023) / 1024 * 1024;
+    static constexpr uint32_t P_BYTES = 64 * 64; // one side's P tile
     static constexpr uint32_t S_COLS = G * 64;
     static constexpr uint32_t TM_S = 0;          // two S buffers
     static constexpr uint32_t TM_O = 2 * S_COLS; // two O buffers
     static constexpr uint32_t TMEM_COLS = (2 * S_COLS + 2 * D) <= 256 ? 256 : 512;
-    static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
-    static constexpr uint32_t OFF_V = OFF_K + NS * KV_BYTES;
-    static constexpr uint32_t OFF_P = OFF_V + NS * KV_BYTES;
-    static constexpr uint32_t OFF_META = OFF_P + 2 * P_BYTES;
-    static constexpr uint32_t OFF_ROWMETA = OFF_META + NS * META_BYTES;
-    static constexpr uint32_t OFF_U = OFF_ROWMETA + 2 * 128 * 16; // [2 buf][2 q-block][D] column offsets
-    static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;
-    static constexpr uint32_t OFF_L = OFF_RED + 2 * 2 * 2 * 8;
-    static constexpr uint32_t OFF_BAR = OFF_L + 128 * 4;
-    static constexpr uint32_t NBAR = 2 + 2 * NS + 12;
+    static constexpr uint32_t OFF_Q = 0; // A at +0, B at +QT_BYTES
+    static constexpr uint32_t OFF_STAGE = 2 * QT_BYTES;
+    // within a stage: K_A, K_B, V_A, V_B, meta_A, meta_B
+    static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES; // [2 buf][2 side]
+    static constexpr uint32_t OFF_ROWMETA = OFF_P + 4 * P_BYTES;     // [2 buf][2 side][64] float4
+    static constexpr uint32_t OFF_U = OFF_ROWMETA + 2 * 2 * 64 * 16;  // [2 buf][2 side][D]
+    static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;        // [2 parity][4 quad][2 side] float2
+    static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 side][64]
+    static constexpr uint32_t OFF_BAR = OFF_L + 2 * 64 * 4;
+    static constexpr uint32_t NBAR = 2 + 2 * NS + 13;
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
     // swizzle: rows of D int8 -> 64B (D=64) or 128B (D=128) swizzle atoms of 8 rows
     static constexpr uint32_t LAYOUT = D == 64 ? ptx::kSwizzle64B : ptx::kSwizzle128B;
     static constexpr uint32_t ATOM = 8 * D; // bytes per 8-row swizzle atom
-    static constexpr uint32_t IDESC_QK = ptx::idesc_i8(true, true, false, false, 128, 64);
-    static constexpr uint32_t IDESC_PV = ptx::idesc_i8(false, true, false, true, 128, D);
+    static constexpr uint32_t IDESC_QK = ptx::idesc_i8(true, true, false, false, 64, 64);
+    static constexpr uint32_t IDESC_PV = ptx::idesc_i8(false, true, false, true, 64, D);
+    static constexpr uint32_t LANE16 = 16u << 16; // TMEM address of lane 16 (side B)
 };
 
 enum : uint32_t { B_QFULL = 0, B_QEMPTY = 1 };
@@ -82,7 +85,7 @@ template <int NS>
 struct Bars {
     static constexpr uint32_t KVFULL = 2, KVEMPTY = 2 + NS, SFULL = 2 + 2 * NS, SEMPTY = SFULL + 2,
                               PFULL = SEMPTY + 2, PEMPTY = PFULL + 2, OFULL = PEMPTY + 2, OEMPTY = OFULL + 2,
-                              LFULL = OEMPTY + 2, LEMPTY = LFULL + 1;
+                              LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1;
 };
 
 // K-major operand rows of D bytes (Q, K): SBO = one 8-row atom.
@@ -90,7 +93,7 @@ template <int D>
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
     return ptx::smem_desc(saddr, 16, K3Cfg<D>::ATOM, K3Cfg<D>::LAYOUT);
 }
-// P: 128 rows x 64 u8 (K = keys), K-major, 64B swizzle.
+// P: 64 rows x 64 u8 (K = keys), K-major, 64B swizzle.
 __device__ __forceinline__ uint64_t desc_p(uint32_t saddr) { return ptx::smem_desc(saddr, 16, 512, ptx::kSwizzle64B); }
 // V: [key][D] row-major = MN-major B operand (N = D contiguous); SBO = 8 keys.
 template <int D>
@@ -143,7 +146,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 
-// QK issue for one tile: S_g (g < G) in TMEM columns tm_s + 64*g, two K=32 steps per group
+// QK issue for one q-block tile (M = 64): S_g in TMEM columns tm_s + 64*g at the
+// tile's lane offset; two K=32 steps per 64-column group.
 template <int D>
 __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk) {
     using C = K3Cfg<D>;
@@ -165,126 +169,200 @@ struct K3Params {
     uint32_t n_items;
 };
 
+struct Item {
+    uint32_t h, qa, qb, na, nb, n; // qb = 0xffff when the pair has no B
+};
+
+__device__ __forceinline__ Item load_item(const LayerDev& L, uint32_t it) {
+    Item x;
+    x.h = it >> 16;
+    const uint32_t p = it & 0xffffu;
+    const uint32_t pr = L.pairs[(size_t)x.h * L.np + p];
+    x.qa = pr & 0xffffu;
+    x.qb = pr >> 16;
+    x.na = L.qb_count[(size_t)x.h * L.kb2 + x.qa];
+    x.nb = x.qb != 0xffffu ? L.qb_count[(size_t)x.h * L.kb2 + x.qb] : 0u;
+    x.n = x.na > x.nb ? x.na : x.nb;
+    return x;
+}
+
 // ---------------------------------------------------------------------------
-// Softmax, one kept tile for this thread's row. Pass 1 reads S for the row
-// extremes (exact in the integer domain at d=64); the q-block's tile group
-// lo/hi then come from two exp2 per row (p at the extreme columns, computed
-// with the same formula the elements use, so they are the true min/max of the
-// p values); pass 2 re-reads S and produces p, the row sum and the P codes.
+// Softmax, one step for this thread's row. Pass 1 reads S for the row extremes
+// (exact in the integer domain at d=64); the tile group's lo/hi then come from
+// two exp2 per row (p at the extreme columns, computed with the same formula
+// the elements use, so they are the true min/max of the p values); pass 2
+// re-reads S and produces p, the row sum and the P codes. Lanes whose q-block
+// has no tile this step (`live` false) run the same instructions but change
+// no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
 struct RowState {
     float m, l;
 };
 
+// wait for several mbarrier phases, issuing the probes back to back so their
+// latencies overlap (each try_wait costs ~90 cycles even when already complete)
+__device__ __forceinline__ void mbar_wait2(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1) {
+    const bool r0 = ptx::mbar_try_wait(b0, p0);
+    const bool r1 = ptx::mbar_try_wait(b1, p1);
+    if (!r0)
+        ptx::mbar_wait(b0, p0);
+    if (!r1)
+        ptx::mbar_wait(b1, p1);
+}
+__device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                           uint32_t p2) {
+    const bool r0 = ptx::mbar_try_wait(b0, p0);
+    const bool r1 = ptx::mbar_try_wait(b1, p1);
+    const bool r2 = ptx::mbar_try_wait(b2, p2);
+    if (!r0)
+        ptx::mbar_wait(b0, p0);
+    if (!r1)
+        ptx::mbar_wait(b1, p1);
+    if (!r2)
+        ptx::mbar_wait(b2, p2);
+}
+
+// The P group's min/max is a reduction over 64 rows spread across the 4
+// softmax warps. It is split-phase: each warp publishes its half-warp extremes
+// and arrives on an mbarrier, then computes all p values (the MUFU-bound part)
+// before it waits for the other warps, so the cross-warp latency hides behind
+// exp2 work. The S buffer is released right after p is formed.
 template <int D, bool TAIL>
-__device__ __forceinline__ void softmax_tile(uint32_t s_addr, const float* meta, float cq0, float cq1, uint32_t ncol,
-                                             bool valid_row, RowState& st, float p_qmax, float2* red_slot,
-                                             const float2* red_pair, uint32_t bar_id, uint8_t* prow, uint32_t row,
-                                             float& gamma_out, float& lo_out, float& pscale_out) {
+__device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1, uint32_t ncol, bool live,
+                                             bool valid_row, RowState& st, float p_qmax, float2* red_w,
+                                             const float2* red_r, uint32_t red_bar, uint32_t red_phase,
+                                             uint32_t sempty_bar, uint8_t* prow, uint32_t r, float& gamma_out,
+                                             float& lo_out, float& pscale_out) {
     constexpr int G = D / 64;
-    const float c0 = cq0 * meta[0];
-    const float c1 = G == 2 ? cq1 * meta[1] : 0.f;
-    // -------- pass 1: row extremes
+    const uint32_t lane = threadIdx.x & 31;
+    // -------- pass 1: row extremes (4 independent chains per pass)
     float m_new, pmax_r, pmin_r;
     if (G == 1) {
-        int32_t smax = INT32_MIN, smin = INT32_MAX;
+        int32_t mx[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN}, mn[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
-            uint32_t r[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, r);
+            uint32_t x[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 if (!TAIL || (uint32_t)(h2 * 32 + j) < ncol) {
-                    smax = max(smax, (int32_t)r[j]);
-                    smin = min(smin, (int32_t)r[j]);
+                    mx[j & 3] = max(mx[j & 3], (int32_t)x[j]);
+                    mn[j & 3] = min(mn[j & 3], (int32_t)x[j]);
                 }
             }
         }
+        const int32_t smax = max(max(mx[0], mx[1]), max(mx[2], mx[3]));
+        const int32_t smin = min(min(mn[0], mn[1]), min(mn[2], mn[3]));
         const float tm = __int2float_rn(smax) * c0;
         m_new = fmaxf(st.m, tm);
         pmax_r = ex2(fmaf(__int2float_rn(smax), c0, -m_new));
         pmin_r = ex2(fmaf(__int2float_rn(smin), c0, -m_new));
     } else {
-        float ymax = -INFINITY, ymin = INFINITY;
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
-            uint32_t r0[32], r1[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, r0);
-            ptx::tmem_ld32(s_addr + 64 + h2 * 32, r1);
+            uint32_t x0[32], x1[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x0);
+            ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const float y = fmaf(__int2float_rn((int32_t)r1[j]), c1, __int2float_rn((int32_t)r0[j]) * c0);
+                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
                 if (!TAIL || (uint32_t)(h2 * 32 + j) < ncol) {
-                    ymax = fmaxf(ymax, y);
-                    ymin = fminf(ymin, y);
+                    mx[j & 3] = fmaxf(mx[j & 3], y);
+                    mn[j & 3] = fminf(mn[j & 3], y);
                 }
             }
         }
+        const float ymax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        const float ymin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
         m_new = fmaxf(st.m, ymax);
         pmax_r = ex2(ymax - m_new);
         pmin_r = ex2(ymin - m_new);
     }
     const float gamma = st.l > 0.f ? ex2(st.m - m_new) : 1.0f;
-    if (!valid_row) {
+    if (!(live && valid_row)) {
         pmin_r = INFINITY;
         pmax_r = 0.f;
     }
-    // -------- P group extremes over the q-block's 64 rows (p >= 0: compare as uint)
-    const uint32_t umin = __reduce_min_sync(0xffffffffu, __float_as_uint(pmin_r));
-    const uint32_t umax = __reduce_max_sync(0xffffffffu, __float_as_uint(pmax_r));
-    if ((row & 31) == 0)
-        *red_slot = make_float2(__uint_as_float(umin), __uint_as_float(umax));
-    ptx::named_bar_sync(bar_id, 64);
-    const float2 ra = red_pair[0], rb = red_pair[1];
-    const float lo = fminf(ra.x, rb.x), hi = fmaxf(ra.y, rb.y);
-    float pscale = __fdiv_rn(hi - lo, p_qmax);
-    if (pscale == 0.f)
-        pscale = 1.f;
-    const float inv = __frcp_rn(pscale);
-    // -------- pass 2: p, row sum, codes
-    const uint64_t c00 = pk(c0, c0), nm = pk(-m_new, -m_new), nlo = pk(-lo, -lo), inv2 = pk(inv, inv);
-    const uint64_t half2 = pk(0.5f, 0.5f), magic2 = pk(8388608.0f, 8388608.0f);
+    // -------- publish the half-warp extremes (16 rows of each q-block per warp)
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+        pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
+        pmax_r = fmaxf(pmax_r, __shfl_xor_sync(0xffffffffu, pmax_r, o));
+    }
+    if ((lane & 15) == 0)
+        *red_w = make_float2(pmin_r, pmax_r);
+    __syncwarp();
+    if (lane == 0)
+        ptx::mbar_arrive(red_bar);
+    // -------- pass 2a: p and the row sum (independent of lo/hi)
+    float pv[64];
     uint64_t sum2 = pk(0.f, 0.f);
+    const uint64_t c00 = pk(c0, c0), nm = pk(-m_new, -m_new);
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
-        float pv[32];
         if (G == 1) {
-            uint32_t r[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, r);
+            uint32_t x[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 const uint64_t y2 =
-                    fma2(pk(__int2float_rn((int32_t)r[2 * k]), __int2float_rn((int32_t)r[2 * k + 1])), c00, nm);
+                    fma2(pk(__int2float_rn((int32_t)x[2 * k]), __int2float_rn((int32_t)x[2 * k + 1])), c00, nm);
                 float ya, yb;
                 upk(y2, ya, yb);
-                pv[2 * k] = ex2(ya);
-                pv[2 * k + 1] = ex2(yb);
+                pv[h2 * 32 + 2 * k] = ex2(ya);
+                pv[h2 * 32 + 2 * k + 1] = ex2(yb);
             }
         } else {
-            uint32_t r0[32], r1[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, r0);
-            ptx::tmem_ld32(s_addr + 64 + h2 * 32, r1);
+            uint32_t x0[32], x1[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x0);
+            ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const float y = fmaf(__int2float_rn((int32_t)r1[j]), c1, __int2float_rn((int32_t)r0[j]) * c0);
-                pv[j] = ex2(y - m_new);
+                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
+                pv[h2 * 32 + j] = ex2(y - m_new);
             }
         }
-        if (TAIL) {
+    }
+    // S no longer needed: release the TMEM buffer to the QK issuer
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0)
+        ptx::mbar_arrive(sempty_bar);
+    if (TAIL) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if ((uint32_t)(h2 * 32 + j) >= ncol)
-                    pv[j] = 0.f;
-        }
+        for (int j = 0; j < 64; ++j)
+            if ((uint32_t)j >= ncol)
+                pv[j] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        sum2 = add2(sum2, pk(pv[2 * k], pv[2 * k + 1]));
+    // -------- group extremes from all four warps
+    ptx::mbar_wait(red_bar, red_phase);
+    float lo = red_r[0].x, hi = red_r[0].y;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+        lo = fminf(lo, red_r[2 * q].x);
+        hi = fmaxf(hi, red_r[2 * q].y);
+    }
+    float pscale = __fdiv_rn(hi - lo, p_qmax);
+    if (pscale == 0.f)
+        pscale = 1.f;
+    const float inv = __frcp_rn(pscale);
+    // -------- pass 2b: codes
+    const uint64_t nlo = pk(-lo, -lo), inv2 = pk(inv, inv);
+    const uint64_t half2 = pk(0.5f, 0.5f), magic2 = pk(8388608.0f, 8388608.0f);
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
         uint32_t w[8];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-            const uint64_t p2 = pk(pv[2 * k], pv[2 * k + 1]);
-            sum2 = add2(sum2, p2);
+            const uint64_t p2 = pk(pv[h2 * 32 + 2 * k], pv[h2 * 32 + 2 * k + 1]);
             // q = (p - lo) * (1/pscale); code = floor(q + 0.5) via two round-down adds
             const uint64_t u2 = add2_rm(add2_rm(mul2(add2(p2, nlo), inv2), half2), magic2);
             float ua, ub;
@@ -298,14 +376,16 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, const float* meta,
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const int chunk = h2 * 2 + c;
-            *reinterpret_cast<uint4*>(prow + ((chunk ^ ((row >> 1) & 3)) << 4)) =
+            *reinterpret_cast<uint4*>(prow + ((chunk ^ ((r >> 1) & 3)) << 4)) =
                 make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         }
     }
     float sa, sb;
     upk(sum2, sa, sb);
-    st.l = st.l * gamma + (sa + sb);
-    st.m = m_new;
+    if (live) {
+        st.l = st.l * gamma + (sa + sb);
+        st.m = m_new;
+    }
     gamma_out = gamma;
     lo_out = lo;
     pscale_out = pscale;
@@ -346,6 +426,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         }
         ptx::mbar_init(bar(BR::LFULL), 4);
         ptx::mbar_init(bar(BR::LEMPTY), 4);
+        ptx::mbar_init(bar(BR::RED), 4);
         ptx::fence_barrier_init();
     }
     if (warp == 1)
@@ -362,6 +443,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         const uint32_t idx = r * G_cta + ((r & 1) ? (G_cta - 1 - blockIdx.x) : blockIdx.x);
         return idx < P.n_items ? (int)L.order[idx] : -1;
     };
+    auto stage = [&](uint32_t s) { return sbase + C::OFF_STAGE + s * C::STAGE_BYTES; };
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -374,25 +456,36 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const int it = item_at(r);
                 if (it < 0)
                     continue;
-                const uint32_t h = (uint32_t)it >> 16, p = (uint32_t)it & 0xffffu;
-                const uint32_t n = L.pair_count[h * L.np + p];
-                const uint16_t* list = L.items + ((size_t)h * L.np + p) * L.kb;
-                const int32_t row0 = (int32_t)(h * L.kb2 * 64);
+                const Item x = load_item(L, (uint32_t)it);
+                const uint16_t* la = L.items + ((size_t)x.h * L.kb + x.qa) * L.kb;
+                const uint16_t* lb = L.items + ((size_t)x.h * L.kb + (x.qb != 0xffffu ? x.qb : 0)) * L.kb;
+                const int32_t row0 = (int32_t)(x.h * L.kb2 * 64);
                 ptx::mbar_wait(bar(B_QEMPTY), (I & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(bar(B_QFULL), C::Q_BYTES);
-                ptx::tma_load_2d(sbase + C::OFF_Q, &tm_q, 0, row0 + (int32_t)p * 128, bar(B_QFULL));
-                for (uint32_t t = 0; t < n; ++t, ++T) {
+                ptx::mbar_arrive_expect_tx(bar(B_QFULL), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
+                ptx::tma_load_2d(sbase + C::OFF_Q, &tm_q, 0, row0 + (int32_t)x.qa * 64, bar(B_QFULL));
+                if (x.qb != 0xffffu)
+                    ptx::tma_load_2d(sbase + C::OFF_Q + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64,
+                                     bar(B_QFULL));
+                for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS;
                     ptx::mbar_wait(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
-                    const uint32_t bj = list[t] & 0x3fffu;
-                    ptx::mbar_arrive_expect_tx(bar(BR::KVFULL + s), 2 * C::KV_BYTES + C::META_BYTES);
-                    ptx::tma_load_2d(sbase + C::OFF_K + s * C::KV_BYTES, &tm_k, 0, row0 + (int32_t)bj * 64,
-                                     bar(BR::KVFULL + s));
-                    ptx::tma_load_2d(sbase + C::OFF_V + s * C::KV_BYTES, &tm_v, 0, row0 + (int32_t)bj * 64,
-                                     bar(BR::KVFULL + s));
-                    ptx::bulk_load(sbase + C::OFF_META + s * C::META_BYTES,
-                                   L.meta + ((size_t)h * L.kb2 + bj) * meta_stride(D), C::META_BYTES,
-                                   bar(BR::KVFULL + s));
+                    const bool ha = t < x.na, hb = t < x.nb;
+                    ptx::mbar_arrive_expect_tx(bar(BR::KVFULL + s),
+                                               (ha + hb) * (2 * C::KV_BYTES + C::META_BYTES));
+                    const uint32_t st = stage(s);
+#pragma unroll
+                    for (int side = 0; side < 2; ++side) {
+                        if (side ? hb : ha) {
+                            const uint32_t bj = side ? lb[t] : la[t];
+                            ptx::tma_load_2d(st + side * C::KV_BYTES, &tm_k, 0, row0 + (int32_t)bj * 64,
+                                             bar(BR::KVFULL + s));
+                            ptx::tma_load_2d(st + (2 + side) * C::KV_BYTES, &tm_v, 0, row0 + (int32_t)bj * 64,
+                                             bar(BR::KVFULL + s));
+                            ptx::bulk_load(st + 4 * C::KV_BYTES + side * C::META_BYTES,
+                                           L.meta + ((size_t)x.h * L.kb2 + bj) * meta_stride(D), C::META_BYTES,
+                                           bar(BR::KVFULL + s));
+                        }
+                    }
                 }
                 ++I;
             }
@@ -401,17 +494,22 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             uint32_t T = 0, I = 0;
-            auto issue_pv = [&](uint32_t U) {
+            auto issue_pv = [&](uint32_t U, bool ha, bool hb) {
                 const uint32_t s = U % NS, b = U & 1, ph = (U >> 1) & 1;
                 ptx::mbar_wait(bar(BR::PFULL + b), ph);
                 ptx::mbar_wait(bar(BR::OEMPTY + b), ph ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t sp = sbase + C::OFF_P + b * C::P_BYTES;
-                const uint32_t sv = sbase + C::OFF_V + s * C::KV_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk)
-                    ptx::mma_i8(tmem + C::TM_O + b * D, desc_p(sp + kk * 32), desc_v<D>(sv + kk * 32 * D),
-                                C::IDESC_PV, kk);
+                for (int side = 0; side < 2; ++side) {
+                    if (side ? hb : ha) {
+                        const uint32_t sp = sbase + C::OFF_P + (b * 2 + side) * C::P_BYTES;
+                        const uint32_t sv = stage(s) + (2 + side) * C::KV_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)
+                            ptx::mma_i8(tmem + (side ? C::LANE16 : 0u) + C::TM_O + b * D, desc_p(sp + kk * 32),
+                                        desc_v<D>(sv + kk * 32 * D), C::IDESC_PV, kk);
+                    }
+                }
                 ptx::mma_commit(bar(BR::OFULL + b));
                 ptx::mma_commit(bar(BR::KVEMPTY + s));
                 ptx::mma_commit(bar(BR::PEMPTY + b));
@@ -420,25 +518,27 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const int it = item_at(r);
                 if (it < 0)
                     continue;
-                const uint32_t h = (uint32_t)it >> 16, p = (uint32_t)it & 0xffffu;
-                const uint32_t n = L.pair_count[h * L.np + p];
+                const Item x = load_item(L, (uint32_t)it);
                 ptx::mbar_wait(bar(B_QFULL), I & 1);
                 ptx::tc_fence_after();
-                for (uint32_t t = 0; t < n; ++t, ++T) {
+                for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS, b = T & 1;
                     ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
                     ptx::mbar_wait(bar(BR::SEMPTY + b), ((T >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
-                    issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, sbase + C::OFF_Q,
-                                sbase + C::OFF_K + s * C::KV_BYTES);
+                    if (t < x.na)
+                        issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, sbase + C::OFF_Q, stage(s));
+                    if (t < x.nb)
+                        issue_qk<D>(tmem + C::LANE16 + C::TM_S + b * C::S_COLS, sbase + C::OFF_Q + C::QT_BYTES,
+                                    stage(s) + C::KV_BYTES);
                     ptx::mma_commit(bar(BR::SFULL + b));
-                    if (t + 1 == n)
+                    if (t + 1 == x.n)
                         ptx::mma_commit(bar(B_QEMPTY));
                     if (t > 0)
-                        issue_pv(T - 1);
+                        issue_pv(T - 1, t - 1 < x.na, t - 1 < x.nb);
                 }
-                if (n > 0)
-                    issue_pv(T - 1);
+                if (x.n > 0)
+                    issue_pv(T - 1, x.n - 1 < x.na, x.n - 1 < x.nb);
                 else
                     ptx::mma_commit(bar(B_QEMPTY));
                 ++I;
@@ -447,75 +547,68 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
     } else if (warp < 6) {
         // ------------------------------------------------------------ softmax
         const uint32_t quad = warp & 3;
-        const uint32_t row = quad * 32 + lane;
-        const uint32_t qsel = quad >> 1, wip = quad & 1;
+        const uint32_t side = lane >> 4;
+        const uint32_t r = quad * 16 + (lane & 15); // row within its q-block
         const uint32_t lane_base = (quad * 32) << 16;
-        const uint32_t rl = row & 63;
         float2* red = reinterpret_cast<float2*>(smem + C::OFF_RED);
         float4* rowmeta = reinterpret_cast<float4*>(smem + C::OFF_ROWMETA);
         float* usm = reinterpret_cast<float*>(smem + C::OFF_U);
         float* lsm = reinterpret_cast<float*>(smem + C::OFF_L);
         const uint32_t tail = L.N & 63;
         uint32_t T = 0, I = 0;
-        for (uint32_t r = 0; r < rounds; ++r) {
-            const int it = item_at(r);
+        for (uint32_t rr = 0; rr < rounds; ++rr) {
+            const int it = item_at(rr);
             if (it < 0)
                 continue;
-            const uint32_t h = (uint32_t)it >> 16, p = (uint32_t)it & 0xffffu;
-            const uint32_t n = L.pair_count[h * L.np + p];
-            const uint16_t* list = L.items + ((size_t)h * L.np + p) * L.kb;
-            const uint32_t qb = 2 * p + qsel;
-            const bool valid_row = qb < L.kb && qb * 64 + rl < L.N;
-            const float cq0 = P.scale_log2 * L.qsc[((size_t)h * L.kb2 + qb) * G];
-            const float cq1 = G == 2 ? P.scale_log2 * L.qsc[((size_t)h * L.kb2 + qb) * G + G - 1] : 0.f;
+            const Item x = load_item(L, (uint32_t)it);
+            const bool has_qb = side ? x.qb != 0xffffu : true;
+            const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
+            const uint32_t nmine = side ? x.nb : x.na;
+            const uint16_t* list = L.items + ((size_t)x.h * L.kb + qb) * L.kb;
+            const bool valid_row = has_qb && qb * 64 + r < L.N;
+            const float cq0 = P.scale_log2 * L.qsc[((size_t)x.h * L.kb2 + qb) * G];
+            const float cq1 = G == 2 ? P.scale_log2 * L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
             RowState st{-INFINITY, 0.f};
-            for (uint32_t t = 0; t < n; ++t, ++T) {
+            for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
-                const uint32_t e = list[t];
-                const uint32_t bj = e & 0x3fffu;
-                const bool keep = (e >> (14 + qsel)) & 1u;
-                ptx::mbar_wait(bar(BR::SFULL + b), ph);
-                ptx::mbar_wait(bar(BR::PEMPTY + b), ph ^ 1);
-                if (keep) {
-                    ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
-                    ptx::tc_fence_after();
-                    const float* meta = reinterpret_cast<const float*>(smem + C::OFF_META + s * C::META_BYTES);
-                    uint8_t* prow = smem + C::OFF_P + b * C::P_BYTES + (row >> 3) * 512 + (row & 7) * 64;
-                    const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
-                    float2* slot = red + (T & 1) * 4 + qsel * 2 + wip;
-                    const float2* pair = red + (T & 1) * 4 + qsel * 2;
-                    float gamma, lo, pscale;
-                    if (tail != 0 && bj == L.kb - 1)
-                        softmax_tile<D, true>(s_addr, meta, cq0, cq1, tail, valid_row, st, P.p_qmax, slot, pair,
-                                              1 + qsel, prow, row, gamma, lo, pscale);
-                    else
-                        softmax_tile<D, false>(s_addr, meta, cq0, cq1, 64, valid_row, st, P.p_qmax, slot, pair,
-                                               1 + qsel, prow, row, gamma, lo, pscale);
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0)
-                        ptx::mbar_arrive(bar(BR::SEMPTY + b));
-                    const float vsc = meta[2];
-                    rowmeta[b * 128 + row] = make_float4(gamma, pscale * vsc, 0.f, 1.f);
-                    // per-column offset term of this tile: (lo * vscale) * colsum[c]
-                    const float os = lo * vsc;
-                    float* u = usm + (b * 2 + qsel) * D;
+                const bool live = t < nmine;
+                const uint32_t bj = live ? list[t] : 0u;
+                mbar_wait3(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
+                ptx::tc_fence_after();
+                const float* meta =
+                    reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES + 4 * C::KV_BYTES +
+                                                   side * C::META_BYTES);
+                const float c0 = cq0 * meta[0];
+                const float c1 = G == 2 ? cq1 * meta[1] : 0.f;
+                uint8_t* prow = smem + C::OFF_P + (b * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
+                const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
+                float2* red_w = red + ((T & 1) * 4 + quad) * 2 + side;
+                const float2* red_r = red + (T & 1) * 8 + side;
+                const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
+                float gamma, lo, pscale;
+                if (__any_sync(0xffffffffu, tail_tile))
+                    softmax_step<D, true>(s_addr, c0, c1, tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax,
+                                          red_w, red_r, bar(BR::RED), T & 1, bar(BR::SEMPTY + b), prow, r, gamma,
+                                          lo, pscale);
+                else
+                    softmax_step<D, false>(s_addr, c0, c1, 64u, live, valid_row, st, P.p_qmax, red_w, red_r,
+                                           bar(BR::RED), T & 1, bar(BR::SEMPTY + b), prow, r, gamma, lo, pscale);
+                const float vsc = meta[2];
+                rowmeta[(b * 2 + side) * 64 + r] =
+                    make_float4(live ? gamma : 1.f, live ? pscale * vsc : 0.f, 0.f, live ? 1.f : 0.f);
+                // per-column offset term of this tile: (lo * vscale) * colsum[c] (0 when idle)
+                const float os = live ? lo * vsc : 0.f;
+                float* u = usm + (b * 2 + side) * D;
 #pragma unroll
-                    for (int c = 0; c < D / 64; ++c)
-                        u[rl + 64 * c] = os * meta[4 + rl + 64 * c];
-                } else {
-                    __syncwarp();
-                    if (lane == 0)
-                        ptx::mbar_arrive(bar(BR::SEMPTY + b));
-                    rowmeta[b * 128 + row] = make_float4(1.f, 0.f, 0.f, 0.f);
-                }
+                for (int c = 0; c < D / 64; ++c)
+                    u[r + 64 * c] = os * meta[4 + r + 64 * c];
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0)
                     ptx::mbar_arrive(bar(BR::PFULL + b));
             }
             ptx::mbar_wait(bar(BR::LEMPTY), (I & 1) ^ 1);
-            lsm[row] = st.l;
+            lsm[side * 64 + r] = st.l;
             __syncwarp();
             if (lane == 0)
                 ptx::mbar_arrive(bar(BR::LFULL));
@@ -524,51 +617,48 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
     } else {
         // ------------------------------------------------------------ epilogue
         const uint32_t quad = warp & 3;
-        const uint32_t row = quad * 32 + lane;
-        const uint32_t qsel = quad >> 1;
+        const uint32_t side = lane >> 4;
+        const uint32_t r = quad * 16 + (lane & 15);
         const uint32_t lane_base = (quad * 32) << 16;
-        const uint32_t rl = row & 63;
         const float4* rowmeta = reinterpret_cast<const float4*>(smem + C::OFF_ROWMETA);
         const float* usm = reinterpret_cast<const float*>(smem + C::OFF_U);
         const float* lsm = reinterpret_cast<const float*>(smem + C::OFF_L);
         uint32_t T = 0, I = 0;
-        for (uint32_t r = 0; r < rounds; ++r) {
-            const int it = item_at(r);
+        for (uint32_t rr = 0; rr < rounds; ++rr) {
+            const int it = item_at(rr);
             if (it < 0)
                 continue;
-            const uint32_t h = (uint32_t)it >> 16, p = (uint32_t)it & 0xffffu;
-            const uint32_t n = L.pair_count[h * L.np + p];
-            const uint32_t qb = 2 * p + qsel;
-            const bool valid_row = qb < L.kb && qb * 64 + rl < L.N;
+            const Item x = load_item(L, (uint32_t)it);
+            const bool has_qb = side ? x.qb != 0xffffu : true;
+            const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
+            const bool valid_row = has_qb && qb * 64 + r < L.N;
             uint64_t acc[D / 2];
 #pragma unroll
             for (int c = 0; c < D / 2; ++c)
                 acc[c] = 0ull;
-            for (uint32_t t = 0; t < n; ++t, ++T) {
+            for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t b = T & 1, ph = (T >> 1) & 1;
-                ptx::mbar_wait(bar(BR::OFULL + b), ph);
-                ptx::mbar_wait(bar(BR::PFULL + b), ph);
+                mbar_wait2(bar(BR::OFULL + b), ph, bar(BR::PFULL + b), ph);
                 ptx::tc_fence_after();
-                const float4 rm = rowmeta[b * 128 + row];
-                if (rm.w != 0.f) {
-                    const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
-                    const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + qsel) * D);
+                // idle rows carry gamma 1, ss 0 and u 0: acc*1 + 0*ip + 0 == acc exactly
+                const float4 rm = rowmeta[(b * 2 + side) * 64 + r];
+                const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
+                const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + side) * D);
 #pragma unroll
-                    for (int ch = 0; ch < D / 16; ++ch) {
-                        uint32_t raw[16];
-                        tmem_ld16(tmem + lane_base + C::TM_O + b * D + ch * 16, raw);
-                        ptx::tmem_ld_wait();
+                for (int ch = 0; ch < D / 16; ++ch) {
+                    uint32_t raw[16];
+                    tmem_ld16(tmem + lane_base + C::TM_O + b * D + ch * 16, raw);
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
-                            const float4 uu = u4[ch * 4 + q4];
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 uu = u4[ch * 4 + q4];
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const int j = q4 * 4 + hh * 2;
-                                const uint64_t x2 =
-                                    pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
-                                const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
-                                acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
-                            }
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int j = q4 * 4 + hh * 2;
+                            const uint64_t x2 =
+                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                            const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
+                            acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
                         }
                     }
                 }
@@ -580,14 +670,14 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 }
             }
             ptx::mbar_wait(bar(BR::LFULL), I & 1);
-            const float l = lsm[row];
+            const float l = lsm[side * 64 + r];
             __syncwarp();
             if (lane == 0)
                 ptx::mbar_arrive(bar(BR::LEMPTY));
             ++I;
             if (valid_row) {
-                const uint32_t orig = perm_src(L.perm[h], qb * 64 + rl);
-                float4* dst = reinterpret_cast<float4*>(P.out + ((size_t)h * L.N + orig) * D);
+                const uint32_t orig = perm_src(L.perm[x.h], qb * 64 + r);
+                float4* dst = reinterpret_cast<float4*>(P.out + ((size_t)x.h * L.N + orig) * D);
                 if (l == 0.f) {
 #pragma unroll
                     for (int c = 0; c < D / 4; ++c)
@@ -603,7 +693,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                     }
                 }
                 if (P.zeroed)
-                    P.zeroed[(size_t)h * L.N + orig] = l == 0.f ? 1 : 0;
+                    P.zeroed[(size_t)x.h * L.N + orig] = l == 0.f ? 1 : 0;
             }
         }
     }
@@ -616,8 +706,10 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
 
 // ---------------------------------------------------------------------------
 // Debug / parity: int32 S_g tiles for a list of (h, qb, bj) through the same
-// TMA maps, smem swizzle, descriptors and tcgen05 issue as K3. One CTA (4
-// warps) per tile; writes S[tile][g][row][col] for the 64 rows of qb.
+// TMA maps, smem swizzle, descriptors and M=64 tcgen05 issue as K3; even q-blocks
+// go to TMEM lane offset 0 (side A), odd ones to lane offset 16 (side B), so
+// both placements are checked. One CTA (4 warps) per tile; writes
+// S[tile][g][row][col].
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(128, 1)
@@ -626,10 +718,11 @@ __global__ void __launch_bounds__(128, 1)
     using C = K3Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t sq = sbase, sk = sbase + C::Q_BYTES;
+    const uint32_t sq = sbase, sk = sbase + C::QT_BYTES;
     const uint32_t bar_ld = sk + C::KV_BYTES, bar_mma = bar_ld + 8, tptr = bar_ld + 16;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t h = tiles[3 * blockIdx.x], qb = tiles[3 * blockIdx.x + 1], bj = tiles[3 * blockIdx.x + 2];
+    const uint32_t side = qb & 1;
     if (threadIdx.x == 0) {
         ptx::mbar_init(bar_ld, 1);
         ptx::mbar_init(bar_mma, 1);
@@ -643,24 +736,24 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (tptr - sbase));
     if (threadIdx.x == 0) {
         const int32_t row0 = (int32_t)(h * L.kb2 * 64);
-        ptx::mbar_arrive_expect_tx(bar_ld, C::Q_BYTES + C::KV_BYTES);
-        ptx::tma_load_2d(sq, &tm_q, 0, row0 + (int32_t)(qb / 2) * 128, bar_ld);
+        ptx::mbar_arrive_expect_tx(bar_ld, C::QT_BYTES + C::KV_BYTES);
+        ptx::tma_load_2d(sq, &tm_q, 0, row0 + (int32_t)qb * 64, bar_ld);
         ptx::tma_load_2d(sk, &tm_k, 0, row0 + (int32_t)bj * 64, bar_ld);
         ptx::mbar_wait(bar_ld, 0);
         ptx::tc_fence_after();
-        issue_qk<D>(tmem, sq, sk);
+        issue_qk<D>(tmem + (side ? C::LANE16 : 0u), sq, sk);
         ptx::mma_commit(bar_mma);
     }
     ptx::mbar_wait(bar_mma, 0);
     ptx::tc_fence_after();
-    const uint32_t row = warp * 32 + lane;
+    const uint32_t row = warp * 16 + (lane & 15);
     for (int g = 0; g < C::G; ++g)
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t raw[32];
             ptx::tmem_ld32(tmem + ((warp * 32) << 16) + g * 64 + h2 * 32, raw);
             ptx::tmem_ld_wait();
-            if ((row >> 6) == (qb & 1)) {
-                int32_t* dst = S + (((size_t)blockIdx.x * C::G + g) * 64 + (row & 63)) * 64 + h2 * 32;
+            if ((uint32_t)(lane >> 4) == side) {
+                int32_t* dst = S + (((size_t)blockIdx.x * C::G + g) * 64 + row) * 64 + h2 * 32;
                 for (int j = 0; j < 32; ++j)
                     dst[j] = (int32_t)raw[j];
             }
@@ -704,11 +797,11 @@ cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUte
     if (n_tiles == 0)
         return cudaSuccess;
     if (L.D == 64) {
-        const uint32_t smem = K3Cfg<64>::Q_BYTES + K3Cfg<64>::KV_BYTES + 64;
+        const uint32_t smem = K3Cfg<64>::QT_BYTES + K3Cfg<64>::KV_BYTES + 64;
         cudaFuncSetAttribute(k3_debug_qk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k3_debug_qk<64><<<n_tiles, 128, smem, st>>>(L, tq, tk, tiles, S);
     } else {
-        const uint32_t smem = K3Cfg<128>::Q_BYTES + K3Cfg<128>::KV_BYTES + 64;
+        const uint32_t smem = K3Cfg<128>::QT_BYTES + K3Cfg<128>::KV_BYTES + 64;
         cudaFuncSetAttribute(k3_debug_qk<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k3_debug_qk<128><<<n_tiles, 128, smem, st>>>(L, tq, tk, tiles, S);
     }

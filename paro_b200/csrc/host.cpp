@@ -296,6 +296,7 @@ void free_layer(paro_layer* l) {
     cudaFree(l->L.qsc);
     cudaFree(l->L.meta);
     cudaFree(l->L.items);
+    cudaFree(l->L.pairs);
     cudaFree(l->L.pair_count);
     cudaFree(l->L.qb_count);
     cudaFree(l->L.order);
@@ -673,7 +674,8 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
             L.v = dalloc<int8_t>(rows * head_dim);
             L.qsc = dalloc<float>((size_t)heads * L.kb2 * L.G);
             L.meta = dalloc<float>((size_t)heads * L.kb2 * paro::meta_stride(head_dim));
-            L.items = dalloc<uint16_t>((size_t)heads * L.np * L.kb);
+            L.items = dalloc<uint16_t>((size_t)heads * L.kb * L.kb);
+            L.pairs = dalloc<uint32_t>((size_t)heads * L.np);
             L.pair_count = dalloc<uint32_t>((size_t)heads * L.np);
             L.qb_count = dalloc<uint32_t>((size_t)heads * L.kb2);
             L.order = dalloc<uint32_t>((size_t)heads * L.np);
@@ -683,10 +685,11 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
             cuda_check(cudaMemset(L.q, 0, rows * head_dim), "cudaMemset");
             cuda_check(cudaMemset(L.k, 0, rows * head_dim), "cudaMemset");
             cuda_check(cudaMemset(L.v, 0, rows * head_dim), "cudaMemset");
+            cuda_check(cudaMemset(L.qb_count, 0, (size_t)heads * L.kb2 * 4), "cudaMemset");
             cuda_check(cudaMemcpy(L.perm, l->perm_host.data(), heads * sizeof(PermDesc), cudaMemcpyHostToDevice),
                        "cudaMemcpy perm");
             cuda_check(paro::launch_perm_tables(L.perm, heads, L.N, l->fwd, l->inv, 0), "perm tables");
-            encode_codes_map(ctx, &l->tm_q, L.q, head_dim, rows, 128);
+            encode_codes_map(ctx, &l->tm_q, L.q, head_dim, rows, 64);
             encode_codes_map(ctx, &l->tm_k, L.k, head_dim, rows, 64);
             encode_codes_map(ctx, &l->tm_v, L.v, head_dim, rows, 64);
             cuda_check(cudaDeviceSynchronize(), "layer init");

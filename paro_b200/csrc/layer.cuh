@@ -1,19 +1,21 @@
 // layer.cuh -- HBM layout shared by the host orchestration and the kernels.
 //
 // All per-layer device state for H heads of N tokens, head dim D in {64,128},
-// block 64, kb = ceil(N/64) key/query blocks, kb2 = kb rounded up to even (q
-// blocks are processed in pairs, A = 2p and B = 2p+1, so K3 can run M = 128
-// tcgen05 MMAs over the union of the pair's kept key blocks).
+// block 64, kb = ceil(N/64) key/query blocks, kb2 = kb rounded up to even.
+// K3 runs two q-blocks of a head per work item (A in TMEM lanes 0-15 of each
+// lane quadrant, B in lanes 16-31, independent M = 64 tcgen05 MMAs), so K2
+// pairs q-blocks of a head with similar kept counts.
 //
 //   codes  q/k/v  int8 [H][kb2*64][D]  PERMUTED token order, zero-padded rows
 //   qsc          fp32 [H][kb2][G]     Q scale per (block, 64-column group), G = D/64
 //   meta         fp32 [H][kb2][4 + D] per key block: {ksc[0], ksc[1], vsc, 0, colsum[D]}
 //                                      (colsum = sum of V codes per column, exact in fp32)
 //   perm         PermDesc [H]          permuted index -> original token (div/mod form)
-//   items        u16  [H][np][kb]       per q-block pair: union of kept key blocks,
-//                                      bits 0..13 = key block, bit 14 = A keeps, bit 15 = B keeps
-//   pair_count   u32  [H][np]          entries used in items
+//   items        u16  [H][kb][kb]       per q-block: kept key blocks, ascending
 //   qb_count     u32  [H][kb2]         kept key blocks per q block (0 => zeroed rows)
+//   pairs        u32  [H][np]          q-block pair p: A | B << 16 (B = 0xffff: none);
+//                                      q-blocks sorted by kept count, neighbours paired
+//   pair_count   u32  [H][np]          max(count A, count B) = K3 steps of the pair
 //   order        u32  [H*np]           work items (h << 16 | p), longest first (LPT)
 #pragma once
 #include <cstdint>
@@ -46,6 +48,7 @@ struct LayerDev {
     float* qsc;
     float* meta;
     uint16_t* items;
+    uint32_t* pairs;
     uint32_t* pair_count;
     uint32_t* qb_count;
     uint32_t* order;

@@ -263,66 +263,92 @@ __global__ void k_perm_tables(const PermDesc* __restrict__ perm, uint32_t H, uin
 }
 
 // ---------------------------------------------------------------------------
-// K2a. One CTA (128 threads) per (head, q-block pair). Walks the two mask rows
-// (BlockMask::bits, one byte per block, mask.hpp:15-32) and writes the union of
-// kept key blocks in ascending order with per-q-block keep flags; also the
-// per-q-block kept counts (a row block with 0 kept blocks is zeroed and
+// K2a. One CTA (128 threads) per (head, q-block): compacts the mask row
+// (BlockMask::bits, one byte per block, mask.hpp:15-32) into the ascending list
+// of kept key blocks and its count (a q-block with 0 kept blocks is zeroed and
 // flagged, attention.cpp:242-247). bits == nullptr means all blocks kept.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k2_pair_lists(LayerDev L, const uint8_t* __restrict__ bits) {
-    const uint32_t p = blockIdx.x, h = blockIdx.y;
-    const uint32_t A = 2 * p, B = 2 * p + 1;
-    const bool hasB = B < L.kb;
+__global__ void __launch_bounds__(128) k2_qblock_lists(LayerDev L, const uint8_t* __restrict__ bits) {
+    const uint32_t qb = blockIdx.x, h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __shared__ uint32_t s_warp[4][3];
-    __shared__ uint32_t s_base[3];
+    __shared__ uint32_t s_warp[4];
+    __shared__ uint32_t s_base;
     if (tid == 0)
-        s_base[0] = s_base[1] = s_base[2] = 0;
+        s_base = 0;
     __syncthreads();
-    const uint8_t* rowA = bits ? bits + ((size_t)h * L.kb + A) * L.kb : nullptr;
-    const uint8_t* rowB = (bits && hasB) ? bits + ((size_t)h * L.kb + B) * L.kb : nullptr;
-    uint16_t* out = L.items + ((size_t)h * L.np + p) * L.kb;
+    const uint8_t* row = bits ? bits + ((size_t)h * L.kb + qb) * L.kb : nullptr;
+    uint16_t* out = L.items + ((size_t)h * L.kb + qb) * L.kb;
     for (uint32_t c0 = 0; c0 < L.kb; c0 += 128) {
         const uint32_t j = c0 + tid;
-        bool a = false, bb = false;
-        if (j < L.kb) {
-            a = rowA ? rowA[j] != 0 : true;
-            bb = hasB ? (rowB ? rowB[j] != 0 : true) : false;
-        }
-        const bool any = a || bb;
-        const uint32_t mu = __ballot_sync(0xffffffffu, any);
-        const uint32_t ma = __ballot_sync(0xffffffffu, a);
-        const uint32_t mb = __ballot_sync(0xffffffffu, bb);
-        if (lane == 0) {
-            s_warp[warp][0] = __popc(mu);
-            s_warp[warp][1] = __popc(ma);
-            s_warp[warp][2] = __popc(mb);
-        }
+        const bool keep = j < L.kb && (row ? row[j] != 0 : true);
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0)
+            s_warp[warp] = __popc(m);
         __syncthreads();
-        uint32_t off = s_base[0];
+        uint32_t off = s_base;
         for (int w = 0; w < warp; ++w)
-            off += s_warp[w][0];
-        if (any) {
-            const uint32_t pos = off + __popc(mu & ((1u << lane) - 1u));
-            out[pos] = (uint16_t)(j | (a ? 0x4000u : 0u) | (bb ? 0x8000u : 0u));
-        }
+            off += s_warp[w];
+        if (keep)
+            out[off + __popc(m & ((1u << lane) - 1u))] = (uint16_t)j;
         __syncthreads();
         if (tid == 0)
-            for (int w = 0; w < 4; ++w) {
-                s_base[0] += s_warp[w][0];
-                s_base[1] += s_warp[w][1];
-                s_base[2] += s_warp[w][2];
-            }
+            s_base += s_warp[0] + s_warp[1] + s_warp[2] + s_warp[3];
         __syncthreads();
     }
-    if (tid == 0) {
-        L.pair_count[(size_t)h * L.np + p] = s_base[0];
-        L.qb_count[(size_t)h * L.kb2 + A] = s_base[1];
-        L.qb_count[(size_t)h * L.kb2 + B] = s_base[2];
+    if (tid == 0)
+        L.qb_count[(size_t)h * L.kb2 + qb] = s_base;
+}
+
+// K2b. One CTA per head: stable counting sort of the head's q-blocks by kept
+// count (descending); neighbours become a K3 work pair, so the two
+// independent pipelines of a pair run nearly the same number of steps.
+__global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
+    extern __shared__ uint32_t s_buf[]; // hist[kb + 1] then sorted[kb]
+    uint32_t* hist = s_buf;
+    uint32_t* sorted = s_buf + L.kb + 1;
+    const uint32_t h = blockIdx.x;
+    const uint32_t* cnt = L.qb_count + (size_t)h * L.kb2;
+    for (uint32_t i = threadIdx.x; i <= L.kb; i += blockDim.x)
+        hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < L.kb; i += blockDim.x)
+        atomicAdd(&hist[cnt[i]], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int key = (int)L.kb; key >= 0; --key) {
+            const uint32_t c = hist[key];
+            hist[key] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) { // stable placement, one warp walking q-blocks in order
+        const uint32_t lane = threadIdx.x;
+        for (uint32_t base = 0; base < L.kb; base += 32) {
+            const uint32_t i = base + lane;
+            const bool valid = i < L.kb;
+            const uint32_t key = valid ? cnt[i] : 0xffffffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const uint32_t pos = valid ? hist[key] + __popc(peers & ((1u << lane) - 1u)) : 0;
+            __syncwarp();
+            if (valid && lane == (uint32_t)(__ffs(peers) - 1))
+                hist[key] += __popc(peers);
+            __syncwarp();
+            if (valid)
+                sorted[pos] = i;
+        }
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < L.np; p += blockDim.x) {
+        const uint32_t a = sorted[2 * p];
+        const uint32_t b = 2 * p + 1 < L.kb ? sorted[2 * p + 1] : 0xffffu;
+        L.pairs[(size_t)h * L.np + p] = a | (b << 16);
+        L.pair_count[(size_t)h * L.np + p] = cnt[a]; // sorted descending: A has the larger count
     }
 }
 
-// K2b. Single CTA: counting sort of the H*np work items by union length,
+// K2c. Single CTA: counting sort of the H*np work items by step count,
 // longest first (LPT order for K3's cyclic distribution). Ties are ordered
 // by (h, p) via a stable in-bucket rank, so the order is deterministic.
 __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
@@ -400,9 +426,13 @@ cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uin
 }
 
 cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
-    dim3 grid(L.np, L.H);
-    k2_pair_lists<<<grid, 128, 0, st>>>(L, bits);
+    dim3 grid(L.kb, L.H);
+    k2_qblock_lists<<<grid, 128, 0, st>>>(L, bits);
     cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return e;
+    k2_pair_qblocks<<<L.H, 256, (2 * L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
     k2_work_order<<<1, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
