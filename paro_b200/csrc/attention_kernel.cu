@@ -40,6 +40,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "layer.cuh"
 #include "ptx.cuh"
@@ -60,16 +62,17 @@ struct K3Cfg {
     static constexpr uint32_t TM_S = 0;          // two S buffers
     static constexpr uint32_t TM_O = 2 * S_COLS; // two O buffers
     static constexpr uint32_t TMEM_COLS = (2 * S_COLS + 2 * D) <= 256 ? 256 : 512;
-    static constexpr uint32_t OFF_Q = 0; // A at +0, B at +QT_BYTES
-    static constexpr uint32_t OFF_STAGE = 2 * QT_BYTES;
+    static constexpr uint32_t OFF_Q = 0; // [2 item buffers][A, B] q-block tiles
+    static constexpr uint32_t OFF_STAGE = 4 * QT_BYTES;
     // within a stage: K_A, K_B, V_A, V_B, meta_A, meta_B
     static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES; // [2 buf][2 side]
     static constexpr uint32_t OFF_ROWMETA = OFF_P + 4 * P_BYTES;     // [2 buf][2 side][64] float4
     static constexpr uint32_t OFF_U = OFF_ROWMETA + 2 * 2 * 64 * 16;  // [2 buf][2 side][D]
     static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;        // [2 parity][4 quad][2 side] float2
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 side][64]
-    static constexpr uint32_t OFF_BAR = OFF_L + 2 * 64 * 4;
-    static constexpr uint32_t NBAR = 2 + 2 * NS + 13;
+    static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
+    static constexpr uint32_t OFF_BAR = OFF_ROWSTAT + 2 * 2 * 64 * 40;
+    static constexpr uint32_t NBAR = 2 + 2 * NS + 15;
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
     // swizzle: rows of D int8 -> 64B (D=64) or 128B (D=128) swizzle atoms of 8 rows
@@ -85,7 +88,8 @@ template <int NS>
 struct Bars {
     static constexpr uint32_t KVFULL = 2, KVEMPTY = 2 + NS, SFULL = 2 + 2 * NS, SEMPTY = SFULL + 2,
                               PFULL = SEMPTY + 2, PEMPTY = PFULL + 2, OFULL = PEMPTY + 2, OEMPTY = OFULL + 2,
-                              LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1;
+                              LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1,
+                              QFULL1 = RED + 1, QEMPTY1 = RED + 2;
 };
 
 // K-major operand rows of D bytes (Q, K): SBO = one 8-row atom.
@@ -162,11 +166,13 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
 
 struct K3Params {
     LayerDev L;
+    double scale64;   // effective scale (AttnInputs::effective_scale, fp64)
     float scale_log2; // effective scale * log2(e)
     float p_qmax;     // 255 or 15
     float* out;       // [H][N][D] original token order
     uint8_t* zeroed;  // [H][N] or null
     uint32_t n_items;
+    unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
 };
 
 struct Item {
@@ -195,9 +201,6 @@ __device__ __forceinline__ Item load_item(const LayerDev& L, uint32_t it) {
 // has no tile this step (`live` false) run the same instructions but change
 // no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
-struct RowState {
-    float m, l;
-};
 
 // wait for several mbarrier phases, issuing the probes back to back so their
 // latencies overlap (each try_wait costs ~90 cycles even when already complete)
@@ -222,23 +225,99 @@ __device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1
         ptx::mbar_wait(b2, p2);
 }
 
-// The P group's min/max is a reduction over 64 rows spread across the 4
-// softmax warps. It is split-phase: each warp publishes its half-warp extremes
-// and arrives on an mbarrier, then computes all p values (the MUFU-bound part)
-// before it waits for the other warps, so the cross-warp latency hides behind
-// exp2 work. The S buffer is released right after p is formed.
+__device__ __forceinline__ uint64_t fma2_rm(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Per-row, per-step exact statistics published for the boundary path (d=64):
+// the exact (fp64, reference-order) min / max logit of the row's tile and the
+// running max after it.
+struct RowStat { // 40 bytes
+    double tmin, tmax, m;
+    float pmin, pmax; // the fast path's fp32 row extremes (candidate selection)
+    int valid, pad;
+};
+static_assert(sizeof(RowStat) == 40, "RowStat layout");
+
+constexpr double kLog2e = 1.4426950408889634;
+// Relative band of the fast-path quotient q = (p - lo) / pscale at d=64. The
+// fp32 path forms the exp2 argument as (S - smax) * c + d with d = exact
+// (tmax - m) * log2e, so its error is ~6e-8 * |arg| + the ex2.approx error
+// (~2.4e-7); with lo/hi from the same formula the quotient is within ~4-6e-7
+// of the reference's. A code is trusted only if q*(1-kappa) and q*(1+kappa)
+// round to the same integer, else it is recomputed exactly in fp64.
+// Measured on c2/c3 (8M sampled elements each): kappa 0 leaves code flips
+// (max|dO|/max|O| 5.8e-4 INT8, 6.4e-3 INT4); 4e-7 and 8e-7 are exact.
+#ifndef PARO_KAPPA
+#define PARO_KAPPA 6e-7f
+#endif
+constexpr float kKappa = PARO_KAPPA;
+
+// int32 S of (row r, key j) recomputed from the smem Q/K tiles (64-byte rows, 64B swizzle)
+__device__ __forceinline__ int32_t dot_row64(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t j) {
+    const uint8_t* qr = qtile + (r >> 3) * 512 + (r & 7) * 64;
+    const uint8_t* kr = ktile + (j >> 3) * 512 + (j & 7) * 64;
+    int32_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int4 a = *reinterpret_cast<const int4*>(qr + ((c ^ ((r >> 1) & 3)) << 4));
+        const int4 b = *reinterpret_cast<const int4*>(kr + ((c ^ ((j >> 1) & 3)) << 4));
+        acc = __dp4a(a.x, b.x, acc);
+        acc = __dp4a(a.y, b.y, acc);
+        acc = __dp4a(a.z, b.z, acc);
+        acc = __dp4a(a.w, b.w, acc);
+    }
+    return acc;
+}
+
+// round-half-away of q >= 0 exactly as std::round (kernels_scalar.cpp:84)
+__device__ __forceinline__ uint32_t round_half_away_pos(float q) {
+    float t = truncf(q);
+    if (__fsub_rn(q, t) >= 0.5f)
+        t = __fadd_rn(t, 1.0f);
+    return (uint32_t)t;
+}
+
+// ---------------------------------------------------------------------------
+// Softmax, one step for this thread's row (v3 order: pass 1 extremes -> group
+// reduction -> pass 2 p / codes).
+//   d=64 (G=1): the row extremes are integer maxima of S, so the reference's
+//   exact fp64 logits of the extremes and the exact running max m64 are known
+//   every step. P codes are made BIT-EXACT with the reference's fp32
+//   quantizer of the fp64 p: the fast path computes each code twice from
+//   (1 -/+ kappa)-perturbed quotients (one packed FFMA2.RM per element); where
+//   the two differ (~1e-4 of elements) the code is recomputed in fp64 from the
+//   exact tile lo/hi (from every row's published extremes) and S re-derived
+//   with dp4a from the Q/K tiles still in smem.
+//   d=128 (G=2): fp32 fast path only (codes tolerance-level).
+// Lanes whose q-block has no tile this step (`live` false) run the same
+// instructions but change no state and contribute neutral extremes.
+// ---------------------------------------------------------------------------
+struct RowState {
+    float m32, l;
+    double m64;
+};
+
 template <int D, bool TAIL>
-__device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1, uint32_t ncol, bool live,
-                                             bool valid_row, RowState& st, float p_qmax, float2* red_w,
-                                             const float2* red_r, uint32_t red_bar, uint32_t red_phase,
-                                             uint32_t sempty_bar, uint8_t* prow, uint32_t r, float& gamma_out,
-                                             float& lo_out, float& pscale_out) {
+__device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
+                                             float scale_log2, uint32_t ncol, bool live, bool valid_row,
+                                             RowState& st, float p_qmax, float2* red_w, const float2* red_r,
+                                             RowStat* rs_w, const RowStat* rs_r, uint32_t side,
+                                             const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
+                                             float sq1, float& gamma_out, float& lo_out, float& pscale_out,
+                                             unsigned long long* stats) {
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
-    // -------- pass 1: row extremes (4 independent chains per pass)
-    float m_new, pmax_r, pmin_r;
+    const bool valid = live && valid_row;
+    // -------- pass 1: row extremes (4 independent chains)
+    float m32, pmax_r, pmin_r, c0, c1 = 0.f, dmax = 0.f;
+    int32_t smax_i = 0;
+    double a64 = 0.0, m64 = st.m64;
     if (G == 1) {
-        int32_t mx[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN}, mn[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+        int32_t mx[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN},
+                mn[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t x[32];
@@ -254,11 +333,24 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1
         }
         const int32_t smax = max(max(mx[0], mx[1]), max(mx[2], mx[3]));
         const int32_t smin = min(min(mn[0], mn[1]), min(mn[2], mn[3]));
-        const float tm = __int2float_rn(smax) * c0;
-        m_new = fmaxf(st.m, tm);
-        pmax_r = ex2(fmaf(__int2float_rn(smax), c0, -m_new));
-        pmin_r = ex2(fmaf(__int2float_rn(smin), c0, -m_new));
+        // reference order: logit = scale * ((sq * sk) * S) in fp64 (paro_oracle.c, attention.cpp:166)
+        a64 = __dmul_rn((double)sq, (double)sk0);
+        const double tmax64 = __dmul_rn(scale64, __dmul_rn(a64, (double)smax));
+        const double tmin64 = __dmul_rn(scale64, __dmul_rn(a64, (double)smin));
+        if (live)
+            m64 = fmax(st.m64, tmax64);
+        c0 = (float)(__dmul_rn(__dmul_rn(scale64, a64), kLog2e));
+        m32 = (float)(m64 * kLog2e);
+        // exp2 argument of element j = (S_j - smax) * c0 + dmax: exact integer
+        // difference, dmax = (tmax - m) * log2e from the fp64 logits
+        dmax = (float)((tmax64 - m64) * kLog2e);
+        smax_i = smax;
+        pmax_r = ex2(dmax);
+        pmin_r = ex2(fmaf(__int2float_rn(smin - smax), c0, dmax));
+        *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
     } else {
+        c0 = scale_log2 * sq * sk0;
+        c1 = scale_log2 * sq1 * sk1;
         float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -277,16 +369,16 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1
         }
         const float ymax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         const float ymin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
-        m_new = fmaxf(st.m, ymax);
-        pmax_r = ex2(ymax - m_new);
-        pmin_r = ex2(ymin - m_new);
+        m32 = live ? fmaxf(st.m32, ymax) : st.m32;
+        pmax_r = ex2(ymax - m32);
+        pmin_r = ex2(ymin - m32);
     }
-    const float gamma = st.l > 0.f ? ex2(st.m - m_new) : 1.0f;
-    if (!(live && valid_row)) {
+    const float gamma = st.l > 0.f ? ex2(st.m32 - m32) : 1.0f;
+    if (!valid) {
         pmin_r = INFINITY;
         pmax_r = 0.f;
     }
-    // -------- publish the half-warp extremes (16 rows of each q-block per warp)
+    // -------- P group extremes over the q-block's 64 rows: 16 lanes x 4 warps
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
         pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
@@ -294,56 +386,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1
     }
     if ((lane & 15) == 0)
         *red_w = make_float2(pmin_r, pmax_r);
-    __syncwarp();
-    if (lane == 0)
-        ptx::mbar_arrive(red_bar);
-    // -------- pass 2a: p and the row sum (independent of lo/hi)
-    float pv[64];
-    uint64_t sum2 = pk(0.f, 0.f);
-    const uint64_t c00 = pk(c0, c0), nm = pk(-m_new, -m_new);
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-        if (G == 1) {
-            uint32_t x[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, x);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const uint64_t y2 =
-                    fma2(pk(__int2float_rn((int32_t)x[2 * k]), __int2float_rn((int32_t)x[2 * k + 1])), c00, nm);
-                float ya, yb;
-                upk(y2, ya, yb);
-                pv[h2 * 32 + 2 * k] = ex2(ya);
-                pv[h2 * 32 + 2 * k + 1] = ex2(yb);
-            }
-        } else {
-            uint32_t x0[32], x1[32];
-            ptx::tmem_ld32(s_addr + h2 * 32, x0);
-            ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
-                pv[h2 * 32 + j] = ex2(y - m_new);
-            }
-        }
-    }
-    // S no longer needed: release the TMEM buffer to the QK issuer
-    ptx::tc_fence_before();
-    __syncwarp();
-    if (lane == 0)
-        ptx::mbar_arrive(sempty_bar);
-    if (TAIL) {
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-            if ((uint32_t)j >= ncol)
-                pv[j] = 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-        sum2 = add2(sum2, pk(pv[2 * k], pv[2 * k + 1]));
-    // -------- group extremes from all four warps
-    ptx::mbar_wait(red_bar, red_phase);
+    ptx::named_bar_sync(1, 128);
     float lo = red_r[0].x, hi = red_r[0].y;
 #pragma unroll
     for (int q = 1; q < 4; ++q) {
@@ -354,37 +397,192 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float c0, float c1
     if (pscale == 0.f)
         pscale = 1.f;
     const float inv = __frcp_rn(pscale);
-    // -------- pass 2b: codes
-    const uint64_t nlo = pk(-lo, -lo), inv2 = pk(inv, inv);
-    const uint64_t half2 = pk(0.5f, 0.5f), magic2 = pk(8388608.0f, 8388608.0f);
+    // -------- pass 2: p, row sum, codes (two perturbed variants per element)
+    const float kap = G == 1 ? kKappa : 0.f; // d=128: single (unperturbed) code, no exact path
+    const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
+    const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
+    const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
+    const uint64_t c00 = pk(c0, c0), nm = pk(dmax, dmax);
+    uint64_t sum2 = pk(0.f, 0.f);
+    uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t w[8];
+        float pv[32];
+        if (G == 1) {
+            uint32_t x[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x);
+            ptx::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const uint64_t p2 = pk(pv[h2 * 32 + 2 * k], pv[h2 * 32 + 2 * k + 1]);
-            // q = (p - lo) * (1/pscale); code = floor(q + 0.5) via two round-down adds
-            const uint64_t u2 = add2_rm(add2_rm(mul2(add2(p2, nlo), inv2), half2), magic2);
-            float ua, ub;
-            upk(u2, ua, ub);
-            const uint32_t pair = __byte_perm(__float_as_uint(ua), __float_as_uint(ub), 0x0040);
-            if (k & 1)
-                w[k >> 1] = __byte_perm(w[k >> 1], pair, 0x5410);
-            else
-                w[k >> 1] = pair;
+            for (int k = 0; k < 16; ++k) {
+                const uint64_t y2 = fma2(pk(__int2float_rn((int32_t)x[2 * k] - smax_i),
+                                            __int2float_rn((int32_t)x[2 * k + 1] - smax_i)),
+                                         c00, nm);
+                float ya, yb;
+                upk(y2, ya, yb);
+                pv[2 * k] = ex2(ya);
+                pv[2 * k + 1] = ex2(yb);
+            }
+        } else {
+            uint32_t x0[32], x1[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x0);
+            ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
+                pv[j] = ex2(y - m32);
+            }
+        }
+        if (TAIL) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if ((uint32_t)(h2 * 32 + j) >= ncol)
+                    pv[j] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            sum2 = add2(sum2, pk(pv[2 * k], pv[2 * k + 1]));
+        if (TAIL) { // padded keys quantize as p = lo (code 0 in both variants; V rows are zero)
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if ((uint32_t)(h2 * 32 + j) >= ncol)
+                    pv[j] = lo;
+        }
+        uint32_t whi[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t hi4 = 0, lo4 = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = 4 * w + e;
+                // variants (q(1-kappa), q(1+kappa)) of element k; floor(. + 0.5) via round-down adds
+                const uint64_t u2 = add2_rm(fma2_rm(pk(pv[k], pv[k]), A2, B2), magic2);
+                float ul, uh;
+                upk(u2, ul, uh);
+                if (e == 0) {
+                    hi4 = __float_as_uint(uh);
+                    lo4 = __float_as_uint(ul);
+                } else { // insert byte 0 of the code word at byte e
+                    const uint32_t sel = e == 1 ? 0x3240u : (e == 2 ? 0x3410u : 0x4210u);
+                    hi4 = __byte_perm(hi4, __float_as_uint(uh), sel);
+                    lo4 = __byte_perm(lo4, __float_as_uint(ul), sel);
+                }
+            }
+            whi[w] = hi4;
+            if (G == 1 && hi4 != lo4)
+                risk |= 1u << (h2 * 8 + w);
         }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const int chunk = h2 * 2 + c;
             *reinterpret_cast<uint4*>(prow + ((chunk ^ ((r >> 1) & 3)) << 4)) =
-                make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+                make_uint4(whi[4 * c], whi[4 * c + 1], whi[4 * c + 2], whi[4 * c + 3]);
+        }
+    }
+    if (!valid)
+        risk = 0;
+    // -------- exact boundary path (d=64): rare, warp-uniform entry
+#ifdef PARO_K3_STATS
+    if (stats && lane == 0) {
+        atomicAdd(stats, 1ull);
+        const uint32_t any = __any_sync(0xffffffffu, risk != 0);
+        if (any)
+            atomicAdd(stats + 1, 1ull);
+    }
+    if (stats) {
+        const uint32_t nrisk = __popc(risk);
+        if (nrisk)
+            atomicAdd(stats + 2, (unsigned long long)nrisk);
+    }
+#endif
+    if (G == 1 && __any_sync(0xffffffffu, risk != 0)) {
+        // exact tile lo/hi of both q-blocks from every row's published extremes
+        // (only rows whose fast-path extreme is within 1e-5 of the fast tile
+        // extreme can hold the exact one: fp64 exp runs for those few rows, and
+        // only for the q-blocks that have a risky code in this warp)
+        const uint32_t rmask = __ballot_sync(0xffffffffu, risk != 0);
+        float lo_e[2] = {INFINITY, INFINITY}, hi_e[2] = {0.f, 0.f};
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+            if (!((sd ? rmask >> 16 : rmask & 0xffffu)))
+                continue;
+            float lo_a = red_r[-(int)side + sd].x, hi_a = red_r[-(int)side + sd].y;
+#pragma unroll
+            for (int q = 1; q < 4; ++q) {
+                lo_a = fminf(lo_a, red_r[-(int)side + sd + 2 * q].x);
+                hi_a = fmaxf(hi_a, red_r[-(int)side + sd + 2 * q].y);
+            }
+            float mn = INFINITY, mx = 0.f;
+            double args[4];
+            uint32_t kinds = 0, cnt = 0; // bit i: arg i is a max candidate
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const RowStat q = rs_r[sd * 64 + lane + 32 * k];
+                if (!q.valid)
+                    continue;
+                if (q.pmin <= lo_a * 1.00001f)
+                    args[cnt++] = q.tmin - q.m;
+                if (q.pmax >= hi_a * 0.99999f) {
+                    if (q.tmax == q.m)
+                        mx = 1.0f; // exp(0)
+                    else {
+                        kinds |= 1u << cnt;
+                        args[cnt++] = q.tmax - q.m;
+                    }
+                }
+            }
+            for (uint32_t it = 0; __any_sync(0xffffffffu, it < cnt); ++it) {
+                if (it < cnt) {
+                    const float e = (float)exp(args[it]);
+                    if ((kinds >> it) & 1u)
+                        mx = fmaxf(mx, e);
+                    else
+                        mn = fminf(mn, e);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            lo_e[sd] = mn;
+            hi_e[sd] = mx;
+        }
+        const float lo_x = side ? lo_e[1] : lo_e[0], hi_x = side ? hi_e[1] : hi_e[0];
+        float ps_x = __fdiv_rn(hi_x - lo_x, p_qmax);
+        if (ps_x == 0.f)
+            ps_x = 1.f;
+        while (risk) {
+            const int g = __ffs(risk) - 1;
+            risk &= risk - 1;
+#pragma unroll 1
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t j = 4 * g + e;
+                if (j >= ncol)
+                    continue;
+                const int32_t Sj = dot_row64(qtile, ktile, r, j);
+                { // re-run the two fast variants of this element; only a split pair needs fp64
+                    const float pf = ex2(fmaf(__int2float_rn(Sj - smax_i), c0, dmax));
+                    float ul, uh;
+                    upk(add2_rm(fma2_rm(pk(pf, pf), A2, B2), magic2), ul, uh);
+                    if (__float_as_uint(ul) == __float_as_uint(uh))
+                        continue;
+                }
+                const double logit = __dmul_rn(scale64, __dmul_rn(a64, (double)Sj));
+                const float p = (float)exp(logit - m64);
+                float q = __fdiv_rn(__fsub_rn(p, lo_x), ps_x);
+                q = fminf(p_qmax, fmaxf(0.f, q));
+                const int chunk = j >> 4;
+                prow[((chunk ^ ((r >> 1) & 3)) << 4) + (j & 15)] = (uint8_t)round_half_away_pos(q);
+            }
         }
     }
     float sa, sb;
     upk(sum2, sa, sb);
     if (live) {
         st.l = st.l * gamma + (sa + sb);
-        st.m = m_new;
+        st.m32 = m32;
+        st.m64 = m64;
     }
     gamma_out = gamma;
     lo_out = lo;
@@ -410,8 +608,13 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
     const LayerDev& L = P.L;
 
     if (threadIdx.x == 0) {
+        // Q tiles are double-buffered by item parity; a buffer is free once the
+        // item's last QK retired AND the softmax warps finished the item (the
+        // exact boundary path re-reads Q from smem)
         ptx::mbar_init(bar(B_QFULL), 1);
-        ptx::mbar_init(bar(B_QEMPTY), 1);
+        ptx::mbar_init(bar(B_QEMPTY), 1 + 4);
+        ptx::mbar_init(bar(BR::QFULL1), 1);
+        ptx::mbar_init(bar(BR::QEMPTY1), 1 + 4);
         for (int s = 0; s < NS; ++s) {
             ptx::mbar_init(bar(BR::KVFULL + s), 1);
             ptx::mbar_init(bar(BR::KVEMPTY + s), 1);
@@ -444,6 +647,9 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         return idx < P.n_items ? (int)L.order[idx] : -1;
     };
     auto stage = [&](uint32_t s) { return sbase + C::OFF_STAGE + s * C::STAGE_BYTES; };
+    auto qfull = [&](uint32_t i) { return bar((i & 1) ? BR::QFULL1 : (uint32_t)B_QFULL); };
+    auto qempty = [&](uint32_t i) { return bar((i & 1) ? BR::QEMPTY1 : (uint32_t)B_QEMPTY); };
+    auto qbuf = [&](uint32_t i) { return sbase + C::OFF_Q + (i & 1) * 2 * C::QT_BYTES; };
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -460,12 +666,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const uint16_t* la = L.items + ((size_t)x.h * L.kb + x.qa) * L.kb;
                 const uint16_t* lb = L.items + ((size_t)x.h * L.kb + (x.qb != 0xffffu ? x.qb : 0)) * L.kb;
                 const int32_t row0 = (int32_t)(x.h * L.kb2 * 64);
-                ptx::mbar_wait(bar(B_QEMPTY), (I & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(bar(B_QFULL), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
-                ptx::tma_load_2d(sbase + C::OFF_Q, &tm_q, 0, row0 + (int32_t)x.qa * 64, bar(B_QFULL));
+                ptx::mbar_wait(qempty(I), ((I >> 1) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(qfull(I), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
+                ptx::tma_load_2d(qbuf(I), &tm_q, 0, row0 + (int32_t)x.qa * 64, qfull(I));
                 if (x.qb != 0xffffu)
-                    ptx::tma_load_2d(sbase + C::OFF_Q + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64,
-                                     bar(B_QFULL));
+                    ptx::tma_load_2d(qbuf(I) + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
                 for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS;
                     ptx::mbar_wait(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
@@ -519,7 +724,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 if (it < 0)
                     continue;
                 const Item x = load_item(L, (uint32_t)it);
-                ptx::mbar_wait(bar(B_QFULL), I & 1);
+                ptx::mbar_wait(qfull(I), (I >> 1) & 1);
                 ptx::tc_fence_after();
                 for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS, b = T & 1;
@@ -527,20 +732,20 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                     ptx::mbar_wait(bar(BR::SEMPTY + b), ((T >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
                     if (t < x.na)
-                        issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, sbase + C::OFF_Q, stage(s));
+                        issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s));
                     if (t < x.nb)
-                        issue_qk<D>(tmem + C::LANE16 + C::TM_S + b * C::S_COLS, sbase + C::OFF_Q + C::QT_BYTES,
+                        issue_qk<D>(tmem + C::LANE16 + C::TM_S + b * C::S_COLS, qbuf(I) + C::QT_BYTES,
                                     stage(s) + C::KV_BYTES);
                     ptx::mma_commit(bar(BR::SFULL + b));
                     if (t + 1 == x.n)
-                        ptx::mma_commit(bar(B_QEMPTY));
+                        ptx::mma_commit(qempty(I));
                     if (t > 0)
                         issue_pv(T - 1, t - 1 < x.na, t - 1 < x.nb);
                 }
                 if (x.n > 0)
                     issue_pv(T - 1, x.n - 1 < x.na, x.n - 1 < x.nb);
                 else
-                    ptx::mma_commit(bar(B_QEMPTY));
+                    ptx::mma_commit(qempty(I));
                 ++I;
             }
         }
@@ -566,9 +771,10 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
             const uint32_t nmine = side ? x.nb : x.na;
             const uint16_t* list = L.items + ((size_t)x.h * L.kb + qb) * L.kb;
             const bool valid_row = has_qb && qb * 64 + r < L.N;
-            const float cq0 = P.scale_log2 * L.qsc[((size_t)x.h * L.kb2 + qb) * G];
-            const float cq1 = G == 2 ? P.scale_log2 * L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
-            RowState st{-INFINITY, 0.f};
+            const float sq0 = L.qsc[((size_t)x.h * L.kb2 + qb) * G];
+            const float sq1 = G == 2 ? L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
+            RowState st{-INFINITY, 0.f, -INFINITY};
+            RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
                 const bool live = t < nmine;
@@ -578,21 +784,28 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const float* meta =
                     reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES + 4 * C::KV_BYTES +
                                                    side * C::META_BYTES);
-                const float c0 = cq0 * meta[0];
-                const float c1 = G == 2 ? cq1 * meta[1] : 0.f;
                 uint8_t* prow = smem + C::OFF_P + (b * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
                 const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
                 float2* red_w = red + ((T & 1) * 4 + quad) * 2 + side;
                 const float2* red_r = red + (T & 1) * 8 + side;
                 const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
+                RowStat* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
+                const RowStat* rs_r = rowstat + (T & 1) * 128;
+                const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
+                const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
                 if (__any_sync(0xffffffffu, tail_tile))
-                    softmax_step<D, true>(s_addr, c0, c1, tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax,
-                                          red_w, red_r, bar(BR::RED), T & 1, bar(BR::SEMPTY + b), prow, r, gamma,
-                                          lo, pscale);
+                    softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
+                                          tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w,
+                                          rs_r, side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, P.stats);
                 else
-                    softmax_step<D, false>(s_addr, c0, c1, 64u, live, valid_row, st, P.p_qmax, red_w, red_r,
-                                           bar(BR::RED), T & 1, bar(BR::SEMPTY + b), prow, r, gamma, lo, pscale);
+                    softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, 64u, live,
+                                           valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile,
+                                           prow, r, sq1, gamma, lo, pscale, P.stats);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    ptx::mbar_arrive(bar(BR::SEMPTY + b));
                 const float vsc = meta[2];
                 rowmeta[(b * 2 + side) * 64 + r] =
                     make_float4(live ? gamma : 1.f, live ? pscale * vsc : 0.f, 0.f, live ? 1.f : 0.f);
@@ -607,6 +820,9 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 if (lane == 0)
                     ptx::mbar_arrive(bar(BR::PFULL + b));
             }
+            __syncwarp();
+            if (lane == 0)
+                ptx::mbar_arrive(qempty(I)); // this warp no longer reads the item's Q tiles
             ptx::mbar_wait(bar(BR::LEMPTY), (I & 1) ^ 1);
             lsm[side * 64 + r] = st.l;
             __syncwarp();
@@ -779,14 +995,30 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
 }
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      float scale_log2, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st) {
+                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st) {
     K3Params p;
     p.L = L;
-    p.scale_log2 = scale_log2;
+    p.scale64 = scale;
+    p.scale_log2 = (float)(scale * kLog2e);
     p.p_qmax = pv_bits == 4 ? 15.0f : 255.0f;
     p.out = out;
     p.zeroed = zeroed;
     p.n_items = L.H * L.np;
+    p.stats = nullptr;
+#ifdef PARO_K3_STATS
+    static unsigned long long* dstats = nullptr;
+    if (!dstats) {
+        cudaMalloc(&dstats, 32);
+        cudaMemset(dstats, 0, 32);
+    }
+    p.stats = dstats;
+    if (getenv("PARO_K3_STATS_PRINT")) {
+        unsigned long long h[3];
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, dstats, 24, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[k3 stats] warp-steps %llu exact-path %llu risky-groups %llu\n", h[0], h[1], h[2]);
+    }
+#endif
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);
     const int grid = (int)(p.n_items < slots ? p.n_items : slots);
     return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, grid, st) : launch_k3_t<128>(p, tq, tk, tv, grid, st);

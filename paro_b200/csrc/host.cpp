@@ -31,7 +31,7 @@ cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uin
                                cudaStream_t st);
 cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      float scale_log2, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st);
+                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st);
 cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
                             const uint32_t* tiles, int32_t* S, cudaStream_t st);
 } // namespace paro
@@ -330,10 +330,9 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
                                 std::to_string(l->last_v_bits) + " bits); rerun reorder_quantize");
     if (!out)
         fail(PARO_E_CONFIG, "null output");
-    // AttnInputs::effective_scale (attention.cpp:26-28), folded with log2(e) for ex2
+    // AttnInputs::effective_scale (attention.cpp:26-28), in fp64 exactly as the reference
     const double eff = scale != 0.0f ? (double)scale : 1.0 / std::sqrt((double)l->L.D);
-    const float scale_log2 = (float)(eff * 1.4426950408889634);
-    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, scale_log2, pv_bits, out, zeroed, l->ctx->num_sms, st),
+    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st),
                "k3_attention launch");
 }
 

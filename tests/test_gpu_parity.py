@@ -12,6 +12,14 @@ from conftest import randn, rel_err
 pytestmark = pytest.mark.gpu
 
 OUT_TOL = 1e-3  # max|dO| / max|O| (north_star)
+# d=64 P codes are bit-exact with the reference quantizer (boundary path), so the
+# only differences left are fp32 accumulation order: any single code flip would
+# exceed this bound.
+EXACT_TOL = 1e-5
+
+
+def tol(d):
+    return EXACT_TOL if d == 64 else OUT_TOL
 
 # (grid, heads, d, orders) -- c1 from BASELINE.configs[0] plus ragged / 2-D / d=128 shapes
 CASES = [
@@ -146,15 +154,15 @@ def test_attention_matches_oracle(paro, ctx, oracle, grid, H, d, orders, pv_bits
     kb = (paro.parse_grid(grid).token_count() + 63) // 64
     masks = random_masks(H, kb, 0.4, 7)
     err = run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv_bits, 31)
-    assert err <= OUT_TOL, err
+    assert err <= tol(d), err
 
 
 @pytest.mark.parametrize("d", [64, 128])
 def test_attention_dense_and_zeroed_rows(paro, ctx, oracle, d):
     grid, H, orders = "F:4,H:10,W:12", 2, ["HWF", "FWH"]  # N=480, kb=8
-    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, None, 8, 41) <= OUT_TOL
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, None, 8, 41) <= tol(d)
     masks = random_masks(H, 8, 0.3, 9, empty_row=3)
-    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, 8, 43) <= OUT_TOL
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, 8, 43) <= tol(d)
 
 
 def test_single_head_api_matches_oracle(paro, ctx, oracle):
@@ -164,7 +172,7 @@ def test_single_head_api_matches_oracle(paro, ctx, oracle):
     mask = paro.BlockMask(kb, kb, 64, random_masks(1, kb, 0.5, 4)[0])
     res = ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v), mask, paro.QuantConfig(8))
     ref, z = oracle.stream_engine(q, k, v, mask.bits, 8, qk_mode=1)
-    assert rel_err(res.output, ref) <= OUT_TOL
+    assert rel_err(res.output, ref) <= EXACT_TOL
     assert res.zeroed_rows == list(np.nonzero(z)[0])
 
 
