@@ -245,10 +245,10 @@ def main():
     g = paro.parse_grid(grid_text)
     N = g.token_count()
     kb = (N + 63) // 64
-    if H % world:
-        raise SystemExit(f"{H} heads do not split over {world} ranks")
-    hpr = H // world
-    my_heads = list(range(rank * hpr, (rank + 1) * hpr))
+    from paro_b200.sharding import shard_heads
+
+    my_heads = shard_heads(H, world, rank)  # no data-path collective
+    hpr = len(my_heads)
     orders_all = head_orders(paro, g, H)
     q, k, v, masks = build_inputs(paro, my_heads, N, d, density, args.mask_family)
     my_ops = sum(kept_ops(masks[i], N, d) for i in range(hpr))
