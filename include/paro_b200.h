@@ -162,9 +162,15 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
                        float scale, int pv_bits, float* out, uint8_t* zeroed);
 
 /* End to end from HOST buffers (pinned for full speed): H2D of Q/K/V, K1, K3,
- * D2H of O (and zeroed if non-NULL), synchronised before returning. */
+ * D2H of O (and zeroed if non-NULL), synchronised before returning. Heads are
+ * processed in chunks (default 8) whose uploads, kernels and downloads are
+ * pipelined on three streams. */
 int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
                             float scale, int pv_bits, float* out, uint8_t* zeroed);
+
+/* Number of head chunks forward_host pipelines (clamped to [1, heads]).
+ * Re-sorts the per-chunk work lists on `stream` if masks are already set. */
+int paro_layer_set_pipeline_chunks(paro_layer* layer, paro_stream_t stream, uint32_t chunks);
 
 /* ---- introspection for parity tests ---- */
 /* Device buffers owned by the layer (kb = ceil(N/64), kb2 = kb rounded up to

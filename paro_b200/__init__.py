@@ -545,6 +545,10 @@ class Layer:
         _check(_lib.paro_layer_forward(P(self.ptr), P(stream), P(dq), P(dk), P(dv), ctypes.c_float(scale),
                                        ctypes.c_int(pv_bits), P(dout), P(dzeroed) if dzeroed else None))
 
+    def set_pipeline_chunks(self, chunks: int, stream=None):
+        """Head chunks of the forward_host upload/compute/download pipeline."""
+        _check(_lib.paro_layer_set_pipeline_chunks(P(self.ptr), P(stream), U32(chunks)))
+
     def forward_host(self, q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float, pv_bits: int,
                      out: Optional[np.ndarray] = None, zeroed: Optional[np.ndarray] = None, stream=None):
         shape = (self.heads, self.N, self.head_dim)

@@ -171,6 +171,7 @@ struct K3Params {
     float p_qmax;     // 255 or 15
     float* out;       // [H][N][D] original token order
     uint8_t* zeroed;  // [H][N] or null
+    const uint32_t* order; // LPT-sorted work items (h << 16 | p) of this launch
     uint32_t n_items;
     unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
 };
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
     // snake dealing of the LPT-sorted work list
     auto item_at = [&](uint32_t r) -> int {
         const uint32_t idx = r * G_cta + ((r & 1) ? (G_cta - 1 - blockIdx.x) : blockIdx.x);
-        return idx < P.n_items ? (int)L.order[idx] : -1;
+        return idx < P.n_items ? (int)P.order[idx] : -1;
     };
     auto stage = [&](uint32_t s) { return sbase + C::OFF_STAGE + s * C::STAGE_BYTES; };
     auto qfull = [&](uint32_t i) { return bar((i & 1) ? BR::QFULL1 : (uint32_t)B_QFULL); };
@@ -809,12 +810,13 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const float vsc = meta[2];
                 rowmeta[(b * 2 + side) * 64 + r] =
                     make_float4(live ? gamma : 1.f, live ? pscale * vsc : 0.f, 0.f, live ? 1.f : 0.f);
-                // per-column offset term of this tile: (lo * vscale) * colsum[c] (0 when idle)
-                const float os = live ? lo * vsc : 0.f;
+                // per-column offset term of this tile: (lo * vscale) * colsum[c]; exactly 0
+                // when idle (an idle side's meta slot is not loaded: stale smem, maybe NaN)
+                const float os = lo * vsc;
                 float* u = usm + (b * 2 + side) * D;
 #pragma unroll
                 for (int c = 0; c < D / 64; ++c)
-                    u[r + 64 * c] = os * meta[4 + r + 64 * c];
+                    u[r + 64 * c] = live ? os * meta[4 + r + 64 * c] : 0.f;
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0)
@@ -995,7 +997,10 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
 }
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st) {
+                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      uint32_t head_begin, uint32_t head_count, bool chunked) {
+    if (head_count == 0)
+        return cudaSuccess;
     K3Params p;
     p.L = L;
     p.scale64 = scale;
@@ -1003,7 +1008,8 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
     p.p_qmax = pv_bits == 4 ? 15.0f : 255.0f;
     p.out = out;
     p.zeroed = zeroed;
-    p.n_items = L.H * L.np;
+    p.order = (chunked ? L.order_chunk : L.order) + (size_t)head_begin * L.np;
+    p.n_items = head_count * L.np;
     p.stats = nullptr;
 #ifdef PARO_K3_STATS
     static unsigned long long* dstats = nullptr;

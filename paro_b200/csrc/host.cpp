@@ -22,7 +22,8 @@
 #include "layer.cuh"
 
 namespace paro {
-cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits, cudaStream_t st);
+cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits,
+                      uint32_t head_begin, uint32_t head_count, cudaStream_t st);
 cudaError_t launch_quantize_sym(const float* in, uint32_t rows, uint32_t cols, int bits, int8_t* codes,
                                 float* scales, cudaStream_t st);
 cudaError_t launch_apply_perm_rows(const float* in, uint32_t rows, uint32_t cols, const uint32_t* inverse, float* out,
@@ -30,8 +31,10 @@ cudaError_t launch_apply_perm_rows(const float* in, uint32_t rows, uint32_t cols
 cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uint32_t* fwd, uint32_t* inv,
                                cudaStream_t st);
 cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st);
+cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st);
+                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      uint32_t head_begin, uint32_t head_count, bool chunked);
 cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
                             const uint32_t* tiles, int32_t* S, cudaStream_t st);
 } // namespace paro
@@ -262,9 +265,13 @@ struct paro_layer {
     // e2e staging
     float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
     uint8_t* dzero = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr; // H2D / D2H copy streams
+    std::vector<cudaEvent_t> ev;                  // [0] start, then per chunk: in, computed, out
 };
 
 namespace {
+
+constexpr uint32_t kDefaultChunks = 8; // host-buffer pipeline depth (paro_layer_set_pipeline_chunks)
 
 void set_device(const paro_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
@@ -309,6 +316,13 @@ void free_layer(paro_layer* l) {
     cudaFree(l->dv);
     cudaFree(l->dout);
     cudaFree(l->dzero);
+    cudaFree(l->L.order_chunk);
+    for (cudaEvent_t e : l->ev)
+        cudaEventDestroy(e);
+    if (l->s_in)
+        cudaStreamDestroy(l->s_in);
+    if (l->s_out)
+        cudaStreamDestroy(l->s_out);
 }
 
 void check_bits(int bits) {
@@ -321,7 +335,8 @@ void check_layer(const paro_layer* l) {
         fail(PARO_E_CONFIG, "null layer");
 }
 
-void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, float* out, uint8_t* zeroed) {
+void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, float* out, uint8_t* zeroed,
+                   uint32_t head_begin = 0, uint32_t head_count = ~0u, bool chunked = false) {
     check_bits(pv_bits);
     if (!l->masks_set)
         fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before attention");
@@ -332,7 +347,10 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
         fail(PARO_E_CONFIG, "null output");
     // AttnInputs::effective_scale (attention.cpp:26-28), in fp64 exactly as the reference
     const double eff = scale != 0.0f ? (double)scale : 1.0 / std::sqrt((double)l->L.D);
-    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st),
+    if (head_count == ~0u)
+        head_count = l->L.H;
+    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
+                               head_begin, head_count, chunked),
                "k3_attention launch");
 }
 
@@ -678,6 +696,8 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
             L.pair_count = dalloc<uint32_t>((size_t)heads * L.np);
             L.qb_count = dalloc<uint32_t>((size_t)heads * L.kb2);
             L.order = dalloc<uint32_t>((size_t)heads * L.np);
+            L.order_chunk = dalloc<uint32_t>((size_t)heads * L.np);
+            L.hpc = (heads + kDefaultChunks - 1) / kDefaultChunks;
             L.work_counter = dalloc<uint32_t>(1);
             l->fwd = dalloc<uint32_t>((size_t)heads * N);
             l->inv = dalloc<uint32_t>((size_t)heads * N);
@@ -746,7 +766,7 @@ int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const f
         if (!q || !k || !v)
             fail(PARO_E_CONFIG, "null Q/K/V");
         set_device(layer->ctx);
-        cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, (cudaStream_t)stream), "k1 launch");
+        cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, 0, layer->L.H, (cudaStream_t)stream), "k1 launch");
         layer->last_v_bits = v_bits;
     });
 }
@@ -769,13 +789,32 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
             fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
         set_device(layer->ctx);
         cudaStream_t st = (cudaStream_t)stream;
-        cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, st), "k1 launch");
+        cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, 0, layer->L.H, st), "k1 launch");
         layer->last_v_bits = pv_bits;
         run_attention(layer, st, scale, pv_bits, out, zeroed);
         layer->last_launches = 2;
     });
 }
 
+int paro_layer_set_pipeline_chunks(paro_layer* layer, paro_stream_t stream, uint32_t chunks) {
+    return guarded([&] {
+        check_layer(layer);
+        if (chunks == 0)
+            fail(PARO_E_CONFIG, "pipeline chunk count must be >= 1");
+        set_device(layer->ctx);
+        LayerDev& L = layer->L;
+        const uint32_t c = std::min(chunks, L.H);
+        L.hpc = (L.H + c - 1) / c;
+        if (layer->masks_set) // re-sort the per-chunk work lists for the new split
+            cuda_check(paro::launch_k2_order(L, (cudaStream_t)stream), "k2 order launch");
+    });
+}
+
+// Host-buffer forward. Heads are split into chunks of L.hpc; chunk c's Q/K/V
+// upload (stream s_in), K1 + K3 (caller's stream) and output download
+// (stream s_out) are event-chained so PCIe traffic in both directions
+// overlaps the kernels of the neighbouring chunks. Returns when `out` (and
+// `zeroed`) hold the result.
 int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
                             float scale, int pv_bits, float* out, uint8_t* zeroed) {
     return guarded([&] {
@@ -783,28 +822,58 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
         check_bits(pv_bits);
         if (!layer->masks_set)
             fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
+        if (!q || !k || !v || !out)
+            fail(PARO_E_CONFIG, "null Q/K/V/out");
         set_device(layer->ctx);
         cudaStream_t st = (cudaStream_t)stream;
         const LayerDev& L = layer->L;
-        const size_t elems = (size_t)L.H * L.N * L.D;
+        const size_t head_elems = (size_t)L.N * L.D;
+        const size_t elems = (size_t)L.H * head_elems;
         if (!layer->dq) {
             layer->dq = dalloc<float>(elems);
             layer->dk = dalloc<float>(elems);
             layer->dv = dalloc<float>(elems);
             layer->dout = dalloc<float>(elems);
             layer->dzero = dalloc<uint8_t>((size_t)L.H * L.N);
+            cuda_check(cudaStreamCreateWithFlags(&layer->s_in, cudaStreamNonBlocking), "stream create");
+            cuda_check(cudaStreamCreateWithFlags(&layer->s_out, cudaStreamNonBlocking), "stream create");
         }
-        cuda_check(cudaMemcpyAsync(layer->dq, q, elems * 4, cudaMemcpyHostToDevice, st), "H2D q");
-        cuda_check(cudaMemcpyAsync(layer->dk, k, elems * 4, cudaMemcpyHostToDevice, st), "H2D k");
-        cuda_check(cudaMemcpyAsync(layer->dv, v, elems * 4, cudaMemcpyHostToDevice, st), "H2D v");
-        cuda_check(paro::launch_k1(L, layer->dq, layer->dk, layer->dv, pv_bits, st), "k1 launch");
+        const uint32_t nchunks = (L.H + L.hpc - 1) / L.hpc;
+        while (layer->ev.size() < 1 + 3 * (size_t)nchunks) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+            layer->ev.push_back(e);
+        }
+        cudaEvent_t* ev = layer->ev.data();
+        // the copy streams start after everything already queued on the caller's stream (K2)
+        cuda_check(cudaEventRecord(ev[0], st), "event record");
+        cuda_check(cudaStreamWaitEvent(layer->s_in, ev[0], 0), "stream wait");
+        cuda_check(cudaStreamWaitEvent(layer->s_out, ev[0], 0), "stream wait");
         layer->last_v_bits = pv_bits;
-        run_attention(layer, st, scale, pv_bits, layer->dout, zeroed ? layer->dzero : nullptr);
-        cuda_check(cudaMemcpyAsync(out, layer->dout, elems * 4, cudaMemcpyDeviceToHost, st), "D2H out");
-        if (zeroed)
-            cuda_check(cudaMemcpyAsync(zeroed, layer->dzero, (size_t)L.H * L.N, cudaMemcpyDeviceToHost, st), "D2H zeroed");
+        for (uint32_t c = 0; c < nchunks; ++c) {
+            const uint32_t h0 = c * L.hpc, hn = std::min(L.hpc, L.H - h0);
+            const size_t off = (size_t)h0 * head_elems, bytes = (size_t)hn * head_elems * 4;
+            cudaEvent_t e_in = ev[1 + 3 * c], e_k = ev[2 + 3 * c], e_out = ev[3 + 3 * c];
+            cuda_check(cudaMemcpyAsync(layer->dq + off, q + off, bytes, cudaMemcpyHostToDevice, layer->s_in), "H2D q");
+            cuda_check(cudaMemcpyAsync(layer->dk + off, k + off, bytes, cudaMemcpyHostToDevice, layer->s_in), "H2D k");
+            cuda_check(cudaMemcpyAsync(layer->dv + off, v + off, bytes, cudaMemcpyHostToDevice, layer->s_in), "H2D v");
+            cuda_check(cudaEventRecord(e_in, layer->s_in), "event record");
+            cuda_check(cudaStreamWaitEvent(st, e_in, 0), "stream wait");
+            cuda_check(paro::launch_k1(L, layer->dq, layer->dk, layer->dv, pv_bits, h0, hn, st), "k1 launch");
+            run_attention(layer, st, scale, pv_bits, layer->dout, zeroed ? layer->dzero : nullptr, h0, hn, true);
+            cuda_check(cudaEventRecord(e_k, st), "event record");
+            cuda_check(cudaStreamWaitEvent(layer->s_out, e_k, 0), "stream wait");
+            cuda_check(cudaMemcpyAsync(out + off, layer->dout + off, bytes, cudaMemcpyDeviceToHost, layer->s_out),
+                       "D2H out");
+            if (zeroed)
+                cuda_check(cudaMemcpyAsync(zeroed + (size_t)h0 * L.N, layer->dzero + (size_t)h0 * L.N,
+                                           (size_t)hn * L.N, cudaMemcpyDeviceToHost, layer->s_out),
+                           "D2H zeroed");
+            cuda_check(cudaEventRecord(e_out, layer->s_out), "event record");
+        }
+        cuda_check(cudaStreamWaitEvent(st, ev[3 * nchunks], 0), "stream wait");
         cuda_check(cudaStreamSynchronize(st), "forward_host sync");
-        layer->last_launches = 2;
+        layer->last_launches = 2 * (int)nchunks;
     });
 }
 

@@ -51,7 +51,9 @@ struct LayerDev {
     uint32_t* pairs;
     uint32_t* pair_count;
     uint32_t* qb_count;
-    uint32_t* order;
+    uint32_t* order;       // [H*np] global LPT order (h << 16 | p)
+    uint32_t* order_chunk; // [H*np] per-chunk LPT order, chunk c = heads [c*hpc, (c+1)*hpc)
+    uint32_t hpc;          // heads per chunk of the host-buffer pipeline
     uint32_t* work_counter;
 };
 

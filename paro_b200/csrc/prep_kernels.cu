@@ -21,13 +21,22 @@ namespace paro {
 // quant_affine(x, 0, scale, -qmax, qmax) of kernels_scalar.cpp:78-85:
 // (x - 0)/scale in IEEE fp32, clamp to [-qmax, qmax] BEFORE rounding, round
 // half away from zero (std::round). x - 0.0f == x for every finite x.
-__device__ __forceinline__ int quant_sym(float x, float scale, float qmax) {
-    float q = __fdiv_rn(x, scale);
+//
+// The quotient is the correctly rounded x/scale without a per-element MUFU:
+// with rs = RN(1/scale) (one __frcp_rn per group), q0 = RN(x*rs) is within
+// 1 ulp and one FMA residual step gives RN(x/scale) (Markstein's theorem;
+// no overflow/underflow for the bounded quotients here -- a tiny x only
+// changes the sign of a zero code). Round-half-away of |q| uses two
+// round-down adds: floor(RD(|q| + 0.5)) == floor(|q| + 0.5), and
+// RD(t + 2^23) leaves floor(t) in the mantissa. No XU-pipe instruction.
+__device__ __forceinline__ int quant_sym(float x, float scale, float rs, float qmax) {
+    const float q0 = __fmul_rn(x, rs);
+    const float e = __fmaf_rn(-q0, scale, x);
+    float q = __fmaf_rn(e, rs, q0);
     q = fminf(qmax, fmaxf(-qmax, q));
-    float t = truncf(q);
-    if (fabsf(__fsub_rn(q, t)) >= 0.5f)
-        t = __fadd_rn(t, copysignf(1.0f, q));
-    return static_cast<int>(t);
+    const float t = __fadd_rd(fabsf(q), 0.5f);
+    const int m = (int)(__float_as_uint(__fadd_rd(t, 8388608.0f)) & 0x7fffffu);
+    return q < 0.0f ? -m : m;
 }
 
 __device__ __forceinline__ float4 ld_stream(const float* p) {
@@ -61,12 +70,12 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 template <int D>
 __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const float* __restrict__ q,
                                                            const float* __restrict__ k, const float* __restrict__ v,
-                                                           int v_bits) {
+                                                           int v_bits, uint32_t head_begin) {
     constexpr int F4 = D / 4;        // float4 per row
     constexpr int RPP = 256 / F4;    // rows per pass
     constexpr int PASSES = 64 / RPP; // 4 (D=64) or 8 (D=128)
     constexpr int G = D / 64;
-    const uint32_t b = blockIdx.x, h = blockIdx.y;
+    const uint32_t b = blockIdx.x, h = head_begin + blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c4 = tid % F4;
     const int r0 = tid / F4;
@@ -132,6 +141,7 @@ __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const flo
         sk = 1.0f;
     const float vq = v_bits == 4 ? 7.0f : 127.0f;
     const float sv = gv == 0.0f ? 1.0f : __fdiv_rn(gv, vq);
+    const float rq = __frcp_rn(sq), rk = __frcp_rn(sk), rv = __frcp_rn(sv);
 
     const size_t head_codes = (size_t)h * L.kb2 * 64 * D;
     int cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
@@ -140,13 +150,13 @@ __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const flo
         const size_t off = head_codes + (size_t)(b * 64 + r0 + RPP * j) * D + c4 * 4;
         const float4 a = xq[j], c = xk[j], e = xv[j];
         *reinterpret_cast<uint32_t*>(L.q + off) =
-            pack4(quant_sym(a.x, sq, 127.f), quant_sym(a.y, sq, 127.f), quant_sym(a.z, sq, 127.f),
-                  quant_sym(a.w, sq, 127.f));
+            pack4(quant_sym(a.x, sq, rq, 127.f), quant_sym(a.y, sq, rq, 127.f), quant_sym(a.z, sq, rq, 127.f),
+                  quant_sym(a.w, sq, rq, 127.f));
         *reinterpret_cast<uint32_t*>(L.k + off) =
-            pack4(quant_sym(c.x, sk, 127.f), quant_sym(c.y, sk, 127.f), quant_sym(c.z, sk, 127.f),
-                  quant_sym(c.w, sk, 127.f));
-        const int v0 = quant_sym(e.x, sv, vq), v1 = quant_sym(e.y, sv, vq), v2 = quant_sym(e.z, sv, vq),
-                  v3 = quant_sym(e.w, sv, vq);
+            pack4(quant_sym(c.x, sk, rk, 127.f), quant_sym(c.y, sk, rk, 127.f), quant_sym(c.z, sk, rk, 127.f),
+                  quant_sym(c.w, sk, rk, 127.f));
+        const int v0 = quant_sym(e.x, sv, rv, vq), v1 = quant_sym(e.y, sv, rv, vq), v2 = quant_sym(e.z, sv, rv, vq),
+                  v3 = quant_sym(e.w, sv, rv, vq);
         *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
         cs0 += v0;
         cs1 += v1;
@@ -224,13 +234,14 @@ __global__ void __launch_bounds__(256) k_quantize_sym(const float* __restrict__ 
     float s = __fdiv_rn(g, qmax);
     if (s == 0.0f)
         s = 1.0f;
+    const float rs = __frcp_rn(s);
 #pragma unroll
     for (int j = 0; j < PASSES; ++j) {
         const uint32_t i = b * 64 + r0 + RPP * j;
         if (i < rows)
             *reinterpret_cast<uint32_t*>(codes + (size_t)i * D + c4 * 4) =
-                pack4(quant_sym(x[j].x, s, qmax), quant_sym(x[j].y, s, qmax), quant_sym(x[j].z, s, qmax),
-                      quant_sym(x[j].w, s, qmax));
+                pack4(quant_sym(x[j].x, s, rs, qmax), quant_sym(x[j].y, s, rs, qmax), quant_sym(x[j].z, s, rs, qmax),
+                      quant_sym(x[j].w, s, rs, qmax));
     }
     if (tid == 0)
         scales[(size_t)b * G] = s;
@@ -348,17 +359,29 @@ __global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
     }
 }
 
-// K2c. Single CTA: counting sort of the H*np work items by step count,
-// longest first (LPT order for K3's cyclic distribution). Ties are ordered
-// by (h, p) via a stable in-bucket rank, so the order is deterministic.
+// K2c. Counting sort of work items by step count, longest first (LPT order
+// for K3's snake distribution). Ties are ordered by (h, p) via a stable
+// in-bucket rank, so the order is deterministic. Block 0 sorts all H*np items
+// into L.order; block c >= 1 sorts the items of heads [(c-1)*hpc, c*hpc) into
+// the same span of L.order_chunk (the chunked host-buffer pipeline runs K3
+// once per chunk).
 __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
     extern __shared__ uint32_t s_hist[]; // kb + 1 buckets
-    const uint32_t total = L.H * L.np;
+    uint32_t h0 = 0, h1 = L.H;
+    uint32_t* out = L.order;
+    if (blockIdx.x > 0) {
+        h0 = (blockIdx.x - 1) * L.hpc;
+        h1 = min(L.H, h0 + L.hpc);
+        out = L.order_chunk;
+    }
+    const uint32_t first = h0 * L.np, total = (h1 - h0) * L.np;
+    const uint32_t* key_of = L.pair_count + first;
+    out += first;
     for (uint32_t i = threadIdx.x; i <= L.kb; i += blockDim.x)
         s_hist[i] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x)
-        atomicAdd(&s_hist[L.pair_count[i]], 1u);
+        atomicAdd(&s_hist[key_of[i]], 1u);
     __syncthreads();
     if (threadIdx.x == 0) { // exclusive offsets, descending key
         uint32_t run = 0;
@@ -375,7 +398,7 @@ __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
         for (uint32_t base = 0; base < total; base += 32) {
             const uint32_t i = base + lane;
             const bool valid = i < total;
-            const uint32_t key = valid ? L.pair_count[i] : 0xffffffffu;
+            const uint32_t key = valid ? key_of[i] : 0xffffffffu;
             const uint32_t peers = __match_any_sync(0xffffffffu, key);
             const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
             const uint32_t pos = valid ? s_hist[key] + rank : 0;
@@ -384,7 +407,7 @@ __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
                 s_hist[key] += __popc(peers);
             __syncwarp();
             if (valid)
-                L.order[pos] = ((i / L.np) << 16) | (i % L.np);
+                out[pos] = ((h0 + i / L.np) << 16) | (i % L.np);
         }
     }
 }
@@ -393,12 +416,14 @@ __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
 // host-side launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits,
-                      cudaStream_t st) {
-    dim3 grid(L.kb2, L.H);
+                      uint32_t head_begin, uint32_t head_count, cudaStream_t st) {
+    if (head_count == 0)
+        return cudaSuccess;
+    dim3 grid(L.kb2, head_count);
     if (L.D == 64)
-        k1_reorder_quantize<64><<<grid, 256, 0, st>>>(L, q, k, v, v_bits);
+        k1_reorder_quantize<64><<<grid, 256, 0, st>>>(L, q, k, v, v_bits, head_begin);
     else
-        k1_reorder_quantize<128><<<grid, 256, 0, st>>>(L, q, k, v, v_bits);
+        k1_reorder_quantize<128><<<grid, 256, 0, st>>>(L, q, k, v, v_bits, head_begin);
     return cudaGetLastError();
 }
 
@@ -425,6 +450,8 @@ cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uin
     return cudaGetLastError();
 }
 
+cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
+
 cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
     dim3 grid(L.kb, L.H);
     k2_qblock_lists<<<grid, 128, 0, st>>>(L, bits);
@@ -435,7 +462,12 @@ cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
-    k2_work_order<<<1, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    return launch_k2_order(L, st);
+}
+
+cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st) {
+    const uint32_t nchunks = (L.H + L.hpc - 1) / L.hpc;
+    k2_work_order<<<1 + nchunks, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
     return cudaGetLastError();
 }
 

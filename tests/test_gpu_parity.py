@@ -197,6 +197,31 @@ def test_device_and_host_paths_identical(paro, ctx):
     layer.close()
 
 
+@pytest.mark.parametrize("chunks", [1, 2, 3, 5])
+def test_pipelined_host_forward_matches_device_forward(paro, ctx, chunks):
+    """forward_host's chunked upload/compute/download pipeline (per-chunk LPT
+    work lists, K1 head ranges) reproduces the one-shot device forward bit for
+    bit, for chunk counts that do and do not divide the head count."""
+    grid, H, d = "F:3,H:7,W:11", 5, 64
+    N = 231
+    q, k, v = make_inputs(H, N, d, 70)
+    masks = random_masks(H, 4, 0.4, 3, empty_row=1)
+    layer = paro.Layer(ctx, H, d, grid, ["WHF", "HFW", "FHW", "FWH", "HWF"])
+    layer.set_masks(masks)
+    dq, dk, dv = (paro.DeviceBuffer.from_array(x) for x in (q, k, v))
+    dout = paro.DeviceBuffer(q.nbytes)
+    dz = paro.DeviceBuffer(H * N)
+    layer.forward(dq.ptr, dk.ptr, dv.ptr, 0.0, 8, dout.ptr, dz.ptr)
+    paro.stream_sync()
+    ref, zref = dout.download(q.shape, np.float32), dz.download((H, N), np.uint8)
+    layer.set_pipeline_chunks(chunks)
+    out_h, z_h = layer.forward_host(q, k, v, 0.0, 8)
+    assert np.all(np.isfinite(ref))
+    assert np.array_equal(out_h, ref)
+    assert np.array_equal(z_h, zref)
+    layer.close()
+
+
 def test_device_apply_perm_rows_and_quantize(paro, ctx, oracle):
     g = paro.parse_grid("F:13,H:30,W:45")
     plan = paro.make_perm(g, "WHF")
