@@ -42,6 +42,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "layer.cuh"
 #include "ptx.cuh"
@@ -72,7 +73,7 @@ struct K3Cfg {
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 side][64]
     static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
     static constexpr uint32_t OFF_BAR = OFF_ROWSTAT + 2 * 2 * 64 * 40;
-    static constexpr uint32_t NBAR = 2 + 2 * NS + 15;
+    static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
     // swizzle: rows of D int8 -> 64B (D=64) or 128B (D=128) swizzle atoms of 8 rows
@@ -89,8 +90,10 @@ struct Bars {
     static constexpr uint32_t KVFULL = 2, KVEMPTY = 2 + NS, SFULL = 2 + 2 * NS, SEMPTY = SFULL + 2,
                               PFULL = SEMPTY + 2, PEMPTY = PFULL + 2, OFULL = PEMPTY + 2, OEMPTY = OFULL + 2,
                               LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1,
-                              QFULL1 = RED + 1, QEMPTY1 = RED + 2;
+                              QFULL1 = RED + 1, QEMPTY1 = RED + 2, COUNT = QEMPTY1 + 1;
 };
+static_assert(Bars<K3Cfg<64>::NS>::COUNT == K3Cfg<64>::NBAR && Bars<K3Cfg<128>::NS>::COUNT == K3Cfg<128>::NBAR,
+              "mbarrier block must hold every barrier (the TMEM pointer slot follows it)");
 
 // K-major operand rows of D bytes (Q, K): SBO = one 8-row atom.
 template <int D>
@@ -163,6 +166,19 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
             ptx::mma_i8(tmem + g * 64, desc_kmajor<D>(sq + koff), desc_kmajor<D>(sk + koff), C::IDESC_QK, kk);
         }
 }
+
+// Phase timers (PARO_K3_PROF builds only): clock64 deltas summed per warp role.
+//   [0..7]  softmax: wait, pass1, reduce, pass2, exact, post, steps, items
+//   [8..11] epilogue: wait, dequant, store, steps
+//   [12..15] mma: wait KV/S, wait P/O, issue, steps
+#ifdef PARO_K3_PROF
+static __device__ unsigned long long g_prof[16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(i, d) prof[i] += (unsigned long long)(d)
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, d)
+#endif
 
 struct K3Params {
     LayerDev L;
@@ -308,7 +324,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             unsigned long long* stats) {
+                                             unsigned long long* stats, unsigned long long (&prof)[8]) {
+    PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = live && valid_row;
@@ -375,6 +392,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmin_r = ex2(ymin - m32);
     }
     const float gamma = st.l > 0.f ? ex2(st.m32 - m32) : 1.0f;
+    PROF_T(tp1);
+    PROF_ADD(1, tp1 - tp0);
     if (!valid) {
         pmin_r = INFINITY;
         pmax_r = 0.f;
@@ -398,6 +417,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     if (pscale == 0.f)
         pscale = 1.f;
     const float inv = __frcp_rn(pscale);
+    PROF_T(tp2);
+    PROF_ADD(2, tp2 - tp1);
     // -------- pass 2: p, row sum, codes (two perturbed variants per element)
     const float kap = G == 1 ? kKappa : 0.f; // d=128: single (unperturbed) code, no exact path
     const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
@@ -482,6 +503,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     }
     if (!valid)
         risk = 0;
+    PROF_T(tp3);
+    PROF_ADD(3, tp3 - tp2);
     // -------- exact boundary path (d=64): rare, warp-uniform entry
 #ifdef PARO_K3_STATS
     if (stats && lane == 0) {
@@ -578,6 +601,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             }
         }
     }
+    PROF_T(tp4);
+    PROF_ADD(4, tp4 - tp3);
     float sa, sb;
     upk(sum2, sa, sb);
     if (live) {
@@ -700,11 +725,15 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             uint32_t T = 0, I = 0;
+            unsigned long long prof[4] = {0, 0, 0, 0};
             auto issue_pv = [&](uint32_t U, bool ha, bool hb) {
                 const uint32_t s = U % NS, b = U & 1, ph = (U >> 1) & 1;
+                PROF_T(tm0);
                 ptx::mbar_wait(bar(BR::PFULL + b), ph);
                 ptx::mbar_wait(bar(BR::OEMPTY + b), ph ^ 1);
                 ptx::tc_fence_after();
+                PROF_T(tm1);
+                PROF_ADD(1, tm1 - tm0);
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     if (side ? hb : ha) {
@@ -729,9 +758,13 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 ptx::tc_fence_after();
                 for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS, b = T & 1;
+                    PROF_T(tm2);
                     ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
                     ptx::mbar_wait(bar(BR::SEMPTY + b), ((T >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
+                    PROF_T(tm3);
+                    PROF_ADD(0, tm3 - tm2);
+                    PROF_ADD(3, 1);
                     if (t < x.na)
                         issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s));
                     if (t < x.nb)
@@ -749,6 +782,10 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                     ptx::mma_commit(qempty(I));
                 ++I;
             }
+#ifdef PARO_K3_PROF
+            for (int i = 0; i < 4; ++i)
+                atomicAdd(&g_prof[12 + i], prof[i]);
+#endif
         }
     } else if (warp < 6) {
         // ------------------------------------------------------------ softmax
@@ -762,6 +799,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         float* lsm = reinterpret_cast<float*>(smem + C::OFF_L);
         const uint32_t tail = L.N & 63;
         uint32_t T = 0, I = 0;
+        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t rr = 0; rr < rounds; ++rr) {
             const int it = item_at(rr);
             if (it < 0)
@@ -780,8 +818,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
                 const bool live = t < nmine;
                 const uint32_t bj = live ? list[t] : 0u;
+                PROF_T(tw0);
                 mbar_wait3(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
+                PROF_T(tw1);
+                PROF_ADD(0, tw1 - tw0);
                 const float* meta =
                     reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES + 4 * C::KV_BYTES +
                                                    side * C::META_BYTES);
@@ -798,11 +839,12 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 if (__any_sync(0xffffffffu, tail_tile))
                     softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
                                           tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w,
-                                          rs_r, side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, P.stats);
+                                          rs_r, side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, P.stats, prof);
                 else
                     softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, 64u, live,
                                            valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile,
-                                           prow, r, sq1, gamma, lo, pscale, P.stats);
+                                           prow, r, sq1, gamma, lo, pscale, P.stats, prof);
+                PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0)
@@ -821,7 +863,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 __syncwarp();
                 if (lane == 0)
                     ptx::mbar_arrive(bar(BR::PFULL + b));
+                PROF_T(tw3);
+                PROF_ADD(5, tw3 - tw2);
+                PROF_ADD(6, 1);
             }
+            PROF_ADD(7, 1);
             __syncwarp();
             if (lane == 0)
                 ptx::mbar_arrive(qempty(I)); // this warp no longer reads the item's Q tiles
@@ -832,6 +878,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 ptx::mbar_arrive(bar(BR::LFULL));
             ++I;
         }
+#ifdef PARO_K3_PROF
+        if (lane == 0)
+            for (int i = 0; i < 8; ++i)
+                atomicAdd(&g_prof[i], prof[i]);
+#endif
     } else {
         // ------------------------------------------------------------ epilogue
         const uint32_t quad = warp & 3;
@@ -842,6 +893,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         const float* usm = reinterpret_cast<const float*>(smem + C::OFF_U);
         const float* lsm = reinterpret_cast<const float*>(smem + C::OFF_L);
         uint32_t T = 0, I = 0;
+        unsigned long long prof[4] = {0, 0, 0, 0};
         for (uint32_t rr = 0; rr < rounds; ++rr) {
             const int it = item_at(rr);
             if (it < 0)
@@ -856,8 +908,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 acc[c] = 0ull;
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t b = T & 1, ph = (T >> 1) & 1;
+                PROF_T(te0);
                 mbar_wait2(bar(BR::OFULL + b), ph, bar(BR::PFULL + b), ph);
                 ptx::tc_fence_after();
+                PROF_T(te1);
+                PROF_ADD(0, te1 - te0);
                 // idle rows carry gamma 1, ss 0 and u 0: acc*1 + 0*ip + 0 == acc exactly
                 const float4 rm = rowmeta[(b * 2 + side) * 64 + r];
                 const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
@@ -886,7 +941,11 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                     ptx::mbar_arrive(bar(BR::OEMPTY + b));
                     ptx::mbar_arrive(bar(BR::PEMPTY + b));
                 }
+                PROF_T(te2);
+                PROF_ADD(1, te2 - te1);
+                PROF_ADD(3, 1);
             }
+            PROF_T(te3);
             ptx::mbar_wait(bar(BR::LFULL), I & 1);
             const float l = lsm[side * 64 + r];
             __syncwarp();
@@ -913,7 +972,14 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 if (P.zeroed)
                     P.zeroed[(size_t)x.h * L.N + orig] = l == 0.f ? 1 : 0;
             }
+            PROF_T(te4);
+            PROF_ADD(2, te4 - te3);
         }
+#ifdef PARO_K3_PROF
+        if (lane == 0)
+            for (int i = 0; i < 4; ++i)
+                atomicAdd(&g_prof[8 + i], prof[i]);
+#endif
     }
 
     ptx::tc_fence_before();
@@ -985,9 +1051,21 @@ __global__ void __launch_bounds__(128, 1)
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+static void init_watchdog() {
+    static bool done = false;
+    if (done)
+        return;
+    done = true;
+    if (const char* e = getenv("PARO_WATCHDOG_S")) {
+        const unsigned long long ns = (unsigned long long)(atof(e) * 1e9);
+        cudaMemcpyToSymbol(ptx::g_watchdog_ns, &ns, sizeof(ns));
+    }
+}
+
 template <int D>
 static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, int grid, cudaStream_t st) {
+    init_watchdog();
     const uint32_t smem = K3Cfg<D>::SMEM_BYTES;
     cudaError_t e = cudaFuncSetAttribute(k3_attention<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
@@ -1023,6 +1101,22 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
         cudaDeviceSynchronize();
         cudaMemcpy(h, dstats, 24, cudaMemcpyDeviceToHost);
         fprintf(stderr, "[k3 stats] warp-steps %llu exact-path %llu risky-groups %llu\n", h[0], h[1], h[2]);
+    }
+#endif
+#ifdef PARO_K3_PROF
+    if (getenv("PARO_K3_PROF_PRINT")) {
+        unsigned long long h[16];
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
+        fprintf(stderr, "[k3 prof] softmax/step: wait %.0f pass1 %.0f reduce %.0f pass2 %.0f exact %.0f post %.0f (steps %llu items %llu)\n",
+                (double)h[0] / h[6], (double)h[1] / h[6], (double)h[2] / h[6], (double)h[3] / h[6], (double)h[4] / h[6],
+                (double)h[5] / h[6], h[6], h[7]);
+        fprintf(stderr, "[k3 prof] epilogue/step: wait %.0f dequant %.0f store/item %.0f (steps %llu)\n",
+                (double)h[8] / h[11], (double)h[9] / h[11], (double)h[10] / (h[7] ? h[7] : 1) , h[11]);
+        fprintf(stderr, "[k3 prof] mma/step: wait KV+S %.0f wait P+O %.0f (steps %llu)\n", (double)h[12] / h[15],
+                (double)h[13] / h[15], h[15]);
+        memset(h, 0, sizeof(h));
+        cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }
 #endif
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);

@@ -68,15 +68,35 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware
+// until the phase completes (or the hint expires) instead of spinning through
+// issue slots the softmax warps on the same SM sub-partition need.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
+
+// Watchdog for mbar_wait (ns; 0 = off). One copy per translation unit; the
+// launcher sets it from PARO_WATCHDOG_S (default 4 s; profilers that replay
+// instrumented kernels need it off).
+static __device__ unsigned long long g_watchdog_ns = 4000000000ull;
+
 // Wait for the phase with `parity` to complete. A pipeline bug must not hang
-// the GPU: after ~4 s of waiting the kernel traps (a launch error, not a hang).
+// the GPU: after the watchdog time the kernel traps (a launch error, not a hang).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity))
         return;
     const uint64_t t0 = globaltimer();
-    uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if ((++spins & 1023u) == 0 && globaltimer() - t0 > 4000000000ull)
+    while (!mbar_try_wait_sleep(bar, parity)) {
+        const unsigned long long lim = g_watchdog_ns;
+        if (lim && globaltimer() - t0 > lim)
             __trap();
     }
 }
