@@ -297,6 +297,43 @@ __device__ __forceinline__ uint32_t round_half_away_pos(float q) {
     return (uint32_t)t;
 }
 
+// d=128: the two int32 group sums S_0, S_1 of (row r, key j) from the smem Q/K
+// tiles (128-byte rows, 128B swizzle: 16-B chunk c of row r at c ^ (r & 7))
+__device__ __forceinline__ void dot_row128(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t j,
+                                           int32_t& s0, int32_t& s1) {
+    const uint8_t* qr = qtile + (r >> 3) * 1024 + (r & 7) * 128;
+    const uint8_t* kr = ktile + (j >> 3) * 1024 + (j & 7) * 128;
+    int32_t acc[2] = {0, 0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int4 a = *reinterpret_cast<const int4*>(qr + ((c ^ (r & 7)) << 4));
+        const int4 b = *reinterpret_cast<const int4*>(kr + ((c ^ (j & 7)) << 4));
+        int32_t& t = acc[c >> 2];
+        t = __dp4a(a.x, b.x, t);
+        t = __dp4a(a.y, b.y, t);
+        t = __dp4a(a.z, b.z, t);
+        t = __dp4a(a.w, b.w, t);
+    }
+    s0 = acc[0];
+    s1 = acc[1];
+}
+
+// d=128 logit in the reference's fp64 order (paro_oracle.c qk_mode 1, attention.cpp:166):
+// scale * ((a0 * S_0) + (a1 * S_1)), a_g = sq_g * sk_g exact in fp64
+__device__ __forceinline__ double logit128(double scale64, double a0, double a1, int32_t s0, int32_t s1) {
+    return __dmul_rn(scale64, __dadd_rn(__dmul_rn(a0, (double)s0), __dmul_rn(a1, (double)s1)));
+}
+
+// column-tagged fp32 logit: the low 6 mantissa bits carry the column, so a max /
+// min over keys also names its column (perturbation < 64 ulp, covered by kGapSlack)
+__device__ __forceinline__ float tagf(float y, uint32_t j) {
+    return __uint_as_float((__float_as_uint(y) & ~63u) | j);
+}
+// |fp32 logit (log2 units) - exact| <= kErrS * (c0 + c1) * kSBound (+ tag slack): a
+// top-2 / bottom-2 gap below that bound falls back to an exact rescan
+constexpr float kSBound = 64.f * 127.f * 127.f; // |S_g| <= 64 * 127^2
+constexpr float kErrS = 5e-7f, kGapSlack = 2e-5f;
+
 // ---------------------------------------------------------------------------
 // Softmax, one step for this thread's row (v3 order: pass 1 extremes -> group
 // reduction -> pass 2 p / codes).
@@ -331,8 +368,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const bool valid = live && valid_row;
     // -------- pass 1: row extremes (4 independent chains)
     float m32, pmax_r, pmin_r, c0, c1 = 0.f, dmax = 0.f;
-    int32_t smax_i = 0;
-    double a64 = 0.0, m64 = st.m64;
+    int32_t smax_i = 0, smax1_i = 0; // d=64: row max of S; d=128: (S_0, S_1) of the row's argmax column
+    double a64 = 0.0, a64b = 0.0, m64 = st.m64;
     if (G == 1) {
         int32_t mx[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN},
                 mn[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
@@ -367,9 +404,16 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmin_r = ex2(fmaf(__int2float_rn(smin - smax), c0, dmax));
         *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
     } else {
-        c0 = scale_log2 * sq * sk0;
-        c1 = scale_log2 * sq1 * sk1;
-        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        // d=128: the argmax / argmin columns from column-tagged fp32 logits (two
+        // chains of top-2 / bottom-2), their exact fp64 logits from dp4a over the
+        // Q/K tiles, and an exact warp-uniform rescan of the near candidates when a
+        // top-2 / bottom-2 gap is within the fp32 error bound (rare)
+        a64 = __dmul_rn((double)sq, (double)sk0);
+        a64b = __dmul_rn((double)sq1, (double)sk1);
+        c0 = (float)(__dmul_rn(__dmul_rn(scale64, a64), kLog2e));
+        c1 = (float)(__dmul_rn(__dmul_rn(scale64, a64b), kLog2e));
+        float M1[2] = {-INFINITY, -INFINITY}, M2[2] = {-INFINITY, -INFINITY};
+        float N1[2] = {INFINITY, INFINITY}, N2[2] = {INFINITY, INFINITY};
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t x0[32], x1[32];
@@ -377,19 +421,80 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
-                if (!TAIL || (uint32_t)(h2 * 32 + j) < ncol) {
-                    mx[j & 3] = fmaxf(mx[j & 3], y);
-                    mn[j & 3] = fminf(mn[j & 3], y);
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t ja = h2 * 32 + 2 * k, jb = ja + 1;
+                const float ya = fmaf(__int2float_rn((int32_t)x1[2 * k]), c1, __int2float_rn((int32_t)x0[2 * k]) * c0);
+                const float yb =
+                    fmaf(__int2float_rn((int32_t)x1[2 * k + 1]), c1, __int2float_rn((int32_t)x0[2 * k + 1]) * c0);
+                const float ka = tagf(ya, ja), kb = tagf(yb, jb);
+                float xa = ka, xb = kb, na = ka, nb = kb;
+                if (TAIL) {
+                    if (ja >= ncol) {
+                        xa = -INFINITY;
+                        na = INFINITY;
+                    }
+                    if (jb >= ncol) {
+                        xb = -INFINITY;
+                        nb = INFINITY;
+                    }
+                }
+                const float hi = fmaxf(xa, xb), lo = fminf(xa, xb);
+                const float hi2 = TAIL ? fmaxf(na, nb) : hi, lo2 = TAIL ? fminf(na, nb) : lo;
+                const int c = k & 1;
+                M2[c] = fmaxf(fmaxf(fminf(M1[c], hi), M2[c]), lo);
+                M1[c] = fmaxf(M1[c], hi);
+                N2[c] = fminf(fminf(fmaxf(N1[c], lo2), N2[c]), hi2);
+                N1[c] = fminf(N1[c], lo2);
+            }
+        }
+        const float mA = fmaxf(M1[0], M1[1]), mB = fmaxf(fmaxf(fminf(M1[0], M1[1]), M2[0]), M2[1]);
+        const float nA = fminf(N1[0], N1[1]), nB = fminf(fminf(fmaxf(N1[0], N1[1]), N2[0]), N2[1]);
+        const float slack = kErrS * (c0 + c1) * kSBound + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
+        const bool unsure = !(mA - mB > slack) || !(nB - nA > slack);
+        int32_t s0x, s1x, s0n, s1n;
+        dot_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, s0x, s1x);
+        dot_row128(qtile, ktile, r, __float_as_uint(nA) & 63u, s0n, s1n);
+        double tmax64 = logit128(scale64, a64, a64b, s0x, s1x);
+        double tmin64 = logit128(scale64, a64, a64b, s0n, s1n);
+        if (__any_sync(0xffffffffu, unsure && valid)) {
+            const float thr_hi = mA - slack, thr_lo = nA + slack;
+#pragma unroll 1
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t x0[32], x1[32];
+                ptx::tmem_ld32(s_addr + h2 * 32, x0);
+                ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float y =
+                        fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
+                    if (unsure && (uint32_t)(h2 * 32 + j) < ncol && (y >= thr_hi || y <= thr_lo)) {
+                        const int32_t a = (int32_t)x0[j], b = (int32_t)x1[j];
+                        const double L = logit128(scale64, a64, a64b, a, b);
+                        if (L > tmax64) {
+                            tmax64 = L;
+                            s0x = a;
+                            s1x = b;
+                        }
+                        if (L < tmin64) {
+                            tmin64 = L;
+                            s0n = a;
+                            s1n = b;
+                        }
+                    }
                 }
             }
         }
-        const float ymax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-        const float ymin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
-        m32 = live ? fmaxf(st.m32, ymax) : st.m32;
-        pmax_r = ex2(ymax - m32);
-        pmin_r = ex2(ymin - m32);
+        if (live)
+            m64 = fmax(st.m64, tmax64);
+        m32 = (float)(m64 * kLog2e);
+        dmax = (float)((tmax64 - m64) * kLog2e);
+        smax_i = s0x;
+        smax1_i = s1x;
+        // exp2 argument of element j = (S0_j - S0x) * c0 + (S1_j - S1x) * c1 + dmax
+        pmax_r = ex2(dmax);
+        pmin_r = ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
+        *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
     }
     const float gamma = st.l > 0.f ? ex2(st.m32 - m32) : 1.0f;
     PROF_T(tp1);
@@ -420,11 +525,11 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     PROF_T(tp2);
     PROF_ADD(2, tp2 - tp1);
     // -------- pass 2: p, row sum, codes (two perturbed variants per element)
-    const float kap = G == 1 ? kKappa : 0.f; // d=128: single (unperturbed) code, no exact path
+    const float kap = kKappa;
     const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
     const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
     const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
-    const uint64_t c00 = pk(c0, c0), nm = pk(dmax, dmax);
+    const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
     uint64_t sum2 = pk(0.f, 0.f);
     uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
 #pragma unroll
@@ -450,9 +555,16 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float y = fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
-                pv[j] = ex2(y - m32);
+            for (int k = 0; k < 16; ++k) {
+                const uint64_t d0 = pk(__int2float_rn((int32_t)x0[2 * k] - smax_i),
+                                       __int2float_rn((int32_t)x0[2 * k + 1] - smax_i));
+                const uint64_t d1 = pk(__int2float_rn((int32_t)x1[2 * k] - smax1_i),
+                                       __int2float_rn((int32_t)x1[2 * k + 1] - smax1_i));
+                const uint64_t y2 = fma2(d1, c11, fma2(d0, c00, nm));
+                float ya, yb;
+                upk(y2, ya, yb);
+                pv[2 * k] = ex2(ya);
+                pv[2 * k + 1] = ex2(yb);
             }
         }
         if (TAIL) {
@@ -491,7 +603,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 }
             }
             whi[w] = hi4;
-            if (G == 1 && hi4 != lo4)
+            if (hi4 != lo4)
                 risk |= 1u << (h2 * 8 + w);
         }
 #pragma unroll
@@ -519,7 +631,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             atomicAdd(stats + 2, (unsigned long long)nrisk);
     }
 #endif
-    if (G == 1 && __any_sync(0xffffffffu, risk != 0)) {
+    if (__any_sync(0xffffffffu, risk != 0)) {
         // exact tile lo/hi of both q-blocks from every row's published extremes
         // (only rows whose fast-path extreme is within 1e-5 of the fast tile
         // extreme can hold the exact one: fp64 exp runs for those few rows, and
@@ -584,15 +696,22 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 const uint32_t j = 4 * g + e;
                 if (j >= ncol)
                     continue;
-                const int32_t Sj = dot_row64(qtile, ktile, r, j);
+                int32_t Sj, S1j = 0;
+                if (G == 1)
+                    Sj = dot_row64(qtile, ktile, r, j);
+                else
+                    dot_row128(qtile, ktile, r, j, Sj, S1j);
                 { // re-run the two fast variants of this element; only a split pair needs fp64
-                    const float pf = ex2(fmaf(__int2float_rn(Sj - smax_i), c0, dmax));
+                    const float pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_i), c0, dmax))
+                                            : ex2(fmaf(__int2float_rn(S1j - smax1_i), c1,
+                                                       fmaf(__int2float_rn(Sj - smax_i), c0, dmax)));
                     float ul, uh;
                     upk(add2_rm(fma2_rm(pk(pf, pf), A2, B2), magic2), ul, uh);
                     if (__float_as_uint(ul) == __float_as_uint(uh))
                         continue;
                 }
-                const double logit = __dmul_rn(scale64, __dmul_rn(a64, (double)Sj));
+                const double logit = G == 1 ? __dmul_rn(scale64, __dmul_rn(a64, (double)Sj))
+                                            : logit128(scale64, a64, a64b, Sj, S1j);
                 const float p = (float)exp(logit - m64);
                 float q = __fdiv_rn(__fsub_rn(p, lo_x), ps_x);
                 q = fminf(p_qmax, fmaxf(0.f, q));
