@@ -318,6 +318,46 @@ __device__ __forceinline__ void dot_row128(const uint8_t* qtile, const uint8_t* 
     s1 = acc[1];
 }
 
+// both (S_0, S_1) pairs of columns ja and jb of row r in one pass (shared Q-row loads)
+__device__ __forceinline__ void dot2_row128(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t ja,
+                                            uint32_t jb, int32_t& a0, int32_t& a1, int32_t& b0, int32_t& b1) {
+    const uint8_t* qr = qtile + (r >> 3) * 1024 + (r & 7) * 128;
+    const uint8_t* ka = ktile + (ja >> 3) * 1024 + (ja & 7) * 128;
+    const uint8_t* kb = ktile + (jb >> 3) * 1024 + (jb & 7) * 128;
+    int32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int4 q = *reinterpret_cast<const int4*>(qr + ((c ^ (r & 7)) << 4));
+        const int4 x = *reinterpret_cast<const int4*>(ka + ((c ^ (ja & 7)) << 4));
+        const int4 y = *reinterpret_cast<const int4*>(kb + ((c ^ (jb & 7)) << 4));
+        int32_t& t = acc[c >> 2];
+        int32_t& u = acc[2 + (c >> 2)];
+        t = __dp4a(q.x, x.x, t);
+        u = __dp4a(q.x, y.x, u);
+        t = __dp4a(q.y, x.y, t);
+        u = __dp4a(q.y, y.y, u);
+        t = __dp4a(q.z, x.z, t);
+        u = __dp4a(q.z, y.z, u);
+        t = __dp4a(q.w, x.w, t);
+        u = __dp4a(q.w, y.w, u);
+    }
+    a0 = acc[0];
+    a1 = acc[1];
+    b0 = acc[2];
+    b1 = acc[3];
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 // d=128 logit in the reference's fp64 order (paro_oracle.c qk_mode 1, attention.cpp:166):
 // scale * ((a0 * S_0) + (a1 * S_1)), a_g = sq_g * sk_g exact in fp64
 __device__ __forceinline__ double logit128(double scale64, double a0, double a1, int32_t s0, int32_t s1) {
@@ -354,7 +394,7 @@ struct RowState {
     double m64;
 };
 
-template <int D, bool TAIL>
+template <int D>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
                                              RowState& st, float p_qmax, float2* red_w, const float2* red_r,
@@ -379,11 +419,9 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             ptx::tmem_ld32(s_addr + h2 * 32, x);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                if (!TAIL || (uint32_t)(h2 * 32 + j) < ncol) {
-                    mx[j & 3] = max(mx[j & 3], (int32_t)x[j]);
-                    mn[j & 3] = min(mn[j & 3], (int32_t)x[j]);
-                }
+            for (int j = 0; j < 32; ++j) { // padded key columns repeat column 0 (K1): no masking
+                mx[j & 3] = max(mx[j & 3], (int32_t)x[j]);
+                mn[j & 3] = min(mn[j & 3], (int32_t)x[j]);
             }
         }
         const int32_t smax = max(max(mx[0], mx[1]), max(mx[2], mx[3]));
@@ -412,8 +450,14 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         a64b = __dmul_rn((double)sq1, (double)sk1);
         c0 = (float)(__dmul_rn(__dmul_rn(scale64, a64), kLog2e));
         c1 = (float)(__dmul_rn(__dmul_rn(scale64, a64b), kLog2e));
-        float M1[2] = {-INFINITY, -INFINITY}, M2[2] = {-INFINITY, -INFINITY};
-        float N1[2] = {INFINITY, INFINITY}, N2[2] = {INFINITY, INFINITY};
+        // 4 chains (pair k -> chain k & 3) for latency; top-2 / bottom-2 merges with
+        // 3-input min / max: M2' = max(M2, min(M1, hi), lo), M1' = max(M1, hi)
+        float M1[4], M2[4], N1[4], N2[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            M1[c] = M2[c] = -INFINITY;
+            N1[c] = N2[c] = INFINITY;
+        }
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t x0[32], x1[32];
@@ -427,33 +471,28 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 const float yb =
                     fmaf(__int2float_rn((int32_t)x1[2 * k + 1]), c1, __int2float_rn((int32_t)x0[2 * k + 1]) * c0);
                 const float ka = tagf(ya, ja), kb = tagf(yb, jb);
-                float xa = ka, xb = kb, na = ka, nb = kb;
-                if (TAIL) {
-                    if (ja >= ncol) {
-                        xa = -INFINITY;
-                        na = INFINITY;
-                    }
-                    if (jb >= ncol) {
-                        xb = -INFINITY;
-                        nb = INFINITY;
-                    }
-                }
-                const float hi = fmaxf(xa, xb), lo = fminf(xa, xb);
-                const float hi2 = TAIL ? fmaxf(na, nb) : hi, lo2 = TAIL ? fminf(na, nb) : lo;
-                const int c = k & 1;
-                M2[c] = fmaxf(fmaxf(fminf(M1[c], hi), M2[c]), lo);
+                const float hi = fmaxf(ka, kb), lo = fminf(ka, kb);
+                const int c = k & 3;
+                M2[c] = fmax3(M2[c], fminf(M1[c], hi), lo);
                 M1[c] = fmaxf(M1[c], hi);
-                N2[c] = fminf(fminf(fmaxf(N1[c], lo2), N2[c]), hi2);
-                N1[c] = fminf(N1[c], lo2);
+                N2[c] = fmin3(N2[c], fmaxf(N1[c], lo), hi);
+                N1[c] = fminf(N1[c], lo);
             }
         }
-        const float mA = fmaxf(M1[0], M1[1]), mB = fmaxf(fmaxf(fminf(M1[0], M1[1]), M2[0]), M2[1]);
-        const float nA = fminf(N1[0], N1[1]), nB = fminf(fminf(fmaxf(N1[0], N1[1]), N2[0]), N2[1]);
+        // merge chains pairwise (same top-2 rule)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            M2[c] = fmax3(fmaxf(M2[c], M2[c + 2]), fminf(M1[c], M1[c + 2]), -INFINITY);
+            M1[c] = fmaxf(M1[c], M1[c + 2]);
+            N2[c] = fmin3(fminf(N2[c], N2[c + 2]), fmaxf(N1[c], N1[c + 2]), INFINITY);
+            N1[c] = fminf(N1[c], N1[c + 2]);
+        }
+        const float mA = fmaxf(M1[0], M1[1]), mB = fmax3(fminf(M1[0], M1[1]), M2[0], M2[1]);
+        const float nA = fminf(N1[0], N1[1]), nB = fmin3(fmaxf(N1[0], N1[1]), N2[0], N2[1]);
         const float slack = kErrS * (c0 + c1) * kSBound + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
         const bool unsure = !(mA - mB > slack) || !(nB - nA > slack);
         int32_t s0x, s1x, s0n, s1n;
-        dot_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, s0x, s1x);
-        dot_row128(qtile, ktile, r, __float_as_uint(nA) & 63u, s0n, s1n);
+        dot2_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, __float_as_uint(nA) & 63u, s0x, s1x, s0n, s1n);
         double tmax64 = logit128(scale64, a64, a64b, s0x, s1x);
         double tmin64 = logit128(scale64, a64, a64b, s0n, s1n);
         if (__any_sync(0xffffffffu, unsure && valid)) {
@@ -531,6 +570,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
     const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
     uint64_t sum2 = pk(0.f, 0.f);
+    const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
     uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
@@ -567,7 +607,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 pv[2 * k + 1] = ex2(yb);
             }
         }
-        if (TAIL) {
+        if (tail_any) { // tail tile: the padded key columns (copies of column 0) leave the row sum
 #pragma unroll
             for (int j = 0; j < 32; ++j)
                 if ((uint32_t)(h2 * 32 + j) >= ncol)
@@ -576,12 +616,6 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             sum2 = add2(sum2, pk(pv[2 * k], pv[2 * k + 1]));
-        if (TAIL) { // padded keys quantize as p = lo (code 0 in both variants; V rows are zero)
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if ((uint32_t)(h2 * 32 + j) >= ncol)
-                    pv[j] = lo;
-        }
         uint32_t whi[8];
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
@@ -955,14 +989,9 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
-                if (__any_sync(0xffffffffu, tail_tile))
-                    softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
-                                          tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w,
-                                          rs_r, side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, P.stats, prof);
-                else
-                    softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, 64u, live,
-                                           valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile,
-                                           prow, r, sq1, gamma, lo, pscale, P.stats, prof);
+                softmax_step<D>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
+                                valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
+                                gamma, lo, pscale, P.stats, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();

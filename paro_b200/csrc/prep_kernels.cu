@@ -63,9 +63,12 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 //         group per 64x64 tile, scale = amax/127 (0 -> 1).
 //   V   : engine V-tile quantizer (attention.cpp:104-126): one group per key
 //         block over all D columns, scale = amax==0 ? 1 : amax/qmax, colsum.
-// Rows i >= N (block padding) read as zero and write zero codes; an all-zero
-// row never changes amax (max starts at 0) or colsum, so groups keep the
-// reference's true-extent semantics.
+// Rows i >= N (block padding): Q and V read as zero and write zero codes (an
+// all-zero row never changes amax or colsum, so groups keep the reference's
+// true-extent semantics). K padding rows are copies of the block's first row:
+// in K3 a padded key column then repeats key column 0's logit, so row and tile
+// extremes are those of the true columns without per-element masking, and the
+// zero V rows keep it out of P.V (K3 only corrects the row sum on tail tiles).
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const float* __restrict__ q,
@@ -96,7 +99,9 @@ __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const flo
             xk[j] = ld_stream(k + off);
             xv[j] = ld_stream(v + off);
         } else {
-            xq[j] = xk[j] = xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            xq[j] = xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            xk[j] = b * 64 < L.N ? ld_stream(k + head_in + (size_t)perm_src(pd, b * 64) * D + c4 * 4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f); // the even-count filler block stays zero
         }
     }
 
