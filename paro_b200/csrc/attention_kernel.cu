@@ -54,6 +54,18 @@ struct K3Cfg {
     static constexpr int G = D / 64;
     static constexpr int NS = 3;
     static constexpr int MINB = D == 64 ? 2 : 1; // CTAs per SM
+    // SPLIT (d=128): 12 warps, warpgroup 0 = TMA producer, MMA issuer, 2 idle
+    // (registers released with setmaxnreg), warpgroups 1-2 = 8 compute warps
+    // (TMEM quadrant x key-column half), each doing softmax + dequant of its half.
+    // !SPLIT (d=64): 10 warps, producer, MMA, 4 softmax, 4 epilogue (at d=64 the
+    // split's two warps per quadrant contend for one SMSP in the synchronised
+    // pass 2; measured 5.71 vs 4.86 ms at c2, while d=128 gains 188 -> 165 ms).
+    static constexpr bool SPLIT = D == 128;
+    static constexpr int THREADS = SPLIT ? 384 : 320;
+    static constexpr uint32_t NCW = SPLIT ? 8 : 4; // warps arriving on the S / P / O barriers
+    static constexpr uint32_t REG_LAUNCH = (65536 / (THREADS * MINB)) / 8 * 8;
+    static constexpr uint32_t REG_LOW = 32;
+    static constexpr uint32_t REG_COMPUTE = ((REG_LAUNCH * THREADS - REG_LOW * 128) / 256) / 8 * 8;
     static constexpr uint32_t QT_BYTES = 64 * D; // one q-block tile
     static constexpr uint32_t KV_BYTES = 64 * D;
     static constexpr uint32_t META_BYTES = (4 + D) * 4; // multiple of 16
@@ -70,8 +82,8 @@ struct K3Cfg {
     static constexpr uint32_t OFF_ROWMETA = OFF_P + 4 * P_BYTES;     // [2 buf][2 side][64] float4
     static constexpr uint32_t OFF_U = OFF_ROWMETA + 2 * 2 * 64 * 16;  // [2 buf][2 side][D]
     static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;        // [2 parity][4 quad][2 side] float2
-    static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 side][64]
-    static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
+    static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
+    static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
     static constexpr uint32_t OFF_BAR = OFF_ROWSTAT + 2 * 2 * 64 * 40;
     static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
@@ -394,14 +406,14 @@ struct RowState {
     double m64;
 };
 
-template <int D>
+template <int D, bool SPLIT>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
                                              RowState& st, float p_qmax, float2* red_w, const float2* red_r,
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             unsigned long long* stats, unsigned long long (&prof)[8]) {
+                                             uint32_t half, unsigned long long (&prof)[8]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -440,7 +452,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         smax_i = smax;
         pmax_r = ex2(dmax);
         pmin_r = ex2(fmaf(__int2float_rn(smin - smax), c0, dmax));
-        *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
+        if (!SPLIT || half == 0)
+            *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
     } else {
         // d=128: the argmax / argmin columns from column-tagged fp32 logits (two
         // chains of top-2 / bottom-2), their exact fp64 logits from dp4a over the
@@ -533,9 +546,12 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         // exp2 argument of element j = (S0_j - S0x) * c0 + (S1_j - S1x) * c1 + dmax
         pmax_r = ex2(dmax);
         pmin_r = ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
-        *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
+        if (!SPLIT || half == 0)
+            *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
     }
-    const float gamma = st.l > 0.f ? ex2(st.m32 - m32) : 1.0f;
+    // rescale when an earlier tile of the item was live (the reference's l > 0,
+    // attention.cpp:170): both column halves agree on it
+    const float gamma = st.m32 != -INFINITY ? ex2(st.m32 - m32) : 1.0f;
     PROF_T(tp1);
     PROF_ADD(1, tp1 - tp0);
     if (!valid) {
@@ -548,9 +564,9 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
         pmax_r = fmaxf(pmax_r, __shfl_xor_sync(0xffffffffu, pmax_r, o));
     }
-    if ((lane & 15) == 0)
+    if ((!SPLIT || half == 0) && (lane & 15) == 0)
         *red_w = make_float2(pmin_r, pmax_r);
-    ptx::named_bar_sync(1, 128);
+    ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
     float lo = red_r[0].x, hi = red_r[0].y;
 #pragma unroll
     for (int q = 1; q < 4; ++q) {
@@ -573,7 +589,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
     uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
+    for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) { // the warp's key-column half (SPLIT) or both
+        const int h2 = SPLIT ? (int)half : hh;
         float pv[32];
         if (G == 1) {
             uint32_t x[32];
@@ -652,19 +669,6 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     PROF_T(tp3);
     PROF_ADD(3, tp3 - tp2);
     // -------- exact boundary path (d=64): rare, warp-uniform entry
-#ifdef PARO_K3_STATS
-    if (stats && lane == 0) {
-        atomicAdd(stats, 1ull);
-        const uint32_t any = __any_sync(0xffffffffu, risk != 0);
-        if (any)
-            atomicAdd(stats + 1, 1ull);
-    }
-    if (stats) {
-        const uint32_t nrisk = __popc(risk);
-        if (nrisk)
-            atomicAdd(stats + 2, (unsigned long long)nrisk);
-    }
-#endif
     if (__any_sync(0xffffffffu, risk != 0)) {
         // exact tile lo/hi of both q-blocks from every row's published extremes
         // (only rows whose fast-path extreme is within 1e-5 of the fast tile
@@ -769,7 +773,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 }
 
 template <int D>
-__global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
+__global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     k3_attention(const __grid_constant__ K3Params P, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
     using C = K3Cfg<D>;
@@ -791,24 +795,23 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         // item's last QK retired AND the softmax warps finished the item (the
         // exact boundary path re-reads Q from smem)
         ptx::mbar_init(bar(B_QFULL), 1);
-        ptx::mbar_init(bar(B_QEMPTY), 1 + 4);
+        ptx::mbar_init(bar(B_QEMPTY), 1 + C::NCW);
         ptx::mbar_init(bar(BR::QFULL1), 1);
-        ptx::mbar_init(bar(BR::QEMPTY1), 1 + 4);
+        ptx::mbar_init(bar(BR::QEMPTY1), 1 + C::NCW);
         for (int s = 0; s < NS; ++s) {
             ptx::mbar_init(bar(BR::KVFULL + s), 1);
             ptx::mbar_init(bar(BR::KVEMPTY + s), 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(bar(BR::SFULL + b), 1);
-            ptx::mbar_init(bar(BR::SEMPTY + b), 4);
-            ptx::mbar_init(bar(BR::PFULL + b), 4);
-            ptx::mbar_init(bar(BR::PEMPTY + b), 1 + 4);
+            ptx::mbar_init(bar(BR::SEMPTY + b), C::NCW);
+            ptx::mbar_init(bar(BR::PFULL + b), C::NCW);
+            ptx::mbar_init(bar(BR::PEMPTY + b), 1 + C::NCW);
             ptx::mbar_init(bar(BR::OFULL + b), 1);
-            ptx::mbar_init(bar(BR::OEMPTY + b), 4);
+            ptx::mbar_init(bar(BR::OEMPTY + b), C::NCW);
         }
-        ptx::mbar_init(bar(BR::LFULL), 4);
+        ptx::mbar_init(bar(BR::LFULL), 4); // !SPLIT: softmax -> epilogue row sums
         ptx::mbar_init(bar(BR::LEMPTY), 4);
-        ptx::mbar_init(bar(BR::RED), 4);
         ptx::fence_barrier_init();
     }
     if (warp == 1)
@@ -832,6 +835,8 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
+        if (C::SPLIT)
+            ptx::setmaxnreg_dec<C::REG_LOW>();
         if (lane == 0) {
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_k);
@@ -876,6 +881,8 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        if (C::SPLIT)
+            ptx::setmaxnreg_dec<C::REG_LOW>();
         if (lane == 0) {
             uint32_t T = 0, I = 0;
             unsigned long long prof[4] = {0, 0, 0, 0};
@@ -940,7 +947,8 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 atomicAdd(&g_prof[12 + i], prof[i]);
 #endif
         }
-    } else if (warp < 6) {
+    } else if (!C::SPLIT) {
+        if (warp < 6) {
         // ------------------------------------------------------------ softmax
         const uint32_t quad = warp & 3;
         const uint32_t side = lane >> 4;
@@ -989,9 +997,9 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
                 const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
-                softmax_step<D>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
+                softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
-                                gamma, lo, pscale, P.stats, prof);
+                                gamma, lo, pscale, 0u, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1031,7 +1039,7 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
 #endif
-    } else {
+        } else {
         // ------------------------------------------------------------ epilogue
         const uint32_t quad = warp & 3;
         const uint32_t side = lane >> 4;
@@ -1128,6 +1136,176 @@ __global__ void __launch_bounds__(320, K3Cfg<D>::MINB)
             for (int i = 0; i < 4; ++i)
                 atomicAdd(&g_prof[8 + i], prof[i]);
 #endif
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ compute warps
+        // warp 4 + 4*half + quad: TMEM lane quadrant `quad` (rows 16q..16q+15 of
+        // q-blocks A and B), key columns / O columns of half `half`. Pass 1 runs on
+        // the whole row in both warps of a quadrant (identical results); pass 2, the
+        // P codes, the exact path and the dequant cover the warp's half only.
+        ptx::setmaxnreg_inc<C::REG_COMPUTE>();
+        const uint32_t quad = warp & 3;
+        const uint32_t half = (uint32_t)(warp - 4) >> 2;
+        const uint32_t side = lane >> 4;
+        const uint32_t r = quad * 16 + (lane & 15); // row within its q-block
+        const uint32_t lane_base = (quad * 32) << 16;
+        float2* red = reinterpret_cast<float2*>(smem + C::OFF_RED);
+        float4* rowmeta = reinterpret_cast<float4*>(smem + C::OFF_ROWMETA);
+        float* usm = reinterpret_cast<float*>(smem + C::OFF_U);
+        float* lsm = reinterpret_cast<float*>(smem + C::OFF_L); // [2 item parity][2 half][2 side][64]
+        RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
+        const uint32_t tail = L.N & 63;
+        constexpr int DH = D / 2; // O columns per warp
+        uint32_t T = 0, I = 0;
+        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t rr = 0; rr < rounds; ++rr) {
+            const int it = item_at(rr);
+            if (it < 0)
+                continue;
+            const Item x = load_item(L, (uint32_t)it);
+            const bool has_qb = side ? x.qb != 0xffffu : true;
+            const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
+            const uint32_t nmine = side ? x.nb : x.na;
+            const uint16_t* list = L.items + ((size_t)x.h * L.kb + qb) * L.kb;
+            const bool valid_row = has_qb && qb * 64 + r < L.N;
+            const float sq0 = L.qsc[((size_t)x.h * L.kb2 + qb) * G];
+            const float sq1 = G == 2 ? L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
+            RowState st{-INFINITY, 0.f, -INFINITY};
+            uint64_t acc[DH / 2];
+#pragma unroll
+            for (int c = 0; c < DH / 2; ++c)
+                acc[c] = 0ull;
+            // acc = gamma * acc + (pscale * vscale) * ip + u_c over this warp's O columns,
+            // for step U (its P side was published before this warp's own PFULL arrive)
+            auto dequant = [&](uint32_t U) {
+                const uint32_t b = U & 1, ph = (U >> 1) & 1;
+                PROF_T(te0);
+                ptx::mbar_wait(bar(BR::OFULL + b), ph);
+                ptx::tc_fence_after();
+                PROF_T(te1);
+                PROF_ADD(5, te1 - te0);
+                // idle rows carry gamma 1, ss 0 and u 0: acc*1 + 0*ip + 0 == acc exactly
+                const float4 rm = rowmeta[(b * 2 + side) * 64 + r];
+                const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
+                const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + side) * D + half * DH);
+#pragma unroll
+                for (int ch = 0; ch < DH / 16; ++ch) {
+                    uint32_t raw[16];
+                    tmem_ld16(tmem + lane_base + C::TM_O + b * D + half * DH + ch * 16, raw);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 uu = u4[ch * 4 + q4];
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int j = q4 * 4 + hh * 2;
+                            const uint64_t x2 =
+                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                            const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
+                            acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(bar(BR::OEMPTY + b));
+                    ptx::mbar_arrive(bar(BR::PEMPTY + b));
+                }
+                PROF_T(te2);
+                PROF_ADD(6, te2 - te1);
+            };
+            for (uint32_t t = 0; t < x.n; ++t, ++T) {
+                const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
+                const bool live = t < nmine;
+                const uint32_t bj = live ? list[t] : 0u;
+                PROF_T(tw0);
+                mbar_wait3(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
+                ptx::tc_fence_after();
+                PROF_T(tw1);
+                PROF_ADD(0, tw1 - tw0);
+                const float* meta =
+                    reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES + 4 * C::KV_BYTES +
+                                                   side * C::META_BYTES);
+                uint8_t* prow = smem + C::OFF_P + (b * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
+                const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
+                float2* red_w = red + ((T & 1) * 4 + quad) * 2 + side;
+                const float2* red_r = red + (T & 1) * 8 + side;
+                const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
+                RowStat* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
+                const RowStat* rs_r = rowstat + (T & 1) * 128;
+                const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
+                const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
+                float gamma, lo, pscale;
+                softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
+                                      tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r,
+                                      side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half, prof);
+                PROF_T(tw2);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    ptx::mbar_arrive(bar(BR::SEMPTY + b));
+                if (half == 0) {
+                    const float vsc = meta[2];
+                    rowmeta[(b * 2 + side) * 64 + r] =
+                        make_float4(live ? gamma : 1.f, live ? pscale * vsc : 0.f, 0.f, live ? 1.f : 0.f);
+                    // per-column offset term of this tile: (lo * vscale) * colsum[c]; exactly 0
+                    // when idle (an idle side's meta slot is not loaded: stale smem, maybe NaN)
+                    const float os = lo * vsc;
+                    float* u = usm + (b * 2 + side) * D;
+#pragma unroll
+                    for (int c = 0; c < D / 64; ++c)
+                        u[r + 64 * c] = live ? os * meta[4 + r + 64 * c] : 0.f;
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0)
+                    ptx::mbar_arrive(bar(BR::PFULL + b));
+                PROF_T(tw3);
+                PROF_ADD(4, tw3 - tw2);
+                if (t > 0) // its PV was issued a whole step earlier
+                    dequant(T - 1);
+                PROF_ADD(7, 1);
+            }
+            if (x.n > 0)
+                dequant(T - 1);
+            __syncwarp();
+            if (lane == 0)
+                ptx::mbar_arrive(qempty(I)); // this warp no longer reads the item's Q tiles
+            // row sum = the two halves' partial sums (same order in both warps)
+            float* lw = lsm + (I & 1) * 256;
+            lw[(half * 2 + side) * 64 + r] = st.l;
+            ptx::named_bar_sync(2 + quad, 64);
+            const float l = lw[side * 64 + r] + lw[(2 + side) * 64 + r];
+            ++I;
+            if (valid_row) {
+                const uint32_t orig = perm_src(L.perm[x.h], qb * 64 + r);
+                float4* dst = reinterpret_cast<float4*>(P.out + ((size_t)x.h * L.N + orig) * D + half * DH);
+                if (l == 0.f) {
+#pragma unroll
+                    for (int c = 0; c < DH / 4; ++c)
+                        dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    const float il = 1.0f / l;
+#pragma unroll
+                    for (int c = 0; c < DH / 4; ++c) {
+                        float a0, a1, a2, a3;
+                        upk(acc[2 * c], a0, a1);
+                        upk(acc[2 * c + 1], a2, a3);
+                        dst[c] = make_float4(a0 * il, a1 * il, a2 * il, a3 * il);
+                    }
+                }
+                if (P.zeroed && half == 0)
+                    P.zeroed[(size_t)x.h * L.N + orig] = l == 0.f ? 1 : 0;
+            }
+        }
+#ifdef PARO_K3_PROF
+        if (lane == 0)
+            for (int i = 0; i < 8; ++i)
+                atomicAdd(&g_prof[i], prof[i]);
+#endif
+    } else {
+        ptx::setmaxnreg_dec<C::REG_LOW>(); // warps 2-3: idle members of warpgroup 0
     }
 
     ptx::tc_fence_before();
@@ -1218,7 +1396,7 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
     cudaError_t e = cudaFuncSetAttribute(k3_attention<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    k3_attention<D><<<grid, 320, smem, st>>>(p, tq, tk, tv);
+    k3_attention<D><<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv);
     return cudaGetLastError();
 }
 
@@ -1256,11 +1434,11 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
         unsigned long long h[16];
         cudaDeviceSynchronize();
         cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
-        fprintf(stderr, "[k3 prof] softmax/step: wait %.0f pass1 %.0f reduce %.0f pass2 %.0f exact %.0f post %.0f (steps %llu items %llu)\n",
-                (double)h[0] / h[6], (double)h[1] / h[6], (double)h[2] / h[6], (double)h[3] / h[6], (double)h[4] / h[6],
-                (double)h[5] / h[6], h[6], h[7]);
-        fprintf(stderr, "[k3 prof] epilogue/step: wait %.0f dequant %.0f store/item %.0f (steps %llu)\n",
-                (double)h[8] / h[11], (double)h[9] / h[11], (double)h[10] / (h[7] ? h[7] : 1) , h[11]);
+        const double n = (double)(h[7] ? h[7] : 1);
+        fprintf(stderr,
+                "[k3 prof] compute warp/step: wait %.0f pass1 %.0f reduce %.0f pass2 %.0f exact+publish %.0f "
+                "dequant-wait %.0f dequant %.0f (warp-steps %llu)\n",
+                h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7]);
         fprintf(stderr, "[k3 prof] mma/step: wait KV+S %.0f wait P+O %.0f (steps %llu)\n", (double)h[12] / h[15],
                 (double)h[13] / h[15], h[15]);
         memset(h, 0, sizeof(h));
