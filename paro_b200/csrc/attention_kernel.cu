@@ -84,7 +84,8 @@ struct K3Cfg {
     static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;        // [2 parity][4 quad][2 side] float2
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
     static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
-    static constexpr uint32_t OFF_BAR = OFF_ROWSTAT + 2 * 2 * 64 * 40;
+    static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
+    static constexpr uint32_t OFF_BAR = OFF_XCH + (SPLIT ? 2 * 2 * 64 * 16 : 0);
     static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
@@ -413,7 +414,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             uint32_t half, unsigned long long (&prof)[8]) {
+                                             uint32_t half, float4* xch, unsigned long long (&prof)[8]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -471,8 +472,11 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             M1[c] = M2[c] = -INFINITY;
             N1[c] = N2[c] = INFINITY;
         }
+        // SPLIT: each warp of the quadrant pair scans its 32 key columns; the pair
+        // then exchanges its top-2 / bottom-2 through smem (one 64-thread barrier)
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
+        for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) {
+            const int h2 = SPLIT ? (int)half : hh;
             uint32_t x0[32], x1[32];
             ptx::tmem_ld32(s_addr + h2 * 32, x0);
             ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
@@ -500,8 +504,19 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             N2[c] = fmin3(fminf(N2[c], N2[c + 2]), fmaxf(N1[c], N1[c + 2]), INFINITY);
             N1[c] = fminf(N1[c], N1[c + 2]);
         }
-        const float mA = fmaxf(M1[0], M1[1]), mB = fmax3(fminf(M1[0], M1[1]), M2[0], M2[1]);
-        const float nA = fminf(N1[0], N1[1]), nB = fmin3(fmaxf(N1[0], N1[1]), N2[0], N2[1]);
+        float mA = fmaxf(M1[0], M1[1]), mB = fmax3(fminf(M1[0], M1[1]), M2[0], M2[1]);
+        float nA = fminf(N1[0], N1[1]), nB = fmin3(fmaxf(N1[0], N1[1]), N2[0], N2[1]);
+        if (SPLIT) {
+            xch[(half * 2 + side) * 64 + r] = make_float4(mA, mB, nA, nB);
+            ptx::named_bar_sync(2 + r / 16, 64); // the quadrant's two warps
+            const float4 o = xch[((half ^ 1) * 2 + side) * 64 + r];
+            // merge in half order so both warps get bit-identical results
+            const float4 a = half ? o : make_float4(mA, mB, nA, nB), b = half ? make_float4(mA, mB, nA, nB) : o;
+            mA = fmaxf(a.x, b.x);
+            mB = fmax3(fminf(a.x, b.x), a.y, b.y);
+            nA = fminf(a.z, b.z);
+            nB = fmin3(fmaxf(a.z, b.z), a.w, b.w);
+        }
         const float slack = kErrS * (c0 + c1) * kSBound + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
         const bool unsure = !(mA - mB > slack) || !(nB - nA > slack);
         int32_t s0x, s1x, s0n, s1n;
@@ -999,7 +1014,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 float gamma, lo, pscale;
                 softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
-                                gamma, lo, pscale, 0u, prof);
+                                gamma, lo, pscale, 0u, nullptr, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1239,7 +1254,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 float gamma, lo, pscale;
                 softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
                                       tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r,
-                                      side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half, prof);
+                                      side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half,
+                                      reinterpret_cast<float4*>(smem + C::OFF_XCH), prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
