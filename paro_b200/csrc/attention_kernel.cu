@@ -85,7 +85,7 @@ struct K3Cfg {
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
     static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
     static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
-    static constexpr uint32_t OFF_BAR = OFF_XCH + (SPLIT ? 2 * 2 * 64 * 16 : 0);
+    static constexpr uint32_t OFF_BAR = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 8) : 0); // + int2 S pairs
     static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
@@ -185,7 +185,7 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
 //   [8..11] epilogue: wait, dequant, store, steps
 //   [12..15] mma: wait KV/S, wait P/O, issue, steps
 #ifdef PARO_K3_PROF
-static __device__ unsigned long long g_prof[16];
+static __device__ unsigned long long g_prof[24];
 #define PROF_T(v) const long long v = clock64()
 #define PROF_ADD(i, d) prof[i] += (unsigned long long)(d)
 #else
@@ -414,7 +414,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             uint32_t half, float4* xch, unsigned long long (&prof)[8]) {
+                                             uint32_t half, float4* xch, unsigned long long (&prof)[14]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -506,6 +506,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         }
         float mA = fmaxf(M1[0], M1[1]), mB = fmax3(fminf(M1[0], M1[1]), M2[0], M2[1]);
         float nA = fminf(N1[0], N1[1]), nB = fmin3(fmaxf(N1[0], N1[1]), N2[0], N2[1]);
+        PROF_T(tq0);
         if (SPLIT) {
             xch[(half * 2 + side) * 64 + r] = make_float4(mA, mB, nA, nB);
             ptx::named_bar_sync(2 + r / 16, 64); // the quadrant's two warps
@@ -517,12 +518,30 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             nA = fminf(a.z, b.z);
             nB = fmin3(fmaxf(a.z, b.z), a.w, b.w);
         }
+        PROF_T(tq1);
         const float slack = kErrS * (c0 + c1) * kSBound + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
         const bool unsure = !(mA - mB > slack) || !(nB - nA > slack);
         int32_t s0x, s1x, s0n, s1n;
-        dot2_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, __float_as_uint(nA) & 63u, s0x, s1x, s0n, s1n);
+        if (SPLIT) { // half 0 takes the argmax column, half 1 the argmin column, then swap
+            int32_t u0, u1;
+            dot_row128(qtile, ktile, r, __float_as_uint(half ? nA : mA) & 63u, u0, u1);
+            int2* xs = reinterpret_cast<int2*>(xch + 2 * 2 * 64);
+            xs[(half * 2 + side) * 64 + r] = make_int2(u0, u1);
+            ptx::named_bar_sync(2 + r / 16, 64);
+            const int2 o = xs[((half ^ 1) * 2 + side) * 64 + r];
+            s0x = half ? o.x : u0;
+            s1x = half ? o.y : u1;
+            s0n = half ? u0 : o.x;
+            s1n = half ? u1 : o.y;
+        } else {
+            dot2_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, __float_as_uint(nA) & 63u, s0x, s1x, s0n, s1n);
+        }
         double tmax64 = logit128(scale64, a64, a64b, s0x, s1x);
         double tmin64 = logit128(scale64, a64, a64b, s0n, s1n);
+#ifdef PARO_K3_PROF
+        asm volatile("" ::"d"(tmax64 + tmin64));
+#endif
+        PROF_T(tq2);
         if (__any_sync(0xffffffffu, unsure && valid)) {
             const float thr_hi = mA - slack, thr_lo = nA + slack;
 #pragma unroll 1
@@ -552,6 +571,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 }
             }
         }
+        PROF_T(tq3);
         if (live)
             m64 = fmax(st.m64, tmax64);
         m32 = (float)(m64 * kLog2e);
@@ -563,6 +583,14 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmin_r = ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
         if (!SPLIT || half == 0)
             *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
+        PROF_T(tq4);
+        PROF_ADD(8, tq0 - tp0);
+        PROF_ADD(9, tq1 - tq0);
+        PROF_ADD(10, tq2 - tq1);
+        PROF_ADD(11, tq3 - tq2);
+        PROF_ADD(12, tq4 - tq3);
+        if (__any_sync(0xffffffffu, unsure && valid))
+            PROF_ADD(13, 1);
     }
     // rescale when an earlier tile of the item was live (the reference's l > 0,
     // attention.cpp:170): both column halves agree on it
@@ -975,7 +1003,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         float* lsm = reinterpret_cast<float*>(smem + C::OFF_L);
         const uint32_t tail = L.N & 63;
         uint32_t T = 0, I = 0;
-        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t rr = 0; rr < rounds; ++rr) {
             const int it = item_at(rr);
             if (it < 0)
@@ -1172,7 +1200,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         const uint32_t tail = L.N & 63;
         constexpr int DH = D / 2; // O columns per warp
         uint32_t T = 0, I = 0;
-        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t rr = 0; rr < rounds; ++rr) {
             const int it = item_at(rr);
             if (it < 0)
@@ -1316,9 +1344,12 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             }
         }
 #ifdef PARO_K3_PROF
-        if (lane == 0)
+        if (lane == 0) {
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
+            for (int i = 8; i < 14; ++i)
+                atomicAdd(&g_prof[8 + i], prof[i]);
+        }
 #endif
     } else {
         ptx::setmaxnreg_dec<C::REG_LOW>(); // warps 2-3: idle members of warpgroup 0
@@ -1447,7 +1478,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
 #endif
 #ifdef PARO_K3_PROF
     if (getenv("PARO_K3_PROF_PRINT")) {
-        unsigned long long h[16];
+        unsigned long long h[24];
         cudaDeviceSynchronize();
         cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
         const double n = (double)(h[7] ? h[7] : 1);
@@ -1457,6 +1488,8 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
                 h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7]);
         fprintf(stderr, "[k3 prof] mma/step: wait KV+S %.0f wait P+O %.0f (steps %llu)\n", (double)h[12] / h[15],
                 (double)h[13] / h[15], h[15]);
+        fprintf(stderr, "[k3 prof] d=128 pass1: scan %.0f exchange %.0f dp4a %.0f rescan %.0f tail %.0f (rescans %.4f)\n",
+                h[16] / n, h[17] / n, h[18] / n, h[19] / n, h[20] / n, h[21] / n);
         memset(h, 0, sizeof(h));
         cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }
