@@ -712,6 +712,9 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     PROF_T(tp3);
     PROF_ADD(3, tp3 - tp2);
     // -------- exact boundary path (d=64): rare, warp-uniform entry
+#ifdef PARO_EXP_NOEXACT
+    risk = 0;
+#endif
     if (__any_sync(0xffffffffu, risk != 0)) {
         // exact tile lo/hi of both q-blocks from every row's published extremes
         // (only rows whose fast-path extreme is within 1e-5 of the fast tile

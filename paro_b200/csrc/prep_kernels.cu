@@ -39,6 +39,44 @@ __device__ __forceinline__ int quant_sym(float x, float scale, float rs, float q
     return q < 0.0f ? -m : m;
 }
 
+// Four codes of one float4 for K1. The clamp is provably a no-op there: the
+// group scale is RN(amax/qmax) >= (amax/qmax)(1 - 2^-24) and |x| <= amax, so
+// |x/scale| <= qmax(1 + 2^-23) and RN of it rounds (half away) to at most qmax
+// -- the same code the reference's clamp-then-round gives. The quotients are
+// formed two at a time with packed IEEE f32x2 ops (same per-lane rounding as
+// quant_sym's __fmul_rn / __fmaf_rn).
+__device__ __forceinline__ uint64_t f2pk(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2upk(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t quot2(uint64_t x2, uint64_t scale2, uint64_t rs2, uint64_t neg_scale2) {
+    uint64_t q0, e, q;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q0) : "l"(x2), "l"(rs2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(q0), "l"(neg_scale2), "l"(x2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(e), "l"(rs2), "l"(q0));
+    (void)scale2;
+    return q;
+}
+__device__ __forceinline__ int round_half_away(float q) {
+    const float t = __fadd_rd(fabsf(q), 0.5f);
+    const int m = (int)(__float_as_uint(__fadd_rd(t, 8388608.0f)) & 0x7fffffu);
+    return q < 0.0f ? -m : m;
+}
+__device__ __forceinline__ void quant_sym4(float4 v, float scale, float rs, int& c0, int& c1, int& c2, int& c3) {
+    const uint64_t s2 = f2pk(scale, scale), r2 = f2pk(rs, rs), ns2 = f2pk(-scale, -scale);
+    float a, b, c, d;
+    f2upk(quot2(f2pk(v.x, v.y), s2, r2, ns2), a, b);
+    f2upk(quot2(f2pk(v.z, v.w), s2, r2, ns2), c, d);
+    c0 = round_half_away(a);
+    c1 = round_half_away(b);
+    c2 = round_half_away(c);
+    c3 = round_half_away(d);
+}
+
 __device__ __forceinline__ float4 ld_stream(const float* p) {
     float4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -71,7 +109,7 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // zero V rows keep it out of P.V (K3 only corrects the row sum on tail tiles).
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const float* __restrict__ q,
+__global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(LayerDev L, const float* __restrict__ q,
                                                            const float* __restrict__ k, const float* __restrict__ v,
                                                            int v_bits, uint32_t head_begin) {
     constexpr int F4 = D / 4;        // float4 per row
@@ -154,14 +192,12 @@ __global__ void __launch_bounds__(256) k1_reorder_quantize(LayerDev L, const flo
     for (int j = 0; j < PASSES; ++j) {
         const size_t off = head_codes + (size_t)(b * 64 + r0 + RPP * j) * D + c4 * 4;
         const float4 a = xq[j], c = xk[j], e = xv[j];
-        *reinterpret_cast<uint32_t*>(L.q + off) =
-            pack4(quant_sym(a.x, sq, rq, 127.f), quant_sym(a.y, sq, rq, 127.f), quant_sym(a.z, sq, rq, 127.f),
-                  quant_sym(a.w, sq, rq, 127.f));
-        *reinterpret_cast<uint32_t*>(L.k + off) =
-            pack4(quant_sym(c.x, sk, rk, 127.f), quant_sym(c.y, sk, rk, 127.f), quant_sym(c.z, sk, rk, 127.f),
-                  quant_sym(c.w, sk, rk, 127.f));
-        const int v0 = quant_sym(e.x, sv, rv, vq), v1 = quant_sym(e.y, sv, rv, vq), v2 = quant_sym(e.z, sv, rv, vq),
-                  v3 = quant_sym(e.w, sv, rv, vq);
+        int a0, a1, a2, a3, k0, k1, k2, k3, v0, v1, v2, v3;
+        quant_sym4(a, sq, rq, a0, a1, a2, a3);
+        quant_sym4(c, sk, rk, k0, k1, k2, k3);
+        quant_sym4(e, sv, rv, v0, v1, v2, v3);
+        *reinterpret_cast<uint32_t*>(L.q + off) = pack4(a0, a1, a2, a3);
+        *reinterpret_cast<uint32_t*>(L.k + off) = pack4(k0, k1, k2, k3);
         *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
         cs0 += v0;
         cs1 += v1;
