@@ -48,7 +48,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["maskgen"],
+                    help="maskgen: the GPU mask producer (K5) on one c2-shaped calibration map instead of the layer")
     ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -204,8 +205,83 @@ def cpu_reference_sample(cfg_name, threads, max_heads=None):
 
 
 # ----------------------------------------------------------------------------- main
+def maskgen_main(args):
+    """K5 on one CogVideoX-shaped calibration map (N = 17550, 1.23 GB fp32): fused
+    apply_perm_map + block_sums (HBM-bound: the map is read once) and gen_mask on
+    the resulting 275 x 275 grid; the reference's CPU path (apply_perm_map +
+    block_sums, oracle/_ref) timed on the same map."""
+    import ctypes
+
+    import torch
+
+    import paro_b200 as paro
+
+    g = paro.parse_grid("F:13,H:30,W:45")
+    N = g.token_count()
+    k = (N + 63) // 64
+    plan = paro.make_perm(g, "WHF")
+    torch.manual_seed(0)
+    dmap = torch.rand((N, N), dtype=torch.float32, device="cuda")
+    dinv = torch.from_numpy(plan.inverse.astype(np.int32)).cuda()
+    dsum = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    dbits = torch.empty((k, k), dtype=torch.uint8, device="cuda")
+    ctx = paro.Context(0)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    lib = paro._lib
+
+    def sums():
+        paro._check(lib.paro_perm_block_sums_device(ctypes.c_void_p(ctx.ptr), sp, ctypes.c_void_p(dmap.data_ptr()),
+                                                    ctypes.c_uint32(N), ctypes.c_void_p(dinv.data_ptr()),
+                                                    ctypes.c_uint32(64), ctypes.c_void_p(dsum.data_ptr())))
+
+    for _ in range(max(args.warmup, 3)):
+        sums()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        sums()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    rep = (ctypes.c_uint32 * 1)()
+    t0 = time.perf_counter()
+    paro._check(lib.paro_gen_mask_device(ctypes.c_void_p(ctx.ptr), sp, ctypes.c_void_p(dsum.data_ptr()),
+                                         ctypes.c_uint32(1), ctypes.c_uint32(k), ctypes.c_uint32(k),
+                                         ctypes.c_double(0.3), ctypes.c_uint32(64), ctypes.c_uint32(0),
+                                         ctypes.c_void_p(dbits.data_ptr()), rep))
+    gm_ms = (time.perf_counter() - t0) * 1e3
+    bytes_ = N * N * 4.0
+    peak = measured_peaks()[0]
+    line = {"metric": "K5 mask producer: permuted block_sums of one calibration map (GB/s of map read)",
+            "value": bytes_ / ms / 1e6, "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 in, fp64 sums",
+            "data": "synthetic U[0,1) map on the device", "config": {"workload": f"N={N} (F:13,H:30,W:45) order WHF, block 64"},
+            "roofline": {"bound": "hbm", "achieved": bytes_ / ms / 1e6, "peak": peak, "unit": "GB/s",
+                         "frac": (bytes_ / ms / 1e6) / peak if peak else None, "traffic": None},
+            "gen_mask_ms_incl_sync": gm_ms}
+    try:
+        from oracle.pyoracle import Reference, have_reference
+
+        if have_reference():
+            r = Reference()
+            r.select_kernels("auto")
+            m = dmap.cpu().numpy()
+            t0 = time.perf_counter()
+            r.perm_block_sums(m, 64, plan.forward, plan.inverse)
+            cpu_s = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": bytes_ / cpu_s / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                                    "sample": "the same map: apply_perm_map + block_sums (main.cpp:236-238)"}
+    except Exception as e:  # the CPU leg is a reported baseline only
+        line["cpu_baseline"] = {"unavailable": str(e)[:120]}
+    print(json.dumps(line))
+
+
 def main():
     args = parse_args()
+    if args.config == "maskgen":
+        return maskgen_main(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -87,6 +87,37 @@ int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_r
 int paro_gen_mask(const double* sums, uint32_t k_rows, uint32_t k_cols, double density, uint32_t block,
                   uint32_t guard_blocks, uint8_t* bits, uint32_t* repaired_rows);
 
+/* ---------------------------------------------------------------------------
+ * Mask producer on the GPU. Device pointers; the
+ * calls validate like the reference and return its error classes.
+ * ------------------------------------------------------------------------- */
+
+/* block_sums(AttnMap(apply_perm_map(map, plan), block)) fused -- replaces
+ * reorder.cpp:103-114 + metrics.cpp:41-58 (cmd_maskgen, main.cpp:236-238):
+ * map fp32 [n][n] (device), inverse = plan.inverse (device, NULL = identity),
+ * sums fp64 [k][k] (device), k = ceil(n/block), block <= 256. The N x N map is read
+ * once; sums are bit-identical to the reference's scalar kernels. */
+int paro_perm_block_sums_device(paro_ctx* ctx, paro_stream_t stream, const float* map, uint32_t n,
+                                const uint32_t* inverse, uint32_t block, double* sums);
+
+/* gen_mask(sums, density, block, guard) for `count` grids -- replaces
+ * mask.cpp:56-130 (incl. guard blocks and the degenerate-row repair):
+ * sums fp64 [count][k_rows][k_cols] (device), bits [count][k_rows][k_cols]
+ * (device, one byte per block), repaired_rows (host, count entries, may be
+ * NULL). Synchronises `stream`. Bit-identical to the reference. */
+int paro_gen_mask_device(paro_ctx* ctx, paro_stream_t stream, const double* sums, uint32_t count, uint32_t k_rows,
+                         uint32_t k_cols, double density, uint32_t block, uint32_t guard, uint8_t* bits,
+                         uint32_t* repaired_rows);
+
+/* build_schedule(calib sums, density, T, block, guard) -- replaces
+ * mask.cpp:142-172: sums fp64 [T][k_rows][k_cols] (device); masks receives
+ * the T/2 distinct early masks then the shared late mask,
+ * [(T/2)+1][k_rows][k_cols] bytes (device); repaired_rows (host) = total.
+ * Serialize with paro_serialize_mask for a PSCH image. */
+int paro_build_schedule_device(paro_ctx* ctx, paro_stream_t stream, const double* sums, uint32_t timesteps,
+                               uint32_t k_rows, uint32_t k_cols, double density, uint32_t block, uint32_t guard,
+                               uint8_t* masks, uint32_t* repaired_rows);
+
 /* Synthetic N(0,1) fp32 inputs: MT19937-64, u = (x>>11)*2^-53, Box-Muller on
  * (1-u1, u2), the generator documented in synth.cpp:20-22,173-182. */
 int paro_synth_randn(uint64_t seed, size_t count, float* out);

@@ -287,6 +287,18 @@ class Reference:
             return rc, None, None
         return 0, bits, rep.value
 
+    def perm_block_sums(self, m, block, forward=None, inverse=None):
+        """block_sums(AttnMap(apply_perm_map(m, plan), block, relaxed)) of the reference."""
+        m = np.ascontiguousarray(m, np.float32)
+        n = m.shape[0]
+        k = (n + block - 1) // block
+        out = np.empty((k, k), np.float64)
+        f = None if forward is None else np.ascontiguousarray(forward, np.uint32)
+        i = None if inverse is None else np.ascontiguousarray(inverse, np.uint32)
+        self._chk(self.lib.ref_perm_block_sums(_ptr(m), SZ(n), _ptr(f) if f is not None else None,
+                                               _ptr(i) if i is not None else None, SZ(block), _ptr(out)))
+        return out
+
     def serialize_mask(self, bits, block):
         bits = np.ascontiguousarray(bits, np.uint8)
         kr, kc = bits.shape

@@ -27,6 +27,7 @@
 #include "paro/error.hpp"
 #include "paro/kernels.hpp"
 #include "paro/mask.hpp"
+#include "paro/metrics.hpp"
 #include "paro/quant.hpp"
 #include "paro/reorder.hpp"
 #include "paro/synth.hpp"
@@ -326,6 +327,25 @@ int ref_run_heads(const char* grid_text, size_t H_run, size_t d, const float* q,
         *seconds = std::chrono::duration<double>(t1 - t0).count();
         if (failed)
             throw paro::InvariantError("a reference head failed");
+    });
+}
+
+// block_sums(AttnMap(apply_perm_map(m, plan), block, relaxed)) -- cmd_maskgen's
+// sums (main.cpp:236-238); identity when forward is NULL
+int ref_perm_block_sums(const float* m, size_t n, const uint32_t* forward, const uint32_t* inverse, size_t block,
+                        double* out) {
+    return guarded([&] {
+        paro::Matrix mat(n, n);
+        std::memcpy(mat.data.data(), m, n * n * sizeof(float));
+        paro::Matrix pm = mat;
+        if (forward) {
+            paro::PermPlan plan;
+            plan.forward.assign(forward, forward + n);
+            plan.inverse.assign(inverse, inverse + n);
+            pm = paro::apply_perm_map(mat, plan);
+        }
+        paro::BlockGrid g = paro::block_sums(paro::AttnMap(std::move(pm), block, /*relaxed=*/true));
+        std::memcpy(out, g.v.data(), g.v.size() * sizeof(double));
     });
 }
 

@@ -436,6 +436,57 @@ class Context:
             _lib.paro_ctx_destroy(P(self.ptr))
             self.ptr = None
 
+    # -- mask producer ----------------------------------
+    def block_sums(self, m: np.ndarray, block: int = 64, plan: "PermPlan | None" = None) -> np.ndarray:
+        """block_sums(AttnMap(apply_perm_map(m, plan), block)) on the GPU, fused
+        (reorder.cpp:103-114, metrics.cpp:41-58; cmd_maskgen main.cpp:236-238).
+        Returns the fp64 [k, k] grid, bit-identical to the reference's scalar kernels."""
+        m = np.ascontiguousarray(m, np.float32)
+        if m.ndim != 2 or m.shape[0] != m.shape[1]:
+            raise ShapeError(f"attention map must be square, got {m.shape}")
+        n = m.shape[0]
+        if plan is not None and len(plan.inverse) != n:
+            raise ShapeError("apply_perm_map: map/plan size mismatch")
+        k = (n + block - 1) // block
+        dm = DeviceBuffer.from_array(m)
+        dinv = DeviceBuffer.from_array(np.ascontiguousarray(plan.inverse, np.uint32)) if plan is not None else None
+        ds = DeviceBuffer(k * k * 8)
+        _check(_lib.paro_perm_block_sums_device(P(self.ptr), None, P(dm.ptr), U32(n), P(dinv.ptr if dinv else None),
+                                                U32(block), P(ds.ptr)))
+        return ds.download((k, k), np.float64)
+
+    def gen_mask(self, sums: np.ndarray, density: float, block: int, guard_blocks: int = 0):
+        """gen_mask on the GPU for one [k, k] grid or a stack [count, k, k]
+        (mask.cpp:56-130). Returns (BlockMask | list[BlockMask], repaired rows)."""
+        s = np.ascontiguousarray(sums, np.float64)
+        stack = s.ndim == 3
+        s3 = s if stack else s[None]
+        count, kr, kc = s3.shape
+        ds = DeviceBuffer.from_array(s3)
+        db = DeviceBuffer(count * kr * kc)
+        rep = np.zeros(count, np.uint32)
+        _check(_lib.paro_gen_mask_device(P(self.ptr), None, P(ds.ptr), U32(count), U32(kr), U32(kc),
+                                         ctypes.c_double(density), U32(block), U32(guard_blocks), P(db.ptr),
+                                         P(_ptr(rep))))
+        bits = db.download((count, kr, kc), np.uint8)
+        masks = [BlockMask(kr, kc, block, bits[i]) for i in range(count)]
+        return (masks, rep.tolist()) if stack else (masks[0], int(rep[0]))
+
+    def build_schedule(self, sums: np.ndarray, density: float, block: int, guard_blocks: int = 0):
+        """build_schedule on the GPU (mask.cpp:142-172): sums [T, k, k] ->
+        (list of T/2 distinct masks + the shared late mask, total repaired rows)."""
+        s = np.ascontiguousarray(sums, np.float64)
+        T, kr, kc = s.shape
+        half = T // 2
+        ds = DeviceBuffer.from_array(s)
+        dm = DeviceBuffer((half + 1) * kr * kc)
+        rep = U32()
+        _check(_lib.paro_build_schedule_device(P(self.ptr), None, P(ds.ptr), U32(T), U32(kr), U32(kc),
+                                               ctypes.c_double(density), U32(block), U32(guard_blocks), P(dm.ptr),
+                                               ctypes.byref(rep)))
+        bits = dm.download((half + 1, kr, kc), np.uint8)
+        return [BlockMask(kr, kc, block, bits[i]) for i in range(half + 1)], rep.value
+
     # -- standalone stages -------------------------------------------------
     def apply_perm_rows(self, m: np.ndarray, plan: PermPlan) -> np.ndarray:
         """apply_perm_rows on the GPU (reorder.cpp:93-101)."""

@@ -31,6 +31,12 @@ cudaError_t launch_apply_perm_rows(const float* in, uint32_t rows, uint32_t cols
 cudaError_t launch_perm_tables(const PermDesc* perm, uint32_t H, uint32_t N, uint32_t* fwd, uint32_t* inv,
                                cudaStream_t st);
 cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st);
+cudaError_t launch_perm_block_sums(const float* map, uint32_t n, const uint32_t* inv, uint32_t block, double* sums,
+                                   cudaStream_t st);
+cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uint32_t kc, uint32_t guard, uint64_t K,
+                            uint8_t* bits, uint32_t* row_kept_scratch, uint32_t* repaired, int* status,
+                            cudaStream_t st);
+cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
@@ -560,6 +566,115 @@ int paro_gen_mask(const double* sums, uint32_t kr, uint32_t kc, double density, 
         }
         if (repaired_rows)
             *repaired_rows = repaired;
+    });
+}
+
+// gen_mask's configuration checks (mask.cpp:57-76); returns the number of
+// non-guard blocks to keep (target - guard_count)
+static uint64_t gen_mask_keep_count(uint32_t kr, uint32_t kc, double density, uint32_t guard) {
+    if (!(density > 0.0 && density <= 1.0))
+        fail(PARO_E_CONFIG, "density must be in (0,1], got " + std::to_string(density));
+    const size_t total = (size_t)kr * kc;
+    const size_t target = (size_t)std::ceil(density * (double)total);
+    size_t guard_count = 0;
+    if (guard > 0) {
+        const size_t gr = std::min<size_t>(guard, kr), gc = std::min<size_t>(guard, kc);
+        guard_count = total - (kr - gr) * (kc - gc);
+    }
+    if (guard_count > target)
+        fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
+                                " blocks but the dense prefix alone occupies " + std::to_string(guard_count));
+    if (guard == 0 && target < kr)
+        fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
+                                " blocks, fewer than the " + std::to_string(kr) + " rows that each need one");
+    return (uint64_t)(target - guard_count);
+}
+
+int paro_perm_block_sums_device(paro_ctx* ctx, paro_stream_t stream, const float* map, uint32_t n,
+                                const uint32_t* inverse, uint32_t block, double* sums) {
+    return guarded([&] {
+        if (block < 1)
+            fail(PARO_E_CONFIG, "block must be >= 1");
+        if (n == 0)
+            fail(PARO_E_SHAPE, "empty attention map");
+        if (block > 256)
+            fail(PARO_E_CONFIG, "device block_sums supports block <= 256");
+        set_device(ctx);
+        cuda_check(paro::launch_perm_block_sums(map, n, inverse, block, sums, (cudaStream_t)stream),
+                   "perm_block_sums");
+    });
+}
+
+// gen_mask for `count` grids on the device (synchronises `stream` to return
+// the repaired-row counts and the repair failure status)
+static void gen_mask_device_impl(const double* sums, uint32_t count, uint32_t kr, uint32_t kc, double density,
+                                 uint32_t guard, uint8_t* bits, uint32_t* repaired_rows, cudaStream_t st) {
+    const uint64_t K = gen_mask_keep_count(kr, kc, density, guard);
+    uint32_t* scratch = nullptr; // row_kept [count][kr] + repaired [count] + status
+    const size_t words = (size_t)count * kr + count + 1;
+    cuda_check(cudaMalloc(&scratch, words * 4), "gen_mask scratch");
+    struct Free {
+        uint32_t* p;
+        ~Free() { cudaFree(p); }
+    } guard_free{scratch};
+    cuda_check(cudaMemsetAsync(scratch, 0, words * 4, st), "gen_mask scratch");
+    uint32_t* rep_dev = scratch + (size_t)count * kr;
+    int* status_dev = reinterpret_cast<int*>(rep_dev + count);
+    cuda_check(paro::launch_gen_mask(sums, count, kr, kc, guard, K, bits, scratch, rep_dev, status_dev, st),
+               "gen_mask");
+    std::vector<uint32_t> host(count + 1);
+    cuda_check(cudaMemcpyAsync(host.data(), rep_dev, (count + 1) * 4, cudaMemcpyDeviceToHost, st), "gen_mask");
+    cuda_check(cudaStreamSynchronize(st), "gen_mask");
+    if (host[count] != 0)
+        fail(PARO_E_CONFIG, "cannot repair an empty mask row at density " + std::to_string(density));
+    if (repaired_rows)
+        std::memcpy(repaired_rows, host.data(), count * 4);
+}
+
+int paro_gen_mask_device(paro_ctx* ctx, paro_stream_t stream, const double* sums, uint32_t count, uint32_t k_rows,
+                         uint32_t k_cols, double density, uint32_t block, uint32_t guard, uint8_t* bits,
+                         uint32_t* repaired_rows) {
+    return guarded([&] {
+        (void)block; // recorded in the BlockMask only (mask.cpp:86)
+        if (count == 0 || k_rows == 0 || k_cols == 0)
+            fail(PARO_E_SHAPE, "empty block-sum grid");
+        set_device(ctx);
+        gen_mask_device_impl(sums, count, k_rows, k_cols, density, guard, bits, repaired_rows, (cudaStream_t)stream);
+    });
+}
+
+int paro_build_schedule_device(paro_ctx* ctx, paro_stream_t stream, const double* sums, uint32_t timesteps,
+                               uint32_t k_rows, uint32_t k_cols, double density, uint32_t block, uint32_t guard,
+                               uint8_t* masks, uint32_t* repaired_rows) {
+    return guarded([&] {
+        (void)block;
+        if (timesteps < 1)
+            fail(PARO_E_CONFIG, "schedule needs at least one timestep");
+        if (k_rows == 0 || k_cols == 0)
+            fail(PARO_E_SHAPE, "empty block-sum grid");
+        set_device(ctx);
+        const cudaStream_t st = (cudaStream_t)stream;
+        const uint32_t half = timesteps / 2;
+        const size_t total = (size_t)k_rows * k_cols;
+        uint32_t rep_total = 0;
+        std::vector<uint32_t> rep(half > 0 ? half : 1);
+        if (half > 0) { // distinct early masks, one per timestep (mask.cpp:155-159)
+            gen_mask_device_impl(sums, half, k_rows, k_cols, density, guard, masks, rep.data(), st);
+            for (uint32_t t = 0; t < half; ++t)
+                rep_total += rep[t];
+        }
+        double* mean = nullptr; // shared late mask from the mean of the late sums (:160-169)
+        cuda_check(cudaMalloc(&mean, total * sizeof(double)), "schedule mean");
+        struct Free {
+            double* p;
+            ~Free() { cudaFree(p); }
+        } guard_free{mean};
+        cuda_check(paro::launch_late_mean(sums, timesteps, total, mean, st), "schedule mean");
+        uint32_t r = 0;
+        gen_mask_device_impl(mean, 1, k_rows, k_cols, density, guard, masks + (size_t)half * total, &r, st);
+        rep_total += r;
+        if (repaired_rows)
+            *repaired_rows = rep_total;
     });
 }
 
