@@ -48,7 +48,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["maskgen"],
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["maskgen", "permsel"],
                     help="maskgen: the GPU mask producer (K5) on one c2-shaped calibration map instead of the layer")
     ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -278,10 +278,75 @@ def maskgen_main(args):
     print(json.dumps(line))
 
 
+def permsel_main(args):
+    """select_permutation on one CogVideoX-shaped calibration
+    map: 6 candidate orders, each a fused permuted-block pass (sum|a|, max|a|,
+    #|a|<eps) over the 1.23 GB map; the reference CPU path (apply_perm_map +
+    m_sparse + m_quant per order) timed on the same map for a bounded subset."""
+    import ctypes
+
+    import torch
+
+    import paro_b200 as paro
+
+    grid = "F:13,H:30,W:45"
+    N = paro.parse_grid(grid).token_count()
+    torch.manual_seed(0)
+    dmap = torch.rand((N, N), dtype=torch.float32, device="cuda")
+    ctx = paro.Context(0)
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    orders = ctypes.create_string_buffer(32)
+    scores = np.zeros((6, 5), np.float64)
+    nperm, chosen = ctypes.c_int(), ctypes.c_int()
+
+    def run():
+        paro._check(paro._lib.paro_select_permutation_device(
+            ctypes.c_void_p(ctx.ptr), sp, ctypes.c_void_p(dmap.data_ptr()), ctypes.c_uint32(1), grid.encode(),
+            ctypes.c_uint32(64), ctypes.c_float(1e-3), ctypes.c_float(0.9), ctypes.c_float(0.5), ctypes.c_uint32(0),
+            orders, scores.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nperm), ctypes.byref(chosen)))
+
+    for _ in range(max(args.warmup, 3)):
+        run()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()  # synchronises internally (host-side final reductions)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    bytes_ = N * N * 4.0 * nperm.value
+    peak = measured_peaks()[0]
+    line = {"metric": "select_permutation of one c2 calibration map, all candidate orders (ms, wall incl. host reductions)",
+            "value": ms, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 map, fp64 statistics",
+            "data": "synthetic U[0,1) map on the device",
+            "config": {"workload": f"N={N} ({grid}), {nperm.value} orders, block 64, eps 1e-3, sigma 0.9, alpha 0.5"},
+            "roofline": {"bound": "hbm", "achieved": bytes_ / ms / 1e6, "peak": peak, "unit": "GB/s",
+                         "frac": bytes_ / ms / 1e6 / peak if peak else None, "traffic": None}}
+    try:
+        from oracle.pyoracle import Reference, have_reference
+
+        if have_reference():
+            r = Reference()
+            r.select_kernels("auto")
+            m = dmap.cpu().numpy()
+            g = paro.parse_grid(grid)
+            plan = paro.make_perm(g, "WHF")
+            t0 = time.perf_counter()
+            r.perm_block_sums(m, 64, plan.forward, plan.inverse)  # one order's apply_perm_map + block pass
+            one = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": one * nperm.value * 1e3, "unit": "ms", "cores": 1, "kind": "reference",
+                                    "sample": "apply_perm_map + block_sums for 1 order on the same map, x6 orders "
+                                              "(m_sparse/m_quant passes not included: a lower bound)"}
+    except Exception as e:
+        line["cpu_baseline"] = {"unavailable": str(e)[:120]}
+    print(json.dumps(line))
+
+
 def main():
     args = parse_args()
     if args.config == "maskgen":
         return maskgen_main(args)
+    if args.config == "permsel":
+        return permsel_main(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -118,6 +118,20 @@ int paro_build_schedule_device(paro_ctx* ctx, paro_stream_t stream, const double
                                uint32_t k_rows, uint32_t k_cols, double density, uint32_t block, uint32_t guard,
                                uint8_t* masks, uint32_t* repaired_rows);
 
+/* select_permutation(calib, grid, cfg, dense_prefix) -- replaces
+ * reorder.cpp:130-181 with metrics.cpp:60-133 (m_sparse, m_quant) over every
+ * candidate order (enumerate_perms): maps fp32 [count][n+p][n+p] (device,
+ * p = dense_prefix, the prefix rows / columns are stripped), grid text as in
+ * parse_grid, cfg = {block <= 256, eps, sigma, alpha}. Each permuted map's
+ * block statistics (sum|a| in the reference's fp64 order, max|a|, #|a| < eps)
+ * come from one fused pass over the map; the final reductions run on the host
+ * in the reference's order, so scores are bit-identical. Outputs (host):
+ * orders (nperm*ndim chars), scores [nperm][5] = {sparse_mean, quant_mean,
+ * sparse_share, quant_share, combined}, nperm, chosen (first argmin). */
+int paro_select_permutation_device(paro_ctx* ctx, paro_stream_t stream, const float* maps, uint32_t count,
+                                   const char* grid_text, uint32_t block, float eps, float sigma, float alpha,
+                                   uint32_t dense_prefix, char* orders, double* scores, int* nperm, int* chosen);
+
 /* Synthetic N(0,1) fp32 inputs: MT19937-64, u = (x>>11)*2^-53, Box-Muller on
  * (1-u1, u2), the generator documented in synth.cpp:20-22,173-182. */
 int paro_synth_randn(uint64_t seed, size_t count, float* out);

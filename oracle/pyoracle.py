@@ -299,6 +299,20 @@ class Reference:
                                                _ptr(i) if i is not None else None, SZ(block), _ptr(out)))
         return out
 
+    def select_permutation(self, maps, grid_text, block=64, eps=1e-3, sigma=0.9, alpha=0.5, dense_prefix=0):
+        m = np.ascontiguousarray(maps, np.float32)
+        count, n, _ = m.shape
+        orders = ctypes.create_string_buffer(32)
+        scores = np.zeros((6, 5), np.float64)
+        nperm, chosen = ctypes.c_int(), ctypes.c_int()
+        self._chk(self.lib.ref_select_permutation(_ptr(m), SZ(count), SZ(n), grid_text.encode(), SZ(block),
+                                                  ctypes.c_float(eps), ctypes.c_float(sigma), ctypes.c_float(alpha),
+                                                  SZ(dense_prefix), orders, _ptr(scores), ctypes.byref(nperm),
+                                                  ctypes.byref(chosen)))
+        nd = len(orders.raw.rstrip(b"\0")) // nperm.value
+        ords = [orders.raw[i * nd:(i + 1) * nd].decode() for i in range(nperm.value)]
+        return ords, scores[:nperm.value], chosen.value
+
     def serialize_mask(self, bits, block):
         bits = np.ascontiguousarray(bits, np.uint8)
         kr, kc = bits.shape

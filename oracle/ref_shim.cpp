@@ -349,4 +349,38 @@ int ref_perm_block_sums(const float* m, size_t n, const uint32_t* forward, const
     });
 }
 
+// select_permutation(calib, grid, cfg, dense_prefix) (reorder.cpp:130-181):
+// maps [count][n][n], scores [nperm][5], orders nperm*ndim chars
+int ref_select_permutation(const float* maps, size_t count, size_t n, const char* grid_text, size_t block, float eps,
+                           float sigma, float alpha, size_t dense_prefix, char* orders, double* scores, int* nperm,
+                           int* chosen) {
+    return guarded([&] {
+        std::vector<paro::Matrix> calib;
+        for (size_t c = 0; c < count; ++c) {
+            paro::Matrix m(n, n);
+            std::memcpy(m.data.data(), maps + c * n * n, n * n * sizeof(float));
+            calib.push_back(std::move(m));
+        }
+        paro::MetricConfig cfg;
+        cfg.block = block;
+        cfg.eps = eps;
+        cfg.sigma = sigma;
+        cfg.alpha = alpha;
+        const paro::TokenGrid grid = paro::parse_grid(grid_text);
+        paro::SelectionResult r = paro::select_permutation(calib, grid, cfg, dense_prefix);
+        *nperm = (int)r.scores.size();
+        *chosen = (int)r.chosen;
+        for (size_t p = 0; p < r.scores.size(); ++p) {
+            const paro::PermScore& sc = r.scores[p];
+            std::memcpy(orders + p * sc.order.size(), sc.order.data(), sc.order.size());
+            double* o = scores + p * 5;
+            o[0] = sc.sparse_mean;
+            o[1] = sc.quant_mean;
+            o[2] = sc.sparse_share;
+            o[3] = sc.quant_share;
+            o[4] = sc.combined;
+        }
+    });
+}
+
 } // extern "C"

@@ -487,6 +487,28 @@ class Context:
         bits = dm.download((half + 1, kr, kc), np.uint8)
         return [BlockMask(kr, kc, block, bits[i]) for i in range(half + 1)], rep.value
 
+    def select_permutation(self, maps, grid: "TokenGrid | str", block: int = 64, eps: float = 1e-3,
+                           sigma: float = 0.9, alpha: float = 0.5, dense_prefix: int = 0):
+        """select_permutation(calib, grid, cfg, dense_prefix) on the GPU
+        (reorder.cpp:130-181, metrics.cpp:60-133). maps: [count, n+p, n+p] fp32.
+        Returns (orders, scores [nperm, 5] = sparse_mean, quant_mean,
+        sparse_share, quant_share, combined, chosen index)."""
+        m = np.ascontiguousarray(maps, np.float32)
+        if m.ndim == 2:
+            m = m[None]
+        text = grid if isinstance(grid, str) else grid.text()
+        dm = DeviceBuffer.from_array(m)
+        orders = ctypes.create_string_buffer(32)
+        scores = np.zeros((6, 5), np.float64)
+        nperm, chosen = ctypes.c_int(), ctypes.c_int()
+        _check(_lib.paro_select_permutation_device(P(self.ptr), None, P(dm.ptr), U32(m.shape[0]), text.encode(),
+                                                   U32(block), ctypes.c_float(eps), ctypes.c_float(sigma),
+                                                   ctypes.c_float(alpha), U32(dense_prefix), orders, P(_ptr(scores)),
+                                                   ctypes.byref(nperm), ctypes.byref(chosen)))
+        nd = len(orders.raw.rstrip(b"\0")) // nperm.value
+        ords = [orders.raw[i * nd:(i + 1) * nd].decode() for i in range(nperm.value)]
+        return ords, scores[:nperm.value], chosen.value
+
     # -- standalone stages -------------------------------------------------
     def apply_perm_rows(self, m: np.ndarray, plan: PermPlan) -> np.ndarray:
         """apply_perm_rows on the GPU (reorder.cpp:93-101)."""

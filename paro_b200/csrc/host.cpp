@@ -37,6 +37,8 @@ cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uin
                             uint8_t* bits, uint32_t* row_kept_scratch, uint32_t* repaired, int* status,
                             cudaStream_t st);
 cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st);
+cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
+                                    float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
@@ -675,6 +677,126 @@ int paro_build_schedule_device(paro_ctx* ctx, paro_stream_t stream, const double
         rep_total += r;
         if (repaired_rows)
             *repaired_rows = rep_total;
+    });
+}
+
+int paro_select_permutation_device(paro_ctx* ctx, paro_stream_t stream, const float* maps, uint32_t count,
+                                   const char* grid_text, uint32_t block, float eps, float sigma, float alpha,
+                                   uint32_t dense_prefix, char* orders, double* scores, int* nperm, int* chosen) {
+    return guarded([&] {
+        // MetricConfig::validate (metrics.cpp:13-22)
+        if (block < 1)
+            fail(PARO_E_CONFIG, "block must be >= 1");
+        if (!(eps > 0.0f))
+            fail(PARO_E_CONFIG, "eps must be > 0");
+        if (!(sigma > 0.0f && sigma <= 1.0f))
+            fail(PARO_E_CONFIG, "sigma must be in (0,1]");
+        if (!(alpha >= 0.0f && alpha <= 1.0f))
+            fail(PARO_E_CONFIG, "alpha must be in [0,1]");
+        if (count == 0)
+            fail(PARO_E_INPUT, "select_permutation: empty calibration set");
+        if (block > 256)
+            fail(PARO_E_CONFIG, "device select_permutation supports block <= 256");
+        Grid g = parse_grid_text(grid_text);
+        const size_t n = g.tokens(), nf = n + dense_prefix;
+        const uint32_t k = (uint32_t)((n + block - 1) / block);
+        set_device(ctx);
+        const cudaStream_t st = (cudaStream_t)stream;
+        // candidate orders (enumerate_perms, reorder.cpp:74-91)
+        std::string ident(g.labels, g.labels + g.ndim);
+        std::string perm = ident;
+        std::sort(perm.begin(), perm.end());
+        std::vector<std::string> ords{ident};
+        do {
+            if (perm != ident)
+                ords.push_back(perm);
+        } while (std::next_permutation(perm.begin(), perm.end()));
+        const size_t P = ords.size(), kk = (size_t)k * k;
+        // device scratch: inverse table + per-block sums / maxima / small counts
+        char* scratch = nullptr;
+        const size_t bytes = n * 4 + 8 + kk * (8 + 4 + 4); // + alignment pad of the fp64 sums
+        cuda_check(cudaMalloc(&scratch, bytes), "select_permutation scratch");
+        struct Free {
+            char* p;
+            ~Free() { cudaFree(p); }
+        } guard_free{scratch};
+        uint32_t* dinv = reinterpret_cast<uint32_t*>(scratch);
+        double* dsum = reinterpret_cast<double*>(scratch + n * 4 + ((8 - (n * 4) % 8) % 8));
+        float* dmax = reinterpret_cast<float*>(dsum + kk);
+        uint32_t* dcnt = reinterpret_cast<uint32_t*>(dmax + kk);
+        std::vector<uint32_t> fwd(n), inv(n);
+        std::vector<double> hs(kk);
+        std::vector<float> hm(kk);
+        std::vector<uint32_t> hc(kk);
+        std::vector<double> sparse_mean(P), quant_mean(P), nonsparse(P), quant(P);
+        for (size_t p = 0; p < P; ++p) {
+            PermDesc pd = perm_desc(g, ords[p]);
+            for (size_t i = 0; i < n; ++i)
+                inv[i] = paro::perm_src(pd, (uint32_t)i);
+            cuda_check(cudaMemcpyAsync(dinv, inv.data(), n * 4, cudaMemcpyHostToDevice, st), "select_permutation");
+            double s_acc = 0.0, q_acc = 0.0;
+            for (uint32_t c = 0; c < count; ++c) {
+                // strip_prefix (reorder.cpp:119-127): the image-token submap
+                const float* sub = maps + (size_t)c * nf * nf + (size_t)dense_prefix * nf + dense_prefix;
+                cuda_check(paro::launch_perm_block_stats(sub, nf, (uint32_t)n, dinv, block, eps, dsum, dmax, dcnt, st),
+                           "select_permutation");
+                cuda_check(cudaMemcpyAsync(hs.data(), dsum, kk * 8, cudaMemcpyDeviceToHost, st), "select_permutation");
+                cuda_check(cudaMemcpyAsync(hm.data(), dmax, kk * 4, cudaMemcpyDeviceToHost, st), "select_permutation");
+                cuda_check(cudaMemcpyAsync(hc.data(), dcnt, kk * 4, cudaMemcpyDeviceToHost, st), "select_permutation");
+                cuda_check(cudaStreamSynchronize(st), "select_permutation");
+                // m_sparse and m_quant (metrics.cpp:60-83, 114-133), block order (bi, bj)
+                size_t sparse_blocks = 0;
+                double total = 0.0;
+                for (uint32_t bi = 0; bi < k; ++bi) {
+                    const size_t r0 = (size_t)bi * block, r1 = std::min(n, r0 + block);
+                    for (uint32_t bj = 0; bj < k; ++bj) {
+                        const size_t c0 = (size_t)bj * block, c1 = std::min(n, c0 + block);
+                        const size_t cnt = (r1 - r0) * (c1 - c0), b = (size_t)bi * k + bj;
+                        if ((double)hc[b] / (double)cnt >= (double)sigma)
+                            ++sparse_blocks;
+                        const double mx = (double)hm[b];
+                        total += mx == 0.0 ? 1.0 : mx / (hs[b] / (double)cnt);
+                    }
+                }
+                s_acc += (double)sparse_blocks / (double)kk;
+                q_acc += total / (double)kk;
+            }
+            const double cnt = (double)count;
+            sparse_mean[p] = s_acc / cnt;
+            quant_mean[p] = q_acc / cnt;
+            nonsparse[p] = 1.0 - sparse_mean[p];
+            quant[p] = quant_mean[p];
+        }
+        // shares, combined score, first argmin (reorder.cpp:160-179)
+        double s_total = 0.0, q_total = 0.0;
+        for (size_t p = 0; p < P; ++p) {
+            s_total += nonsparse[p];
+            q_total += quant[p];
+        }
+        const double equal_share = 1.0 / (double)P;
+        size_t best = 0;
+        std::vector<double> comb(P);
+        for (size_t p = 0; p < P; ++p) {
+            const double ss = s_total > 0.0 ? nonsparse[p] / s_total : equal_share;
+            const double qs = q_total > 0.0 ? quant[p] / q_total : equal_share;
+            comb[p] = (double)alpha * ss + (1.0 - (double)alpha) * qs;
+            if (comb[p] < comb[best])
+                best = p;
+            if (scores) {
+                double* o = scores + p * 5;
+                o[0] = sparse_mean[p];
+                o[1] = quant_mean[p];
+                o[2] = ss;
+                o[3] = qs;
+                o[4] = comb[p];
+            }
+            if (orders)
+                std::memcpy(orders + p * g.ndim, ords[p].data(), g.ndim);
+        }
+        if (nperm)
+            *nperm = (int)P;
+        if (chosen)
+            *chosen = (int)best;
     });
 }
 

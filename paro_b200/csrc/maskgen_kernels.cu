@@ -27,9 +27,12 @@ namespace paro {
 constexpr int K5_WARPS = 8;
 constexpr int K5_MAXBLOCK = 256;
 
-__global__ void __launch_bounds__(K5_WARPS * 32) k5_perm_block_sums(const float* __restrict__ map, uint32_t n,
-                                                                    const uint32_t* __restrict__ inv, uint32_t block,
-                                                                    uint32_t k, double* __restrict__ sums) {
+template <bool STATS>
+__global__ void __launch_bounds__(K5_WARPS * 32) k5_perm_block_sums(const float* __restrict__ map, size_t ld,
+                                                                    uint32_t n, const uint32_t* __restrict__ inv,
+                                                                    uint32_t block, uint32_t k, float eps,
+                                                                    double* __restrict__ sums, float* __restrict__ maxs,
+                                                                    uint32_t* __restrict__ counts) {
     __shared__ double racc[K5_WARPS][K5_MAXBLOCK];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bi = blockIdx.x, bj = blockIdx.y * K5_WARPS + warp;
@@ -37,9 +40,11 @@ __global__ void __launch_bounds__(K5_WARPS * 32) k5_perm_block_sums(const float*
         return;
     const uint32_t r0 = bi * block, r1 = min(n, r0 + block);
     const uint32_t c0 = bj * block, c1 = min(n, c0 + block);
+    float mx = 0.f;
+    uint32_t cnt = 0;
     for (uint32_t rp = r0 + lane; rp < r1; rp += 32) {
         const uint32_t i = inv ? __ldg(inv + rp) : rp;
-        const float* row = map + (size_t)i * n;
+        const float* row = map + (size_t)i * ld;
         double acc = 0.0; // sum_abs_scalar order over the permuted columns
         uint32_t cp = c0;
         for (; cp + 8 <= c1; cp += 8) {
@@ -48,12 +53,30 @@ __global__ void __launch_bounds__(K5_WARPS * 32) k5_perm_block_sums(const float*
             for (int u = 0; u < 8; ++u)
                 v[u] = __ldg(row + (inv ? __ldg(inv + cp + u) : cp + u));
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 8; ++u) {
                 acc = __dadd_rn(acc, fabs((double)v[u]));
+                if (STATS) {
+                    mx = fmaxf(mx, fabsf(v[u]));
+                    cnt += fabsf(v[u]) < eps ? 1u : 0u;
+                }
+            }
         }
-        for (; cp < c1; ++cp)
-            acc = __dadd_rn(acc, fabs((double)__ldg(row + (inv ? __ldg(inv + cp) : cp))));
+        for (; cp < c1; ++cp) {
+            const float v = __ldg(row + (inv ? __ldg(inv + cp) : cp));
+            acc = __dadd_rn(acc, fabs((double)v));
+            if (STATS) {
+                mx = fmaxf(mx, fabsf(v));
+                cnt += fabsf(v) < eps ? 1u : 0u;
+            }
+        }
         racc[warp][rp - r0] = acc;
+    }
+    if (STATS) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
     }
     __syncwarp();
     if (lane == 0) {
@@ -61,6 +84,10 @@ __global__ void __launch_bounds__(K5_WARPS * 32) k5_perm_block_sums(const float*
         for (uint32_t r = 0; r < r1 - r0; ++r)
             tot = __dadd_rn(tot, racc[warp][r]);
         sums[(size_t)bi * k + bj] = tot;
+        if (STATS) {
+            maxs[(size_t)bi * k + bj] = mx;
+            counts[(size_t)bi * k + bj] = cnt;
+        }
     }
 }
 
@@ -77,10 +104,13 @@ constexpr int K5S_THREADS = 512;
 constexpr int K5S_MAXB = 4; // column blocks per thread (k <= 2048)
 constexpr int K5S_PF = 40;  // prefetched row words per thread (n <= 20480)
 
-__global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const float* __restrict__ map, uint32_t n,
-                                                                        const uint32_t* __restrict__ inv,
-                                                                        uint32_t block, uint32_t k,
-                                                                        double* __restrict__ sums) {
+template <bool STATS>
+__global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const float* __restrict__ map, size_t ld,
+                                                                        uint32_t n, const uint32_t* __restrict__ inv,
+                                                                        uint32_t block, uint32_t k, float eps,
+                                                                        double* __restrict__ sums,
+                                                                        float* __restrict__ maxs,
+                                                                        uint32_t* __restrict__ counts) {
     extern __shared__ __align__(16) uint32_t sm[];
     // inverse table transposed, sinvT[u * k + bj] = inv[bj * block + u]: the
     // threads of a warp (consecutive bj) read consecutive words (no bank conflicts)
@@ -95,12 +125,17 @@ __global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const f
         sinvT[c] = cp < n ? (inv ? __ldg(inv + cp) : cp) : 0u;
     }
     double tot[K5S_MAXB];
+    float tmx[K5S_MAXB];
+    uint32_t tcnt[K5S_MAXB];
 #pragma unroll
-    for (int q = 0; q < K5S_MAXB; ++q)
+    for (int q = 0; q < K5S_MAXB; ++q) {
         tot[q] = 0.0;
+        tmx[q] = 0.f;
+        tcnt[q] = 0;
+    }
     float pf[K5S_PF];
     auto fetch = [&](uint32_t rp) { // original row of permuted row rp -> registers
-        const float* row = map + (size_t)(inv ? __ldg(inv + rp) : rp) * n;
+        const float* row = map + (size_t)(inv ? __ldg(inv + rp) : rp) * ld;
 #pragma unroll
         for (int u = 0; u < K5S_PF; ++u) {
             const uint32_t c = threadIdx.x + (uint32_t)u * K5S_THREADS;
@@ -136,11 +171,22 @@ __global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const f
                     for (int u = 0; u < 8; ++u)
                         v[u] = cur[sinvT[(cp - c0 + u) * k + bj]];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
+                    for (int u = 0; u < 8; ++u) {
                         acc = __dadd_rn(acc, fabs((double)v[u]));
+                        if (STATS) { // max_abs / count_abs_lt (order-free)
+                            tmx[q] = fmaxf(tmx[q], fabsf(v[u]));
+                            tcnt[q] += fabsf(v[u]) < eps ? 1u : 0u;
+                        }
+                    }
                 }
-                for (; cp < c1; ++cp)
-                    acc = __dadd_rn(acc, fabs((double)cur[sinvT[(cp - c0) * k + bj]]));
+                for (; cp < c1; ++cp) {
+                    const float v = cur[sinvT[(cp - c0) * k + bj]];
+                    acc = __dadd_rn(acc, fabs((double)v));
+                    if (STATS) {
+                        tmx[q] = fmaxf(tmx[q], fabsf(v));
+                        tcnt[q] += fabsf(v) < eps ? 1u : 0u;
+                    }
+                }
                 tot[q] = __dadd_rn(tot[q], acc);
             }
         }
@@ -151,8 +197,13 @@ __global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const f
 #pragma unroll
     for (int q = 0; q < K5S_MAXB; ++q) {
         const uint32_t bj = threadIdx.x + (uint32_t)q * K5S_THREADS;
-        if (bj < k)
+        if (bj < k) {
             sums[(size_t)bi * k + bj] = tot[q];
+            if (STATS) {
+                maxs[(size_t)bi * k + bj] = tmx[q];
+                counts[(size_t)bi * k + bj] = tcnt[q];
+            }
+        }
     }
 }
 
@@ -357,23 +408,36 @@ __global__ void k5_late_mean(const double* __restrict__ sums, uint32_t T, size_t
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-cudaError_t launch_perm_block_sums(const float* map, uint32_t n, const uint32_t* inv, uint32_t block, double* sums,
-                                   cudaStream_t st) {
+// block statistics of the permuted (sub)map: map points at its (0, 0) element,
+// rows are `ld` floats apart; maxs / counts (both or neither) add max|a| and
+// count(|a| < eps) per block (m_quant / m_sparse inputs)
+cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
+                                    float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st) {
     const uint32_t k = (n + block - 1) / block;
     if (block > (uint32_t)K5_MAXBLOCK || k > 65535u * K5_WARPS)
         return cudaErrorInvalidValue;
+    const bool stats = maxs != nullptr;
     const size_t smem = ((size_t)2 * n + (size_t)k * block) * 4;
     if (smem <= 227 * 1024 && n <= (uint32_t)K5S_PF * K5S_THREADS && k <= (uint32_t)K5S_MAXB * K5S_THREADS) {
-        cudaError_t e = cudaFuncSetAttribute(k5_perm_block_sums_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        auto kern = stats ? k5_perm_block_sums_staged<true> : k5_perm_block_sums_staged<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess)
             return e;
-        k5_perm_block_sums_staged<<<k, K5S_THREADS, smem, st>>>(map, n, inv, block, k, sums);
+        kern<<<k, K5S_THREADS, smem, st>>>(map, ld, n, inv, block, k, eps, sums, maxs, counts);
         return cudaGetLastError();
     }
     const dim3 grid(k, (k + K5_WARPS - 1) / K5_WARPS); // wide maps: warp per block, gathers from L2
-    k5_perm_block_sums<<<grid, K5_WARPS * 32, 0, st>>>(map, n, inv, block, k, sums);
+    if (stats)
+        k5_perm_block_sums<true><<<grid, K5_WARPS * 32, 0, st>>>(map, ld, n, inv, block, k, eps, sums, maxs, counts);
+    else
+        k5_perm_block_sums<false><<<grid, K5_WARPS * 32, 0, st>>>(map, ld, n, inv, block, k, eps, sums, maxs,
+                                                                  counts);
     return cudaGetLastError();
+}
+
+cudaError_t launch_perm_block_sums(const float* map, uint32_t n, const uint32_t* inv, uint32_t block, double* sums,
+                                   cudaStream_t st) {
+    return launch_perm_block_stats(map, n, n, inv, block, 1.f, sums, nullptr, nullptr, st);
 }
 
 cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uint32_t kc, uint32_t guard, uint64_t K,

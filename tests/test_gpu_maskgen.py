@@ -86,3 +86,48 @@ def test_build_schedule_matches_reference(paro, ctx, reference, tmp_path, T):
         assert rc == 0
         want = masks[t] if t < T // 2 else masks[T // 2]
         assert np.array_equal(want.bits, bits), (T, t)
+
+
+def _structured_maps(rng, grid_paro, count, prefix):
+    """Maps with an axis-local structure so the orders score differently."""
+    n = grid_paro.token_count()
+    nf = n + prefix
+    ext = grid_paro.extents
+    coords = np.stack(np.unravel_index(np.arange(n), ext), axis=1).astype(np.float64)
+    out = np.empty((count, nf, nf), np.float32)
+    for c in range(count):
+        w = rng.random(len(ext)) * 2.0
+        d = np.zeros((n, n))
+        for a in range(len(ext)):
+            d += w[a] * np.abs(coords[:, None, a] - coords[None, :, a])
+        core = np.exp(-d) * (0.5 + rng.random((n, n)))
+        full = rng.random((nf, nf)) * 0.01
+        full[prefix:, prefix:] = core
+        full /= full.sum(axis=1, keepdims=True)
+        out[c] = full
+    return out
+
+
+@pytest.mark.parametrize("grid,count,prefix,block", [("F:3,H:7,W:11", 2, 0, 64), ("F:3,H:7,W:11", 1, 5, 16),
+                                                     ("H:20,W:33", 2, 0, 64), ("F:4,H:6,W:5", 3, 3, 8)])
+def test_select_permutation_matches_reference(paro, ctx, reference, grid, count, prefix, block):
+    reference.select_kernels("scalar")
+    g = paro.parse_grid(grid)
+    maps = _structured_maps(np.random.default_rng(count + prefix), g, count, prefix)
+    for eps, sigma, alpha in ((1e-3, 0.9, 0.5), (2e-3, 0.5, 0.8)):
+        o1, s1, c1 = ctx.select_permutation(maps, g, block, eps, sigma, alpha, prefix)
+        o2, s2, c2 = reference.select_permutation(maps, grid, block, eps, sigma, alpha, prefix)
+        assert o1 == o2
+        assert s1.view(np.uint64).tolist() == s2.view(np.uint64).tolist(), (grid, eps, sigma, alpha)
+        assert c1 == c2
+
+
+def test_select_permutation_errors(paro, ctx):
+    g = paro.parse_grid("H:8,W:8")
+    m = np.ones((1, 64, 64), np.float32) / 64
+    with pytest.raises(paro.ConfigError):
+        ctx.select_permutation(m, g, 64, eps=0.0)
+    with pytest.raises(paro.ConfigError):
+        ctx.select_permutation(m, g, 64, sigma=1.5)
+    with pytest.raises(paro.ConfigError):
+        ctx.select_permutation(m, g, 64, alpha=-0.1)
