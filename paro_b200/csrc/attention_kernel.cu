@@ -85,7 +85,9 @@ struct K3Cfg {
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
     static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
     static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
-    static constexpr uint32_t OFF_BAR = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 8) : 0); // + int2 S pairs
+    static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 8) : 0); // + int2 S pairs
+    // exact path: per compute warp, its risky (owner lane, group) list (<= 32 x 16 entries)
+    static constexpr uint32_t OFF_BAR = OFF_XLIST + NCW * 512 * 2;
     static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
@@ -414,7 +416,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             uint32_t half, float4* xch, unsigned long long (&prof)[14]) {
+                                             uint32_t half, float4* xch, uint16_t* xlist,
+                                             unsigned long long (&prof)[14]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -768,41 +771,90 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             lo_e[sd] = mn;
             hi_e[sd] = mx;
         }
-        const float lo_x = side ? lo_e[1] : lo_e[0], hi_x = side ? hi_e[1] : hi_e[0];
-        float ps_x = __fdiv_rn(hi_x - lo_x, p_qmax);
-        if (ps_x == 0.f)
-            ps_x = 1.f;
-        while (risk) {
-            const int g = __ffs(risk) - 1;
-            risk &= risk - 1;
-#pragma unroll 1
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t j = 4 * g + e;
-                if (j >= ncol)
-                    continue;
-                int32_t Sj, S1j = 0;
-                if (G == 1)
-                    Sj = dot_row64(qtile, ktile, r, j);
-                else
-                    dot_row128(qtile, ktile, r, j, Sj, S1j);
-                { // re-run the two fast variants of this element; only a split pair needs fp64
-                    const float pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_i), c0, dmax))
-                                            : ex2(fmaf(__int2float_rn(S1j - smax1_i), c1,
-                                                       fmaf(__int2float_rn(Sj - smax_i), c0, dmax)));
-                    float ul, uh;
-                    upk(add2_rm(fma2_rm(pk(pf, pf), A2, B2), magic2), ul, uh);
-                    if (__float_as_uint(ul) == __float_as_uint(uh))
-                        continue;
-                }
-                const double logit = G == 1 ? __dmul_rn(scale64, __dmul_rn(a64, (double)Sj))
-                                            : logit128(scale64, a64, a64b, Sj, S1j);
-                const float p = (float)exp(logit - m64);
-                float q = __fdiv_rn(__fsub_rn(p, lo_x), ps_x);
-                q = fminf(p_qmax, fmaxf(0.f, q));
-                const int chunk = j >> 4;
-                prow[((chunk ^ ((r >> 1) & 3)) << 4) + (j & 15)] = (uint8_t)round_half_away_pos(q);
+        PROF_T(tx1);
+        PROF_ADD(8, tx1 - tp3);
+        // exact tile pscale of both sides (warp-uniform) and each side's fast-variant
+        // coefficients (uniform within a side: taken from lanes 0 and 16)
+        float ps_e[2];
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+            ps_e[sd] = __fdiv_rn(hi_e[sd] - lo_e[sd], p_qmax);
+            if (ps_e[sd] == 0.f)
+                ps_e[sd] = 1.f;
+        }
+        const uint64_t A2s[2] = {__shfl_sync(0xffffffffu, A2, 0), __shfl_sync(0xffffffffu, A2, 16)};
+        const uint64_t B2s[2] = {__shfl_sync(0xffffffffu, B2, 0), __shfl_sync(0xffffffffu, B2, 16)};
+        // the warp's risky 4-element groups, listed (owner lane, group) and spread
+        // over all 32 lanes one element each, instead of serially in their owner lanes
+        const uint32_t ng = __popc(risk);
+        uint32_t incl = ng;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o)
+                incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        {
+            uint32_t pos = incl - ng, rr = risk;
+            while (rr) {
+                const uint32_t g = __ffs(rr) - 1;
+                rr &= rr - 1;
+                xlist[pos++] = (uint16_t)((lane << 4) | g);
             }
         }
+        __syncwarp();
+        const int32_t rowoff = (int32_t)((r >> 3) * 512 + (r & 7) * 64);
+        for (uint32_t base = 0; base < 4 * total; base += 32) {
+            const uint32_t item = base + lane;
+            const bool act = item < 4 * total;
+            const uint32_t ent = act ? xlist[item >> 2] : (lane << 4);
+            const uint32_t o = ent >> 4, j = ((ent & 15u) << 2) + (item & 3u);
+            // the owner row's parameters
+            const uint32_t r_o = __shfl_sync(0xffffffffu, r, (int)o);
+            const int32_t smax_o = __shfl_sync(0xffffffffu, smax_i, (int)o);
+            const int32_t smax1_o = __shfl_sync(0xffffffffu, smax1_i, (int)o);
+            const float c0_o = __shfl_sync(0xffffffffu, c0, (int)o);
+            const float c1_o = __shfl_sync(0xffffffffu, c1, (int)o);
+            const float dmax_o = __shfl_sync(0xffffffffu, dmax, (int)o);
+            const double a64_o = __shfl_sync(0xffffffffu, a64, (int)o);
+            const double a64b_o = __shfl_sync(0xffffffffu, a64b, (int)o);
+            const double m64_o = __shfl_sync(0xffffffffu, m64, (int)o);
+            const uint32_t ncol_o = __shfl_sync(0xffffffffu, ncol, (int)o);
+            if (!act || j >= ncol_o)
+                continue;
+            const uint32_t so = o >> 4;
+            const int32_t dside = (int32_t)so - (int32_t)side;
+            const uint8_t* qt = qtile + dside * (int32_t)(64 * D);
+            const uint8_t* kt = ktile + dside * (int32_t)(64 * D);
+            int32_t Sj, S1j = 0;
+            if (G == 1)
+                Sj = dot_row64(qt, kt, r_o, j);
+            else
+                dot_row128(qt, kt, r_o, j, Sj, S1j);
+            { // re-run the two fast variants of this element; only a split pair needs fp64
+                const float pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o))
+                                        : ex2(fmaf(__int2float_rn(S1j - smax1_o), c1_o,
+                                                   fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o)));
+                float ul, uh;
+                upk(add2_rm(fma2_rm(pk(pf, pf), A2s[so], B2s[so]), magic2), ul, uh);
+                if (__float_as_uint(ul) == __float_as_uint(uh))
+                    continue;
+            }
+            const double logit = G == 1 ? __dmul_rn(scale64, __dmul_rn(a64_o, (double)Sj))
+                                        : logit128(scale64, a64_o, a64b_o, Sj, S1j);
+            const float p = (float)exp(logit - m64_o);
+            float q = __fdiv_rn(__fsub_rn(p, lo_e[so]), ps_e[so]);
+            q = fminf(p_qmax, fmaxf(0.f, q));
+            uint8_t* prow_o = prow + dside * (int32_t)(64 * 64) - rowoff +
+                              (int32_t)((r_o >> 3) * 512 + (r_o & 7) * 64);
+            const int chunk = j >> 4;
+            prow_o[((chunk ^ ((r_o >> 1) & 3)) << 4) + (j & 15)] = (uint8_t)round_half_away_pos(q);
+        }
+        __syncwarp();
+        PROF_T(tx2);
+        PROF_ADD(9, tx2 - tx1);
+        PROF_ADD(10, 1);
     }
     PROF_T(tp4);
     PROF_ADD(4, tp4 - tp3);
@@ -1045,7 +1097,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 float gamma, lo, pscale;
                 softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
-                                gamma, lo, pscale, 0u, nullptr, prof);
+                                gamma, lo, pscale, 0u, nullptr,
+                                reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 2) * 512, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1081,9 +1134,12 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ++I;
         }
 #ifdef PARO_K3_PROF
-        if (lane == 0)
+        if (lane == 0) {
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
+            for (int i = 8; i < 11; ++i)
+                atomicAdd(&g_prof[8 + i], prof[i]);
+        }
 #endif
         } else {
         // ------------------------------------------------------------ epilogue
@@ -1286,7 +1342,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
                                       tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r,
                                       side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half,
-                                      reinterpret_cast<float4*>(smem + C::OFF_XCH), prof);
+                                      reinterpret_cast<float4*>(smem + C::OFF_XCH),
+                                      reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1491,6 +1548,8 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
                 h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7]);
         fprintf(stderr, "[k3 prof] mma/step: wait KV+S %.0f wait P+O %.0f (steps %llu)\n", (double)h[12] / h[15],
                 (double)h[13] / h[15], h[15]);
+        fprintf(stderr, "[k3 prof] exact path: entries %llu, candidates %.0f, elements %.0f cycles/entry\n", h[18],
+                (double)h[16] / (h[18] ? h[18] : 1), (double)h[17] / (h[18] ? h[18] : 1));
         fprintf(stderr, "[k3 prof] d=128 pass1: scan %.0f exchange %.0f dp4a %.0f rescan %.0f tail %.0f (rescans %.4f)\n",
                 h[16] / n, h[17] / n, h[18] / n, h[19] / n, h[20] / n, h[21] / n);
         memset(h, 0, sizeof(h));
