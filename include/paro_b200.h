@@ -13,7 +13,8 @@
  *
  * Supported hot-path configuration (anything else is rejected with
  * PARO_E_CONFIG, never served by a CPU fallback): block = 64, d in {64, 128},
- * P/V bits in {4, 8}, dense_prefix = 0, 2-D (H,W) or 3-D (F,H,W) token grids.
+ * P/V bits in {4, 8}, 2-D (H,W) or 3-D (F,H,W) token grids, any dense_prefix
+ * (paro_layer_create_prefix).
  *
  * Threading: one paro_ctx per GPU, used from one host thread; layers belong to
  * the context they were created on. Device pointers are caller-owned unless a
@@ -181,6 +182,16 @@ int paro_quantize_sym_device(paro_ctx* ctx, paro_stream_t stream, const float* i
  * main.cpp:118-120). */
 int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text, const char* orders,
                       paro_layer** out);
+
+/* paro_layer_create with a dense text-token prefix (AttnInputs::dense_prefix,
+ * attention.cpp:134-199; PermPlan::with_prefix, reorder.cpp:30-47): the layer
+ * has N = grid tokens + dense_prefix rows, the first dense_prefix tokens keep
+ * their position under every head's order, attend densely and unquantized to
+ * all keys, and every key tile touching the prefix stays dense and unquantized
+ * for all rows (K4); the rest follows the quantized path (K3). Masks cover
+ * ceil(N/64)^2 blocks (gen_mask's guard blocks are the dense tiles). */
+int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text,
+                             const char* orders, uint32_t dense_prefix, paro_layer** out);
 int paro_layer_destroy(paro_layer* layer);
 
 /* Masks: H*k*k bytes (BlockMask::bits per head, mask.hpp:15-32), k = ceil(N/64);

@@ -142,7 +142,8 @@ inline paro::QuantBlockTensor quantize(const paro::Matrix& m, const paro::QuantC
 
 // quantized_blocked_attention (attention.hpp:52) with the INT8-QK stage, one
 // head on the GPU. The tile edge is mask->block, else qcfg.block
-// (attention.cpp:266-269); the B200 path serves block 64, dense_prefix 0.
+// (attention.cpp:266-269); the B200 path serves block 64 and any dense_prefix
+// below the token count (identity grid after the prefix, K4 + K3).
 inline paro::AttnResult quantized_blocked_attention(const paro::AttnInputs& in, const paro::BlockMask* mask,
                                                     const paro::QuantConfig& qcfg) {
     in.validate();
@@ -150,16 +151,16 @@ inline paro::AttnResult quantized_blocked_attention(const paro::AttnInputs& in, 
     const size_t block = mask ? mask->block : qcfg.block;
     if (block != 64)
         throw paro::ConfigError("the B200 path runs block 64, got " + std::to_string(block));
-    if (in.dense_prefix != 0)
-        throw paro::ConfigError("dense_prefix > 0 is not served by the B200 path");
-    const size_t n = in.tokens(), d = in.head_dim(), kb = (n + 63) / 64;
+    const size_t n = in.tokens(), d = in.head_dim(), kb = (n + 63) / 64, dp = in.dense_prefix;
+    if (n > 0 && dp >= n)
+        throw paro::ConfigError("dense_prefix covering every token is not served by the B200 path");
     if (mask && (mask->k_rows != kb || mask->k_cols != kb))
         throw paro::ShapeError("mask grid " + std::to_string(mask->k_rows) + "x" + std::to_string(mask->k_cols) +
                                " does not cover " + std::to_string(kb) + "x" + std::to_string(kb) + " blocks");
     paro_ctx* ctx = context();
-    const std::string grid = "H:1,W:" + std::to_string(n); // identity token order
+    const std::string grid = "H:1,W:" + std::to_string(n - dp); // identity token order after the prefix
     paro_layer* layer = nullptr;
-    check(paro_layer_create(ctx, 1, (uint32_t)d, grid.c_str(), nullptr, &layer));
+    check(paro_layer_create_prefix(ctx, 1, (uint32_t)d, grid.c_str(), nullptr, (uint32_t)dp, &layer));
     std::unique_ptr<paro_layer, int (*)(paro_layer*)> guard(layer, paro_layer_destroy);
     check(paro_layer_set_masks(layer, nullptr, mask ? mask->bits.data() : nullptr));
     paro::AttnResult res;

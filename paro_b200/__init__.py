@@ -548,12 +548,13 @@ class Context:
         block = mask.block if mask is not None else qcfg.block
         if block != 64:
             raise ConfigError(f"the B200 path runs block 64, got {block}")
-        if inp.dense_prefix != 0:
-            raise ConfigError("dense_prefix > 0 is not served by the B200 path")
+        dp = int(inp.dense_prefix)
+        if dp >= n and n > 0:
+            raise ConfigError("dense_prefix covering every token is not served by the B200 path")
         kb = (n + 63) // 64
         if mask is not None and (mask.k_rows != kb or mask.k_cols != kb):
             raise ShapeError(f"mask grid {mask.k_rows}x{mask.k_cols} does not cover {kb}x{kb} blocks")
-        layer = Layer(self, 1, d, TokenGrid("HW", (1, n)))
+        layer = Layer(self, 1, d, TokenGrid("HW", (1, n - dp)), dense_prefix=dp)
         try:
             layer.set_masks(None if mask is None else mask.bits.reshape(1, kb, kb))
             out, zeroed = layer.forward_host(inp.q.reshape(1, n, d), inp.k.reshape(1, n, d), inp.v.reshape(1, n, d),
@@ -566,11 +567,15 @@ class Context:
 class Layer:
     """H heads of cmd_run's per-head chain (main.cpp:276-305) on one GPU."""
 
-    def __init__(self, ctx: Context, heads: int, head_dim: int, grid, orders: Optional[Sequence[str]] = None):
+    def __init__(self, ctx: Context, heads: int, head_dim: int, grid, orders: Optional[Sequence[str]] = None,
+                 dense_prefix: int = 0):
+        """dense_prefix: leading text tokens kept in place, dense and unquantized
+        (AttnInputs::dense_prefix, PermPlan::with_prefix); N = grid tokens + prefix."""
         if isinstance(grid, str):
             grid = parse_grid(grid)
         self.ctx, self.heads, self.head_dim, self.grid = ctx, heads, head_dim, grid
-        self.N = grid.token_count()
+        self.dense_prefix = int(dense_prefix)
+        self.N = grid.token_count() + self.dense_prefix
         self.kb = (self.N + 63) // 64
         ords = None
         if orders is not None:
@@ -578,8 +583,8 @@ class Layer:
                 raise ConfigError(f"need {heads} orders, got {len(orders)}")
             ords = "".join(orders).encode()
         p = P()
-        _check(_lib.paro_layer_create(P(ctx.ptr), U32(heads), U32(head_dim), grid.text().encode(), ords,
-                                      ctypes.byref(p)))
+        _check(_lib.paro_layer_create_prefix(P(ctx.ptr), U32(heads), U32(head_dim), grid.text().encode(), ords,
+                                             U32(self.dense_prefix), ctypes.byref(p)))
         self.ptr = p.value
 
     def close(self):

@@ -1068,10 +1068,16 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
             const uint32_t nmine = side ? x.nb : x.na;
             const uint16_t* list = L.items + ((size_t)x.h * L.kb + qb) * L.kb;
-            const bool valid_row = has_qb && qb * 64 + r < L.N;
+            const bool valid_row = has_qb && qb * 64 + r < L.N && qb * 64 + r >= L.dp; // dense rows: K4
             const float sq0 = L.qsc[((size_t)x.h * L.kb2 + qb) * G];
             const float sq1 = G == 2 ? L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
             RowState st{-INFINITY, 0.f, -INFINITY};
+            if (L.dp && valid_row) { // continue from K4's dense-prefix state
+                const size_t srow = (size_t)x.h * L.kb2 * 64 + qb * 64 + r;
+                st.m64 = L.init_m[srow];
+                st.m32 = (float)(st.m64 * kLog2e);
+                st.l = L.init_l[srow];
+            }
             RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
@@ -1159,11 +1165,18 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             const Item x = load_item(L, (uint32_t)it);
             const bool has_qb = side ? x.qb != 0xffffu : true;
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
-            const bool valid_row = has_qb && qb * 64 + r < L.N;
+            const bool valid_row = has_qb && qb * 64 + r < L.N && qb * 64 + r >= L.dp; // dense rows: K4
             uint64_t acc[D / 2];
 #pragma unroll
             for (int c = 0; c < D / 2; ++c)
                 acc[c] = 0ull;
+            if (L.dp && valid_row) {
+                const float2* a0 = reinterpret_cast<const float2*>(
+                    L.init_acc + ((size_t)x.h * L.kb2 * 64 + qb * 64 + r) * D);
+#pragma unroll
+                for (int c = 0; c < D / 2; ++c)
+                    acc[c] = pk(a0[c].x, a0[c].y);
+            }
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t b = T & 1, ph = (T >> 1) & 1;
                 PROF_T(te0);
@@ -1269,14 +1282,27 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
             const uint32_t nmine = side ? x.nb : x.na;
             const uint16_t* list = L.items + ((size_t)x.h * L.kb + qb) * L.kb;
-            const bool valid_row = has_qb && qb * 64 + r < L.N;
+            const bool valid_row = has_qb && qb * 64 + r < L.N && qb * 64 + r >= L.dp; // dense rows: K4
             const float sq0 = L.qsc[((size_t)x.h * L.kb2 + qb) * G];
             const float sq1 = G == 2 ? L.qsc[((size_t)x.h * L.kb2 + qb) * G + G - 1] : 0.f;
             RowState st{-INFINITY, 0.f, -INFINITY};
+            if (L.dp && valid_row) { // continue from K4's dense-prefix state (l: half 0 carries it)
+                const size_t srow = (size_t)x.h * L.kb2 * 64 + qb * 64 + r;
+                st.m64 = L.init_m[srow];
+                st.m32 = (float)(st.m64 * kLog2e);
+                st.l = half == 0 ? L.init_l[srow] : 0.f;
+            }
             uint64_t acc[DH / 2];
 #pragma unroll
             for (int c = 0; c < DH / 2; ++c)
                 acc[c] = 0ull;
+            if (L.dp && valid_row) {
+                const float2* a0 = reinterpret_cast<const float2*>(
+                    L.init_acc + ((size_t)x.h * L.kb2 * 64 + qb * 64 + r) * D + half * DH);
+#pragma unroll
+                for (int c = 0; c < DH / 2; ++c)
+                    acc[c] = pk(a0[c].x, a0[c].y);
+            }
             // acc = gamma * acc + (pscale * vscale) * ip + u_c over this warp's O columns,
             // for step U (its P side was published before this warp's own PFULL arrive)
             auto dequant = [&](uint32_t U) {

@@ -37,6 +37,8 @@ cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uin
                             uint8_t* bits, uint32_t* row_kept_scratch, uint32_t* repaired, int* status,
                             cudaStream_t st);
 cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st);
+cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
+                      uint32_t head_begin, uint32_t head_count, cudaStream_t st);
 cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
                                     float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
@@ -188,7 +190,7 @@ PermDesc perm_desc(const Grid& g, const std::string& order) {
         stride[a] = s;
         s *= g.ext[a];
     }
-    PermDesc pd{{1, 1, 1}, {0, 0, 0}};
+    PermDesc pd{{1, 1, 1}, {0, 0, 0}, 0};
     const int off = 3 - g.ndim;
     for (int a = 0; a < g.ndim; ++a) {
         const int src = g.axis_index(order[a]);
@@ -269,6 +271,7 @@ struct paro_layer {
     bool masks_set = false;
     int last_v_bits = 0;
     int last_launches = 0;
+    const float* last_v = nullptr; // fp32 V of the last reorder_quantize (K4 reads the dense tiles)
     CUtensorMap tm_q, tm_k, tm_v;
     // e2e staging
     float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
@@ -325,6 +328,9 @@ void free_layer(paro_layer* l) {
     cudaFree(l->dout);
     cudaFree(l->dzero);
     cudaFree(l->L.order_chunk);
+    cudaFree(l->L.init_m);
+    cudaFree(l->L.init_l);
+    cudaFree(l->L.init_acc);
     for (cudaEvent_t e : l->ev)
         cudaEventDestroy(e);
     if (l->s_in)
@@ -357,6 +363,11 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
     const double eff = scale != 0.0f ? (double)scale : 1.0 / std::sqrt((double)l->L.D);
     if (head_count == ~0u)
         head_count = l->L.H;
+    if (l->L.dp) { // dense text-token prefix: dense rows done, the others' state for K3
+        if (!l->last_v)
+            fail(PARO_E_CONFIG, "dense prefix: reorder_quantize must run before attention");
+        cuda_check(paro::launch_k4(l->L, l->last_v, eff, out, zeroed, head_begin, head_count, st), "k4 launch");
+    }
     cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
                                head_begin, head_count, chunked),
                "k3_attention launch");
@@ -892,6 +903,11 @@ int paro_quantize_sym_device(paro_ctx* ctx, paro_stream_t stream, const float* i
 
 int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text, const char* orders,
                       paro_layer** out) {
+    return paro_layer_create_prefix(ctx, heads, head_dim, grid_text, orders, 0, out);
+}
+
+int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const char* grid_text,
+                             const char* orders, uint32_t dense_prefix, paro_layer** out) {
     return guarded([&] {
         if (!ctx)
             fail(PARO_E_CONFIG, "null context");
@@ -900,7 +916,7 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
         if (heads == 0 || heads > 65535)
             fail(PARO_E_CONFIG, "heads must be in [1, 65535]");
         Grid g = parse_grid_text(grid_text);
-        const size_t N = g.tokens();
+        const size_t N = g.tokens() + dense_prefix; // text tokens first (PermPlan::with_prefix)
         if (N == 0 || N > (size_t)16383 * 64)
             fail(PARO_E_CONFIG, "token count " + std::to_string(N) + " out of range");
         set_device(ctx);
@@ -912,6 +928,7 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
                 std::string ord = orders ? std::string(orders + (size_t)h * g.ndim, g.ndim)
                                          : std::string(g.labels, g.labels + g.ndim);
                 l->perm_host.push_back(perm_desc(g, ord));
+                l->perm_host.back().prefix = dense_prefix;
             }
             LayerDev& L = l->L;
             L.H = heads;
@@ -921,7 +938,14 @@ int paro_layer_create(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, const ch
             L.kb = (L.N + 63) / 64;
             L.kb2 = (L.kb + 1) & ~1u;
             L.np = L.kb2 / 2;
+            L.dp = dense_prefix;
+            L.nd = (dense_prefix + 63) / 64;
             const size_t rows = (size_t)heads * L.kb2 * 64;
+            if (dense_prefix) {
+                L.init_m = dalloc<double>(rows);
+                L.init_l = dalloc<float>(rows);
+                L.init_acc = dalloc<float>(rows * head_dim);
+            }
             L.perm = dalloc<PermDesc>(heads);
             L.q = dalloc<int8_t>(rows * head_dim);
             L.k = dalloc<int8_t>(rows * head_dim);
@@ -1004,6 +1028,7 @@ int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const f
             fail(PARO_E_CONFIG, "null Q/K/V");
         set_device(layer->ctx);
         cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, 0, layer->L.H, (cudaStream_t)stream), "k1 launch");
+        layer->last_v = v;
         layer->last_v_bits = v_bits;
     });
 }
@@ -1028,6 +1053,7 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
         cudaStream_t st = (cudaStream_t)stream;
         cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, 0, layer->L.H, st), "k1 launch");
         layer->last_v_bits = pv_bits;
+        layer->last_v = v;
         run_attention(layer, st, scale, pv_bits, out, zeroed);
         layer->last_launches = 2;
     });
@@ -1087,6 +1113,7 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
         cuda_check(cudaStreamWaitEvent(layer->s_in, ev[0], 0), "stream wait");
         cuda_check(cudaStreamWaitEvent(layer->s_out, ev[0], 0), "stream wait");
         layer->last_v_bits = pv_bits;
+        layer->last_v = layer->dv;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t h0 = c * L.hpc, hn = std::min(L.hpc, L.H - h0);
             const size_t off = (size_t)h0 * head_elems, bytes = (size_t)hn * head_elems * 4;

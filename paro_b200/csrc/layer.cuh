@@ -27,18 +27,23 @@ constexpr int kBlock = 64;
 // Permuted index i -> original token: decompose i row-major over the permuted
 // extents (pext), then recombine with the original strides of those axes.
 // Equals PermPlan::inverse[i] of make_perm (reorder.cpp:49-72). 2-D grids use
-// pext[0] = 1, ostride[0] = 0.
+// pext[0] = 1, ostride[0] = 0. `prefix` leading (text) tokens stay in place and
+// the grid tokens follow them (PermPlan::with_prefix, reorder.cpp:30-47).
 struct PermDesc {
     uint32_t pext[3];
     uint32_t ostride[3];
+    uint32_t prefix;
 };
 
 __host__ __device__ inline uint32_t perm_src(const PermDesc& pd, uint32_t i) {
+    if (i < pd.prefix)
+        return i;
+    i -= pd.prefix;
     const uint32_t c2 = i % pd.pext[2];
     const uint32_t t = i / pd.pext[2];
     const uint32_t c1 = t % pd.pext[1];
     const uint32_t c0 = t / pd.pext[1];
-    return c0 * pd.ostride[0] + c1 * pd.ostride[1] + c2 * pd.ostride[2];
+    return pd.prefix + c0 * pd.ostride[0] + c1 * pd.ostride[1] + c2 * pd.ostride[2];
 }
 
 struct LayerDev {
@@ -55,6 +60,13 @@ struct LayerDev {
     uint32_t* order_chunk; // [H*np] per-chunk LPT order, chunk c = heads [c*hpc, (c+1)*hpc)
     uint32_t hpc;          // heads per chunk of the host-buffer pipeline
     uint32_t* work_counter;
+    // dense text-token prefix (AttnInputs::dense_prefix): dp rows / tokens, nd =
+    // ceil(dp/64) dense key tiles; K4 hands K3 each non-dense row's running
+    // state after the dense tiles: m (fp64), l, acc [H][kb2*64][(D)]
+    uint32_t dp, nd;
+    double* init_m;
+    float* init_l;
+    float* init_acc;
 };
 
 __host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }

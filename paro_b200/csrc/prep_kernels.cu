@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(128) k2_qblock_lists(LayerDev L, const uint8_t
     uint16_t* out = L.items + ((size_t)h * L.kb + qb) * L.kb;
     for (uint32_t c0 = 0; c0 < L.kb; c0 += 128) {
         const uint32_t j = c0 + tid;
-        const bool keep = j < L.kb && (row ? row[j] != 0 : true);
+        // dense key tiles (K4) and q-blocks made only of dense rows never reach K3
+        const bool keep = j < L.kb && j >= L.nd && (qb + 1) * 64 > L.dp && (row ? row[j] != 0 : true);
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (lane == 0)
             s_warp[warp] = __popc(m);

@@ -254,3 +254,73 @@ def test_gpu_errors(paro, ctx):
     layer.close()
     with pytest.raises(paro.ConfigError):
         ctx.quantized_blocked_attention(paro.AttnInputs(q[0], q[0], q[0]), None, paro.QuantConfig(16))
+
+
+def prefix_inverse(oracle, g, order, dp):
+    """PermPlan::with_prefix (reorder.cpp:30-47): text tokens [0, dp) stay in
+    place, the grid's permutation follows offset by dp. Returns inverse."""
+    _, inv = oracle.make_perm(g.labels, g.extents, order)
+    return np.concatenate([np.arange(dp, dtype=np.int64), dp + inv.astype(np.int64)])
+
+
+def run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, pv_bits, seed):
+    g = paro.parse_grid(grid)
+    N = g.token_count() + dp
+    q, k, v = make_inputs(H, N, d, seed)
+    layer = paro.Layer(ctx, H, d, g, orders, dense_prefix=dp)
+    assert layer.N == N
+    layer.set_masks(masks)
+    out, zeroed = layer.forward_host(q, k, v, 0.0, pv_bits)
+    layer.close()
+    worst = 0.0
+    for h in range(H):
+        inv = prefix_inverse(oracle, g, orders[h], dp)
+        ref_p, z_p = oracle.stream_engine(q[h][inv], k[h][inv], v[h][inv], None if masks is None else masks[h],
+                                          pv_bits, qk_mode=1, dense_prefix=dp)
+        ref = np.empty_like(ref_p)
+        ref[inv] = ref_p
+        zref = np.zeros(N, bool)
+        zref[inv[z_p]] = True
+        assert np.array_equal(zeroed[h].astype(bool), zref), h
+        assert np.all(out[h][zref] == 0)
+        worst = max(worst, rel_err(out[h], ref))
+    print(f"[prefix] {grid}+{dp} H={H} d={d} pv={pv_bits}: max|dO|/max|O| = {worst:.3e}")
+    return worst
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("dp", [1, 40, 64, 100, 130])
+@pytest.mark.parametrize("pv_bits", [8, 4])
+def test_dense_prefix_layer_matches_oracle(paro, ctx, oracle, d, dp, pv_bits):
+    """AttnInputs::dense_prefix (attention.cpp:148-199): prefix rows dense over
+    every key tile, dense key tiles kept and unquantized for every row (K4),
+    the rest quantized from K4's running state (K3)."""
+    grid, H, orders = "F:3,H:7,W:11", 2, ["WHF", "HFW"]
+    kb = (231 + dp + 63) // 64
+    masks = random_masks(H, kb, 0.35, 11 + dp, empty_row=kb - 1)
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, pv_bits, 60 + dp) <= tol(d)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_dense_prefix_without_masks_and_all_empty(paro, ctx, oracle, d):
+    grid, H, orders = "H:9,W:20", 2, ["HW", "WH"]  # 180 grid tokens
+    dp = 77
+    kb = (180 + dp + 63) // 64
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, None, 8, 90) <= tol(d)
+    # every mask row empty: non-prefix rows see only the dense tiles
+    masks = np.zeros((H, kb, kb), np.uint8)
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, 8, 91) <= tol(d)
+
+
+@pytest.mark.parametrize("dp", [1, 63, 200])
+def test_single_head_api_dense_prefix(paro, ctx, oracle, dp):
+    n, d = 300, 64
+    q, k, v = randn(5, (n, d)), randn(6, (n, d)), randn(7, (n, d))
+    kb = (n + 63) // 64
+    mask = paro.BlockMask(kb, kb, 64, random_masks(1, kb, 0.5, dp)[0])
+    res = ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v, dense_prefix=dp), mask, paro.QuantConfig(8))
+    ref, z = oracle.stream_engine(q, k, v, mask.bits, 8, qk_mode=1, dense_prefix=dp)
+    assert rel_err(res.output, ref) <= EXACT_TOL
+    assert res.zeroed_rows == list(np.nonzero(z)[0])
+    with pytest.raises(paro.ConfigError):
+        ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v, dense_prefix=n), mask, paro.QuantConfig(8))
