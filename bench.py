@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["maskgen", "permsel"],
                     help="maskgen: the GPU mask producer (K5) on one c2-shaped calibration map instead of the layer")
     ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
+    ap.add_argument("--dense-prefix", type=int, default=0,
+                    help="diagnostic: text tokens in front of the grid (K4 + K3); BASELINE configs use 0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
@@ -384,7 +386,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     ctx = paro.Context(local_rank)
     g = paro.parse_grid(grid_text)
-    N = g.token_count()
+    N = g.token_count() + args.dense_prefix
     kb = (N + 63) // 64
     from paro_b200.sharding import shard_heads
 
@@ -399,7 +401,7 @@ def main():
         dist.all_reduce(t)
         total_ops = float(t.item())
 
-    layer = paro.Layer(ctx, hpr, d, g, [orders_all[h] for h in my_heads])
+    layer = paro.Layer(ctx, hpr, d, g, [orders_all[h] for h in my_heads], dense_prefix=args.dense_prefix)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     dq = torch.from_numpy(q).cuda()
@@ -511,6 +513,7 @@ def main():
         "config": {
             "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
             "kept_density": round(density_kept, 5), "pv_bits": pv_bits, "mask_family": args.mask_family,
+            **({"dense_prefix": args.dense_prefix} if args.dense_prefix else {}),
             "parallelism": f"head-shard x{world} (no data-path collective)",
             "l2": f"inputs {3 * q.nbytes * world / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
         },

@@ -9,8 +9,23 @@
 // Logits are the restated INT8-QK stage of K3 (scale * sum_g (sq*sk) * S_g in
 // fp64, reference order), so the running max m handed to K3 is exact and its
 // exact P-code path stays bit-exact. p, l and acc use fp32 (tolerance-level:
-// these tiles carry no codes). One CTA per (q-block, head), one thread per row;
-// the K-code tile and the permuted fp32 V tile are staged in shared memory.
+// these tiles carry no codes).
+//
+// Work units (one CTA of 4 warps each, warp w = rows 16w..16w+15 of a q-block):
+//   * the nd q-blocks holding dense rows, split into CB key chunks of CH tiles
+//     (the dense rows span all kb tiles: without the split the prefix CTAs are
+//     the long pole of the layer); each unit writes a partial (m, l, acc) per
+//     row, and k4_combine merges the CB partials;
+//   * every other q-block, one unit over its nd dense tiles, writing K3's
+//     initial state directly.
+// Per tile (cp.async, prefetched one tile ahead: K codes + permuted fp32 V rows):
+//   S = Q.K^T with mma.sync m16n8k32 s8 (exact int32 per 64-column group);
+//   the row max is found on fp32 approximations, and the candidates within the
+//   fp32 error bound are re-evaluated in fp64 in the reference's order, so m is
+//   exact; p = exp2(c . (S - S_argmax) + (m_tile - m) log2e) from integer
+//   differences; P.V with mma.sync m16n8k16 bf16 in a 3-term split
+//   (x = hi + lo, 16 significant bits; hi.hi + hi.lo + lo.hi). The raw V tile
+//   is split once per CTA into a transposed bf16 copy read by ldmatrix.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -28,143 +43,497 @@ __device__ __forceinline__ float ex2f(float x) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(64) k4_dense_prefix(LayerDev L, const float* __restrict__ v, double scale64,
-                                                      float* __restrict__ out, uint8_t* __restrict__ zeroed,
-                                                      uint32_t head_begin) {
+struct K4Cfg {
+    static constexpr int KS = D + 16;   // K code row stride, bytes (conflict-free B fragments)
+    static constexpr int RS = D + 4;    // raw fp32 V row stride, floats (conflict-free transpose reads)
+    static constexpr int TS = 64 + 8;   // transposed bf16 V row stride, elements (conflict-free ldmatrix)
+    static constexpr int K_BYTES = 64 * KS;
+    static constexpr int RAW_BYTES = 64 * RS * 4;
+    static constexpr int T_BYTES = D * TS * 2;
+    static constexpr int OFF_K = 0;                      // 2 buffers
+    static constexpr int OFF_RAW = 2 * K_BYTES;          // 1 buffer (prefetched while the split copy is read)
+    static constexpr int OFF_HI = OFF_RAW + RAW_BYTES;   // V^T hi
+    static constexpr int OFF_LO = OFF_HI + T_BYTES;      // V^T lo
+    static constexpr int OFF_SRC = OFF_LO + T_BYTES;     // original token of each key row of the next tile
+    static constexpr int SMEM = OFF_SRC + 64 * 4;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void mma_s8(int32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+// x = hi + lo with hi, lo bf16 (16 significant bits together); packs two
+// values (element k in the low half, k+1 in the high half)
+__device__ __forceinline__ void bf16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    uint32_t h, l;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+    const float h0 = __uint_as_float(h << 16), h1 = __uint_as_float(h & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(x1 - h1), "f"(x0 - h0));
+    hi = h;
+    lo = l;
+}
+
+// exact logit of one (row, key): scale * sum_g (sq_g*sk_g) * S_g in fp64, reference order
+template <int G>
+__device__ __forceinline__ double k4_exact(double scale64, const double (&a)[G], const int32_t (&sv)[G]) {
+    double accg = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        accg = __dadd_rn(accg, __dmul_rn(a[g], (double)sv[g]));
+    return __dmul_rn(scale64, accg);
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restrict__ v, double scale64,
+                                                float* __restrict__ out, uint8_t* __restrict__ zeroed,
+                                                uint32_t head_begin) {
+    using C = K4Cfg<D>;
     constexpr int G = D / 64;
-    constexpr int W = D / 4; // int32 words of one code row
-    const uint32_t qb = blockIdx.x, h = head_begin + blockIdx.y;
-    const uint32_t r = threadIdx.x;
-    const uint32_t i = qb * 64 + r; // permuted row
-    const uint32_t q0 = qb * 64;
-    const uint32_t ntiles = q0 < L.dp ? L.kb : L.nd; // tiles the CTA has to stage
-    __shared__ __align__(16) int32_t ks[64][W];
-    __shared__ __align__(16) float vs[64][D];
-    __shared__ float ksc[G];
-    const bool row_valid = i < L.N;
-    const bool row_dense = i < L.dp;
-    const uint32_t my_tiles = row_dense ? L.kb : L.nd;
+    constexpr int KSTEPS = D / 32; // k32 steps of Q.K^T (2 per 64-column group)
+    constexpr int NT = D / 8;      // n8 tiles of the output columns
+    extern __shared__ __align__(16) uint8_t k4_smem[];
+    const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(k4_smem);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const uint32_t h = head_begin + blockIdx.y, u = blockIdx.x;
+    const uint32_t ndense_units = L.nd * L.k4_cb;
+    uint32_t qb, t0, t1, chunk = 0;
+    if (u < ndense_units) { // q-block with dense rows, key chunk `chunk`
+        qb = u / L.k4_cb;
+        chunk = u % L.k4_cb;
+        t0 = chunk * L.k4_ch;
+        t1 = min(L.kb, t0 + L.k4_ch);
+    } else { // q-block without dense rows: its dense tiles only
+        qb = L.nd + (u - ndense_units);
+        t0 = 0;
+        t1 = L.nd;
+    }
     const PermDesc pd = L.perm[h];
     const size_t row0 = (size_t)h * L.kb2 * 64;
-    int32_t qv[W];
+    const uint32_t rows[2] = {qb * 64 + warp * 16 + gq, qb * 64 + warp * 16 + gq + 8};
+    uint32_t* src_tab = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_SRC);
+
+    uint32_t qa[KSTEPS][4]; // Q codes, A fragments (row gq / gq+8, k = 4tq.. / 16+4tq..)
     {
-        const int4* src = reinterpret_cast<const int4*>(L.q + (row0 + i) * D);
+        const uint8_t* qr0 = reinterpret_cast<const uint8_t*>(L.q) + (row0 + rows[0]) * D;
+        const uint8_t* qr1 = reinterpret_cast<const uint8_t*>(L.q) + (row0 + rows[1]) * D;
 #pragma unroll
-        for (int w = 0; w < W / 4; ++w) {
-            const int4 t = src[w];
-            qv[4 * w] = t.x;
-            qv[4 * w + 1] = t.y;
-            qv[4 * w + 2] = t.z;
-            qv[4 * w + 3] = t.w;
+        for (int s = 0; s < KSTEPS; ++s) {
+            qa[s][0] = *reinterpret_cast<const uint32_t*>(qr0 + 32 * s + 4 * tq);
+            qa[s][1] = *reinterpret_cast<const uint32_t*>(qr1 + 32 * s + 4 * tq);
+            qa[s][2] = *reinterpret_cast<const uint32_t*>(qr0 + 32 * s + 16 + 4 * tq);
+            qa[s][3] = *reinterpret_cast<const uint32_t*>(qr1 + 32 * s + 16 + 4 * tq);
         }
     }
     float sq[G];
 #pragma unroll
     for (int g = 0; g < G; ++g)
         sq[g] = L.qsc[((size_t)h * L.kb2 + qb) * G + g];
-    double m64 = -INFINITY;
-    float l = 0.f;
-    float acc[D];
+
+    double m64[2] = {-INFINITY, -INFINITY};
+    float lp[2] = {0.f, 0.f}; // this lane's share of l per row
+    float acc[NT][4];
 #pragma unroll
-    for (int c = 0; c < D; ++c)
-        acc[c] = 0.f;
-    for (uint32_t bj = 0; bj < ntiles; ++bj) {
-        __syncthreads(); // previous tile consumed
-        { // stage the K codes (row j = thread) and the permuted fp32 V rows of tile bj
-            const uint32_t j = threadIdx.x, kj = bj * 64 + j;
-            const int4* ksrc = reinterpret_cast<const int4*>(L.k + (row0 + kj) * D);
+    for (int n = 0; n < NT; ++n)
+        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+
+    // tile bj -> K codes (buffer bj & 1) and raw fp32 V rows (permuted order), async
+    auto issue = [&](uint32_t bj) {
+        const uint32_t sk = smem_base + C::OFF_K + (bj & 1) * C::K_BYTES, sr = smem_base + C::OFF_RAW;
+        const uint8_t* ksrc = reinterpret_cast<const uint8_t*>(L.k) + (row0 + (size_t)bj * 64) * D;
 #pragma unroll
-            for (int w = 0; w < W / 4; ++w)
-                reinterpret_cast<int4*>(ks[j])[w] = ksrc[w];
-            if (kj < L.N) {
-                const float4* vsrc = reinterpret_cast<const float4*>(v + ((size_t)h * L.N + perm_src(pd, kj)) * D);
-#pragma unroll
-                for (int w = 0; w < D / 4; ++w)
-                    reinterpret_cast<float4*>(vs[j])[w] = vsrc[w];
-            } else {
-#pragma unroll
-                for (int w = 0; w < D / 4; ++w)
-                    reinterpret_cast<float4*>(vs[j])[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            if (threadIdx.x < G)
-                ksc[threadIdx.x] = L.meta[((size_t)h * L.kb2 + bj) * meta_stride(D) + threadIdx.x];
+        for (int e = tid; e < 64 * D / 16; e += 128) {
+            const int j = e / (D / 16), w = e % (D / 16);
+            cp_async16(sk + j * C::KS + w * 16, ksrc + (size_t)j * D + w * 16, 16);
         }
-        __syncthreads();
-        if (!row_valid || bj >= my_tiles)
+#pragma unroll 4
+        for (int e = tid; e < 64 * D / 4; e += 128) {
+            const int j = e / (D / 4), w = e % (D / 4);
+            const uint32_t s = src_tab[j];
+            const bool ok = s != 0xffffffffu;
+            const float* src = ok ? v + ((size_t)h * L.N + s) * D + 4 * w : v;
+            cp_async16(sr + (j * C::RS + 4 * w) * 4, src, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+    };
+    auto fill_src = [&](uint32_t bj) {
+        if (tid < 64)
+            src_tab[tid] = bj * 64 + tid < L.N ? perm_src(pd, bj * 64 + tid) : 0xffffffffu;
+    };
+
+    fill_src(t0);
+    __syncthreads();
+    issue(t0);
+    for (uint32_t bj = t0; bj < t1; ++bj) {
+        cp_async_wait_all();
+        __syncthreads(); // tile bj landed; every warp is done with tile bj-1
+        { // raw V (key-major fp32) -> V^T hi / lo (column-major bf16 pairs along keys)
+            const float* raw = reinterpret_cast<const float*>(k4_smem + C::OFF_RAW);
+            uint32_t* thi = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_HI);
+            uint32_t* tlo = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_LO);
+            const uint32_t jl = lane >> 3, cl = lane & 7;
+#pragma unroll
+            for (int jb = 0; jb < 2; ++jb) {
+                const uint32_t jp = warp * 8 + jb * 4 + jl; // key pair (2jp, 2jp+1)
+#pragma unroll 4
+                for (int cb = 0; cb < D / 8; ++cb) {
+                    const uint32_t c = cb * 8 + cl;
+                    uint32_t hi, lo;
+                    bf16_split2(raw[(2 * jp) * C::RS + c], raw[(2 * jp + 1) * C::RS + c], hi, lo);
+                    thi[c * (C::TS / 2) + jp] = hi;
+                    tlo[c * (C::TS / 2) + jp] = lo;
+                }
+            }
+        }
+        if (bj + 1 < t1)
+            fill_src(bj + 1);
+        __syncthreads(); // V^T ready, raw buffer and next sources free
+        if (bj + 1 < t1)
+            issue(bj + 1);
+        bool act[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+            act[x] = rows[x] < L.N && (rows[x] < L.dp || bj < L.nd);
+        if (!__any_sync(0xffffffffu, act[0] || act[1]))
             continue;
+        const uint8_t* sk = k4_smem + C::OFF_K + (bj & 1) * C::K_BYTES;
         const uint32_t kn = min(64u, L.N - bj * 64);
-        double a[G];
+        // ---- S = Q.K^T (exact int32 per group)
+        int32_t S[G][8][4];
 #pragma unroll
         for (int g = 0; g < G; ++g)
-            a[g] = __dmul_rn((double)sq[g], (double)ksc[g]);
-        auto logit = [&](uint32_t j) -> double { // attention.cpp:162-168 with the INT8-QK dot
-            double accg = 0.0;
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                int32_t s = 0;
+            for (int n = 0; n < 8; ++n)
+                S[g][n][0] = S[g][n][1] = S[g][n][2] = S[g][n][3] = 0;
 #pragma unroll
-                for (int w = 0; w < 16; ++w)
-                    s = __dp4a(qv[g * 16 + w], ks[j][g * 16 + w], s);
-                accg = __dadd_rn(accg, __dmul_rn(a[g], (double)s));
+        for (int n = 0; n < 8; ++n) {
+            const uint8_t* kr = sk + (n * 8 + gq) * C::KS + 4 * tq;
+#pragma unroll
+            for (int s = 0; s < KSTEPS; ++s) {
+                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + 32 * s);
+                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + 32 * s + 16);
+                mma_s8(S[s / 2][n], qa[s], b0, b1);
             }
-            return __dmul_rn(scale64, accg);
-        };
-        double tmax = -INFINITY;
-        for (uint32_t j = 0; j < kn; ++j)
-            tmax = fmax(tmax, logit(j));
-        const double m_new = fmax(m64, tmax);
-        if (l > 0.f && m_new != m64) { // rescale (attention.cpp:170-178)
-            const float gam = ex2f((float)((m64 - m_new) * kLog2eD));
-            l *= gam;
-#pragma unroll
-            for (int c = 0; c < D; ++c)
-                acc[c] *= gam;
         }
-        m64 = m_new;
-        for (uint32_t j = 0; j < kn; ++j) { // p = exp(s - m), l += p, acc += p * v (:181-199)
-            const float p = ex2f((float)((logit(j) - m_new) * kLog2eD));
-            l += p;
+        // ---- exact row max of the tile: fp32 screen, fp64 on the candidates
+        double a[G];
+        float af[G];
 #pragma unroll
-            for (int c = 0; c < D; ++c)
-                acc[c] = fmaf(p, vs[j][c], acc[c]);
+        for (int g = 0; g < G; ++g) {
+            a[g] = __dmul_rn((double)sq[g], (double)L.meta[((size_t)h * L.kb2 + bj) * meta_stride(D) + g]);
+            af[g] = (float)a[g];
         }
-    }
-    if (!row_valid)
-        return;
-    if (row_dense) { // final row, stored at its original token (attention.cpp:242-251)
-        const uint32_t orig = perm_src(pd, i);
-        float* dst = out + ((size_t)h * L.N + orig) * D;
-        if (l == 0.f) {
+        double best[2] = {-INFINITY, -INFINITY};
+        int32_t bs[2][G];
+        if constexpr (G == 1) {
+            // one group: the logit is a non-negative multiple of S, so the
+            // integer argmax is the exact argmax (ties share the logit)
+            int32_t im[2] = {INT32_MIN, INT32_MIN};
 #pragma unroll
-            for (int c = 0; c < D; ++c)
-                dst[c] = 0.f;
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (n * 8 + 2 * tq + (e & 1) < kn)
+                        im[e >> 1] = max(im[e >> 1], S[0][n][e]);
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                im[x] = max(im[x], __shfl_xor_sync(0xffffffffu, im[x], 1));
+                im[x] = max(im[x], __shfl_xor_sync(0xffffffffu, im[x], 2));
+                bs[x][0] = im[x];
+                const int32_t sv[1] = {im[x]};
+                best[x] = k4_exact<G>(scale64, a, sv);
+            }
         } else {
-            const float il = 1.0f / l;
+        float mx[2] = {-INFINITY, -INFINITY}, mag[2] = {0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < D; ++c)
-                dst[c] = acc[c] * il;
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                float x = 0.f, mg = 0.f;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float tv = af[g] * (float)S[g][n][e];
+                    x += tv;
+                    mg += fabsf(tv);
+                }
+                if (key < kn) {
+                    mx[e >> 1] = fmaxf(mx[e >> 1], x);
+                    mag[e >> 1] = fmaxf(mag[e >> 1], mg);
+                }
+            }
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                mx[x] = fmaxf(mx[x], __shfl_xor_sync(0xffffffffu, mx[x], o));
+                mag[x] = fmaxf(mag[x], __shfl_xor_sync(0xffffffffu, mag[x], o));
+            }
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                bs[x][g] = 0;
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int x = e >> 1;
+                const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                float xv = 0.f;
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    xv += af[g] * (float)S[g][n][e];
+                // fp32 error <= ~3 ulp of the magnitude per element: 1e-6 * mag covers two
+                if (key < kn && xv >= mx[x] - 1e-6f * mag[x]) {
+                    int32_t sv[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        sv[g] = S[g][n][e];
+                    const double lg = k4_exact<G>(scale64, a, sv);
+                    if (lg > best[x]) {
+                        best[x] = lg;
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            bs[x][g] = sv[g];
+                    }
+                }
+            }
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best[x], o);
+                int32_t os[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    os[g] = __shfl_xor_sync(0xffffffffu, bs[x][g], o);
+                if (ob > best[x]) {
+                    best[x] = ob;
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        bs[x][g] = os[g];
+                }
+            }
         }
-        if (zeroed)
-            zeroed[(size_t)h * L.N + orig] = l == 0.f ? 1 : 0;
-    } else { // hand the running state to K3
-        const size_t s = row0 + i;
-        L.init_m[s] = m64;
-        L.init_l[s] = l;
+        // ---- running max, rescale, p
+        float base[2], cg[G];
 #pragma unroll
-        for (int c = 0; c < D; ++c)
-            L.init_acc[s * D + c] = acc[c];
+        for (int g = 0; g < G; ++g)
+            cg[g] = (float)(scale64 * a[g] * kLog2eD);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            if (!act[x]) {
+                base[x] = -INFINITY;
+                continue;
+            }
+            const double mn = fmax(m64[x], best[x]);
+            if (mn != m64[x]) { // (attention.cpp:170-178); m = -inf -> gamma 0 on zero state
+                const float gam = ex2f((float)((m64[x] - mn) * kLog2eD));
+                lp[x] *= gam;
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    acc[n][2 * x] *= gam;
+                    acc[n][2 * x + 1] *= gam;
+                }
+                m64[x] = mn;
+            }
+            base[x] = (float)((best[x] - mn) * kLog2eD);
+        }
+        float P[8][4];
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int x = e >> 1;
+                const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                float arg = base[x];
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    arg = fmaf(cg[g], (float)(S[g][n][e] - bs[x][g]), arg);
+                const float p = key < kn ? ex2f(arg) : 0.f; // base -inf (inactive row) -> 0
+                P[n][e] = p;
+                lp[x] += p;
+            }
+        // ---- acc += P.V: bf16 m16n8k16, 3-term split (hi.hi + hi.lo + lo.hi)
+        const uint32_t thi = smem_base + C::OFF_HI, tlo = smem_base + C::OFF_LO;
+        const uint32_t lrow = (lane & 7) + ((lane >> 4) << 3); // ldmatrix row: n within a pair of n-tiles
+        const uint32_t lk = ((lane >> 3) & 1) * 8;              // k half of the 16-key chunk
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            uint32_t ah[4], al[4];
+            bf16_split2(P[2 * ks][0], P[2 * ks][1], ah[0], al[0]);         // row gq,   keys 16ks+2tq..
+            bf16_split2(P[2 * ks][2], P[2 * ks][3], ah[1], al[1]);         // row gq+8
+            bf16_split2(P[2 * ks + 1][0], P[2 * ks + 1][1], ah[2], al[2]); // row gq,   keys 16ks+8+2tq..
+            bf16_split2(P[2 * ks + 1][2], P[2 * ks + 1][3], ah[3], al[3]); // row gq+8
+#pragma unroll
+            for (int n = 0; n < NT; n += 2) {
+                const uint32_t off = ((n * 8 + lrow) * C::TS + ks * 16 + lk) * 2;
+                uint32_t bh[4], bl[4];
+                ldsm_x4(thi + off, bh[0], bh[1], bh[2], bh[3]);
+                ldsm_x4(tlo + off, bl[0], bl[1], bl[2], bl[3]);
+                mma_bf16(acc[n], al, bh[0], bh[1]);
+                mma_bf16(acc[n], ah, bl[0], bl[1]);
+                mma_bf16(acc[n], ah, bh[0], bh[1]);
+                mma_bf16(acc[n + 1], al, bh[2], bh[3]);
+                mma_bf16(acc[n + 1], ah, bl[2], bl[3]);
+                mma_bf16(acc[n + 1], ah, bh[2], bh[3]);
+            }
+        }
     }
+
+    // ---- per-row results: l = quad sum; lane holds columns n*8 + 2tq, +1
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+        lp[x] += __shfl_xor_sync(0xffffffffu, lp[x], 1);
+        lp[x] += __shfl_xor_sync(0xffffffffu, lp[x], 2);
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+        const uint32_t i = rows[x];
+        if (i >= L.N)
+            continue;
+        float* dst;
+        if (u < ndense_units) { // partial of (row, chunk)
+            const size_t p = ((size_t)h * L.nd * 64 + i) * L.k4_cb + chunk;
+            if (tq == 0) {
+                L.part_m[p] = m64[x];
+                L.part_l[p] = lp[x];
+            }
+            dst = L.part_acc + p * D;
+        } else { // K3's initial state (no dense rows in this q-block)
+            const size_t sr = row0 + i;
+            if (tq == 0) {
+                L.init_m[sr] = m64[x];
+                L.init_l[sr] = lp[x];
+            }
+            dst = L.init_acc + sr * D;
+        }
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+            *reinterpret_cast<float2*>(dst + n * 8 + 2 * tq) = make_float2(acc[n][2 * x], acc[n][2 * x + 1]);
+    }
+}
+
+// final dense row (original token order, attention.cpp:242-251) or K3's initial state
+template <int D>
+__device__ __forceinline__ void k4_finish(const LayerDev& L, uint32_t h, uint32_t i, double m64, float l,
+                                          const float (&acc)[D / 2], float* __restrict__ out,
+                                          uint8_t* __restrict__ zeroed) {
+    constexpr int DH = D / 2;
+    const uint32_t hf = threadIdx.x >> 6;
+    if (i >= L.N)
+        return;
+    if (i < L.dp) {
+        const uint32_t orig = perm_src(L.perm[h], i);
+        float4* dst = reinterpret_cast<float4*>(out + ((size_t)h * L.N + orig) * D + hf * DH);
+        const float il = l == 0.f ? 0.f : 1.0f / l;
+#pragma unroll
+        for (int c = 0; c < DH / 4; ++c)
+            dst[c] = make_float4(acc[4 * c] * il, acc[4 * c + 1] * il, acc[4 * c + 2] * il, acc[4 * c + 3] * il);
+        if (zeroed && hf == 0)
+            zeroed[(size_t)h * L.N + orig] = l == 0.f ? 1 : 0;
+    } else {
+        const size_t s = (size_t)h * L.kb2 * 64 + i;
+        if (hf == 0) {
+            L.init_m[s] = m64;
+            L.init_l[s] = l;
+        }
+        float4* dst = reinterpret_cast<float4*>(L.init_acc + s * D + hf * DH);
+#pragma unroll
+        for (int c = 0; c < DH / 4; ++c)
+            dst[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+    }
+}
+
+// merge the CB key-chunk partials of the rows of the nd dense q-blocks
+template <int D>
+__global__ void __launch_bounds__(128) k4_combine(LayerDev L, float* __restrict__ out, uint8_t* __restrict__ zeroed,
+                                                  uint32_t head_begin) {
+    constexpr int DH = D / 2;
+    const uint32_t h = head_begin + blockIdx.y, qb = blockIdx.x;
+    const uint32_t r = threadIdx.x & 63, hf = threadIdx.x >> 6;
+    const uint32_t i = qb * 64 + r;
+    if (i >= L.N)
+        return;
+    const size_t p0 = ((size_t)h * L.nd * 64 + qb * 64 + r) * L.k4_cb;
+    double m64 = -INFINITY;
+    for (uint32_t c = 0; c < L.k4_cb; ++c)
+        m64 = fmax(m64, L.part_m[p0 + c]);
+    float l = 0.f;
+    float acc[DH];
+#pragma unroll
+    for (int e = 0; e < DH; ++e)
+        acc[e] = 0.f;
+    for (uint32_t c = 0; c < L.k4_cb; ++c) {
+        const float lc = L.part_l[p0 + c];
+        if (lc == 0.f)
+            continue;
+        const float gam = ex2f((float)((L.part_m[p0 + c] - m64) * kLog2eD));
+        l = fmaf(lc, gam, l);
+        const float4* src = reinterpret_cast<const float4*>(L.part_acc + (p0 + c) * D + hf * DH);
+#pragma unroll
+        for (int e = 0; e < DH / 4; ++e) {
+            const float4 a = src[e];
+            acc[4 * e] = fmaf(a.x, gam, acc[4 * e]);
+            acc[4 * e + 1] = fmaf(a.y, gam, acc[4 * e + 1]);
+            acc[4 * e + 2] = fmaf(a.z, gam, acc[4 * e + 2]);
+            acc[4 * e + 3] = fmaf(a.w, gam, acc[4 * e + 3]);
+        }
+    }
+    k4_finish<D>(L, h, i, m64, l, acc, out, zeroed);
+}
+
+// key chunks for the dense q-blocks: about 4096 dense units over all heads,
+// at least 8 tiles per chunk
+void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_t& ch) {
+    const uint64_t work = (uint64_t)kb * nd * heads;
+    ch = (uint32_t)((work + 4095) / 4096);
+    if (ch < 8)
+        ch = 8;
+    if (ch > kb)
+        ch = kb;
+    cb = (kb + ch - 1) / ch;
 }
 
 cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
                       uint32_t head_begin, uint32_t head_count, cudaStream_t st) {
     if (L.dp == 0 || head_count == 0)
         return cudaSuccess;
-    const dim3 grid(L.kb, head_count);
-    if (L.D == 64)
-        k4_dense_prefix<64><<<grid, 64, 0, st>>>(L, v, scale, out, zeroed, head_begin);
-    else
-        k4_dense_prefix<128><<<grid, 64, 0, st>>>(L, v, scale, out, zeroed, head_begin);
+    const dim3 grid(L.nd * L.k4_cb + (L.kb - L.nd), head_count);
+    const dim3 cgrid(L.nd, head_count);
+    if (L.D == 64) {
+        constexpr size_t smem = K4Cfg<64>::SMEM;
+        cudaFuncSetAttribute(k4_dense<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k4_dense<64><<<grid, 128, smem, st>>>(L, v, scale, out, zeroed, head_begin);
+        k4_combine<64><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
+    } else {
+        constexpr size_t smem = K4Cfg<128>::SMEM;
+        cudaFuncSetAttribute(k4_dense<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k4_dense<128><<<grid, 128, smem, st>>>(L, v, scale, out, zeroed, head_begin);
+        k4_combine<128><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
+    }
     return cudaGetLastError();
 }
 

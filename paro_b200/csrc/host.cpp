@@ -37,6 +37,7 @@ cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uin
                             uint8_t* bits, uint32_t* row_kept_scratch, uint32_t* repaired, int* status,
                             cudaStream_t st);
 cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st);
+void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_t& ch);
 cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
                       uint32_t head_begin, uint32_t head_count, cudaStream_t st);
 cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
@@ -331,6 +332,9 @@ void free_layer(paro_layer* l) {
     cudaFree(l->L.init_m);
     cudaFree(l->L.init_l);
     cudaFree(l->L.init_acc);
+    cudaFree(l->L.part_m);
+    cudaFree(l->L.part_l);
+    cudaFree(l->L.part_acc);
     for (cudaEvent_t e : l->ev)
         cudaEventDestroy(e);
     if (l->s_in)
@@ -945,6 +949,11 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
                 L.init_m = dalloc<double>(rows);
                 L.init_l = dalloc<float>(rows);
                 L.init_acc = dalloc<float>(rows * head_dim);
+                paro::k4_chunking(L.kb, L.nd, heads, L.k4_cb, L.k4_ch);
+                const size_t parts = (size_t)heads * L.nd * 64 * L.k4_cb;
+                L.part_m = dalloc<double>(parts);
+                L.part_l = dalloc<float>(parts);
+                L.part_acc = dalloc<float>(parts * head_dim);
             }
             L.perm = dalloc<PermDesc>(heads);
             L.q = dalloc<int8_t>(rows * head_dim);

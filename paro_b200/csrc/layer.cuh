@@ -67,6 +67,12 @@ struct LayerDev {
     double* init_m;
     float* init_l;
     float* init_acc;
+    // K4 splits the keys of the nd dense q-blocks into k4_cb chunks of k4_ch
+    // tiles; per (row, chunk) partial (m, l, acc): [H][nd*64][k4_cb](·D)
+    uint32_t k4_cb, k4_ch;
+    double* part_m;
+    float* part_l;
+    float* part_acc;
 };
 
 __host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }

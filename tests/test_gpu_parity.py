@@ -256,6 +256,12 @@ def test_gpu_errors(paro, ctx):
         ctx.quantized_blocked_attention(paro.AttnInputs(q[0], q[0], q[0]), None, paro.QuantConfig(16))
 
 
+# dense-prefix tiles are unquantized: K4 runs P.V on the tensor cores as a
+# 3-term bf16 split (16 significant bits per operand, fp32 accumulation);
+# observed <= 7e-6, bound set 10x under the north_star 1e-3.
+PREFIX_TOL = 1e-4
+
+
 def prefix_inverse(oracle, g, order, dp):
     """PermPlan::with_prefix (reorder.cpp:30-47): text tokens [0, dp) stay in
     place, the grid's permutation follows offset by dp. Returns inverse."""
@@ -298,7 +304,7 @@ def test_dense_prefix_layer_matches_oracle(paro, ctx, oracle, d, dp, pv_bits):
     grid, H, orders = "F:3,H:7,W:11", 2, ["WHF", "HFW"]
     kb = (231 + dp + 63) // 64
     masks = random_masks(H, kb, 0.35, 11 + dp, empty_row=kb - 1)
-    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, pv_bits, 60 + dp) <= tol(d)
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, pv_bits, 60 + dp) <= PREFIX_TOL
 
 
 @pytest.mark.parametrize("d", [64, 128])
@@ -306,10 +312,10 @@ def test_dense_prefix_without_masks_and_all_empty(paro, ctx, oracle, d):
     grid, H, orders = "H:9,W:20", 2, ["HW", "WH"]  # 180 grid tokens
     dp = 77
     kb = (180 + dp + 63) // 64
-    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, None, 8, 90) <= tol(d)
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, None, 8, 90) <= PREFIX_TOL
     # every mask row empty: non-prefix rows see only the dense tiles
     masks = np.zeros((H, kb, kb), np.uint8)
-    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, 8, 91) <= tol(d)
+    assert run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, dp, masks, 8, 91) <= PREFIX_TOL
 
 
 @pytest.mark.parametrize("dp", [1, 63, 200])
@@ -320,7 +326,7 @@ def test_single_head_api_dense_prefix(paro, ctx, oracle, dp):
     mask = paro.BlockMask(kb, kb, 64, random_masks(1, kb, 0.5, dp)[0])
     res = ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v, dense_prefix=dp), mask, paro.QuantConfig(8))
     ref, z = oracle.stream_engine(q, k, v, mask.bits, 8, qk_mode=1, dense_prefix=dp)
-    assert rel_err(res.output, ref) <= EXACT_TOL
+    assert rel_err(res.output, ref) <= PREFIX_TOL
     assert res.zeroed_rows == list(np.nonzero(z)[0])
     with pytest.raises(paro.ConfigError):
         ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v, dense_prefix=n), mask, paro.QuantConfig(8))
