@@ -37,6 +37,8 @@ cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uin
                             uint8_t* bits, uint32_t* row_kept_scratch, uint32_t* repaired, int* status,
                             cudaStream_t st);
 cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st);
+cudaError_t launch_block_terms(const double* sums, const float* maxs, const uint32_t* counts, uint32_t k, uint32_t n,
+                               uint32_t block, float sigma, double* terms, uint32_t* sparse, cudaStream_t st);
 void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_t& ch);
 cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
                       uint32_t head_begin, uint32_t head_count, cudaStream_t st);
@@ -259,6 +261,23 @@ struct paro_ctx {
     int device = 0;
     int num_sms = 0;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    char* pinned = nullptr; // host staging of select_permutation, grown on demand
+    size_t pinned_bytes = 0;
+    ~paro_ctx() {
+        if (pinned)
+            cudaFreeHost(pinned);
+    }
+    char* pinned_scratch(size_t bytes) {
+        if (bytes > pinned_bytes) {
+            if (pinned)
+                cudaFreeHost(pinned);
+            pinned = nullptr;
+            pinned_bytes = 0;
+            cuda_check(cudaMallocHost(reinterpret_cast<void**>(&pinned), bytes), "pinned staging");
+            pinned_bytes = bytes;
+        }
+        return pinned;
+    }
 };
 
 struct paro_layer {
@@ -727,53 +746,64 @@ int paro_select_permutation_device(paro_ctx* ctx, paro_stream_t stream, const fl
                 ords.push_back(perm);
         } while (std::next_permutation(perm.begin(), perm.end()));
         const size_t P = ords.size(), kk = (size_t)k * k;
-        // device scratch: inverse table + per-block sums / maxima / small counts
+        // every (order, map) pass is queued on the stream with one sync at the
+        // end: K5a statistics -> per-block terms + sparse count on the device,
+        // terms staged through pinned memory, summed on the host in block order
+        const size_t slots = P * count;
+        auto up8 = [](size_t x) { return (x + 7) & ~size_t(7); };
+        const size_t off_inv = 0, off_sum = up8(P * n * 4), off_max = off_sum + kk * 8, off_cnt = off_max + up8(kk * 4),
+                     off_terms = off_cnt + up8(kk * 4), off_sparse = off_terms + slots * kk * 8;
+        const size_t dbytes = off_sparse + slots * 4;
+        const size_t hbytes = P * n * 4 + slots * kk * 8 + slots * 4;
         char* scratch = nullptr;
-        const size_t bytes = n * 4 + 8 + kk * (8 + 4 + 4); // + alignment pad of the fp64 sums
-        cuda_check(cudaMalloc(&scratch, bytes), "select_permutation scratch");
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&scratch), dbytes, st), "select_permutation scratch");
         struct Free {
-            char* p;
-            ~Free() { cudaFree(p); }
-        } guard_free{scratch};
-        uint32_t* dinv = reinterpret_cast<uint32_t*>(scratch);
-        double* dsum = reinterpret_cast<double*>(scratch + n * 4 + ((8 - (n * 4) % 8) % 8));
-        float* dmax = reinterpret_cast<float*>(dsum + kk);
-        uint32_t* dcnt = reinterpret_cast<uint32_t*>(dmax + kk);
-        std::vector<uint32_t> fwd(n), inv(n);
-        std::vector<double> hs(kk);
-        std::vector<float> hm(kk);
-        std::vector<uint32_t> hc(kk);
-        std::vector<double> sparse_mean(P), quant_mean(P), nonsparse(P), quant(P);
+            char* d;
+            cudaStream_t st;
+            ~Free() { cudaFreeAsync(d, st); }
+        } guard_free{scratch, st};
+        char* host = ctx->pinned_scratch(hbytes);
+        uint32_t* hinv = reinterpret_cast<uint32_t*>(host);
+        double* hterms = reinterpret_cast<double*>(host + P * n * 4);
+        uint32_t* hsparse = reinterpret_cast<uint32_t*>(host + P * n * 4 + slots * kk * 8);
         for (size_t p = 0; p < P; ++p) {
-            PermDesc pd = perm_desc(g, ords[p]);
+            const PermDesc pd = perm_desc(g, ords[p]);
             for (size_t i = 0; i < n; ++i)
-                inv[i] = paro::perm_src(pd, (uint32_t)i);
-            cuda_check(cudaMemcpyAsync(dinv, inv.data(), n * 4, cudaMemcpyHostToDevice, st), "select_permutation");
-            double s_acc = 0.0, q_acc = 0.0;
+                hinv[p * n + i] = paro::perm_src(pd, (uint32_t)i);
+        }
+        uint32_t* dinv = reinterpret_cast<uint32_t*>(scratch + off_inv);
+        double* dsum = reinterpret_cast<double*>(scratch + off_sum);
+        float* dmax = reinterpret_cast<float*>(scratch + off_max);
+        uint32_t* dcnt = reinterpret_cast<uint32_t*>(scratch + off_cnt);
+        double* dterms = reinterpret_cast<double*>(scratch + off_terms);
+        uint32_t* dsparse = reinterpret_cast<uint32_t*>(scratch + off_sparse);
+        cuda_check(cudaMemcpyAsync(dinv, hinv, P * n * 4, cudaMemcpyHostToDevice, st), "select_permutation");
+        cuda_check(cudaMemsetAsync(dsparse, 0, slots * 4, st), "select_permutation");
+        for (size_t p = 0; p < P; ++p)
             for (uint32_t c = 0; c < count; ++c) {
+                const size_t sl = p * count + c;
                 // strip_prefix (reorder.cpp:119-127): the image-token submap
                 const float* sub = maps + (size_t)c * nf * nf + (size_t)dense_prefix * nf + dense_prefix;
-                cuda_check(paro::launch_perm_block_stats(sub, nf, (uint32_t)n, dinv, block, eps, dsum, dmax, dcnt, st),
+                cuda_check(paro::launch_perm_block_stats(sub, nf, (uint32_t)n, dinv + p * n, block, eps, dsum, dmax,
+                                                         dcnt, st),
                            "select_permutation");
-                cuda_check(cudaMemcpyAsync(hs.data(), dsum, kk * 8, cudaMemcpyDeviceToHost, st), "select_permutation");
-                cuda_check(cudaMemcpyAsync(hm.data(), dmax, kk * 4, cudaMemcpyDeviceToHost, st), "select_permutation");
-                cuda_check(cudaMemcpyAsync(hc.data(), dcnt, kk * 4, cudaMemcpyDeviceToHost, st), "select_permutation");
-                cuda_check(cudaStreamSynchronize(st), "select_permutation");
-                // m_sparse and m_quant (metrics.cpp:60-83, 114-133), block order (bi, bj)
-                size_t sparse_blocks = 0;
-                double total = 0.0;
-                for (uint32_t bi = 0; bi < k; ++bi) {
-                    const size_t r0 = (size_t)bi * block, r1 = std::min(n, r0 + block);
-                    for (uint32_t bj = 0; bj < k; ++bj) {
-                        const size_t c0 = (size_t)bj * block, c1 = std::min(n, c0 + block);
-                        const size_t cnt = (r1 - r0) * (c1 - c0), b = (size_t)bi * k + bj;
-                        if ((double)hc[b] / (double)cnt >= (double)sigma)
-                            ++sparse_blocks;
-                        const double mx = (double)hm[b];
-                        total += mx == 0.0 ? 1.0 : mx / (hs[b] / (double)cnt);
-                    }
-                }
-                s_acc += (double)sparse_blocks / (double)kk;
+                cuda_check(paro::launch_block_terms(dsum, dmax, dcnt, k, (uint32_t)n, block, sigma, dterms + sl * kk,
+                                                    dsparse + sl, st),
+                           "select_permutation");
+            }
+        cuda_check(cudaMemcpyAsync(hterms, dterms, slots * kk * 8, cudaMemcpyDeviceToHost, st), "select_permutation");
+        cuda_check(cudaMemcpyAsync(hsparse, dsparse, slots * 4, cudaMemcpyDeviceToHost, st), "select_permutation");
+        cuda_check(cudaStreamSynchronize(st), "select_permutation");
+        std::vector<double> sparse_mean(P), quant_mean(P), nonsparse(P), quant(P);
+        for (size_t p = 0; p < P; ++p) {
+            double s_acc = 0.0, q_acc = 0.0;
+            for (uint32_t c = 0; c < count; ++c) {
+                const size_t sl = p * count + c;
+                const double* t = hterms + sl * kk;
+                double total = 0.0; // block order (bi, bj), as metrics.cpp
+                for (size_t b = 0; b < kk; ++b)
+                    total += t[b];
+                s_acc += (double)hsparse[sl] / (double)kk;
                 q_acc += total / (double)kk;
             }
             const double cnt = (double)count;

@@ -447,6 +447,40 @@ cudaError_t launch_gen_mask(const double* sums, uint32_t count, uint32_t kr, uin
     return cudaGetLastError();
 }
 
+// Per-block terms of m_sparse / m_quant (metrics.cpp:60-83, 114-133) from K5a's
+// statistics: term[b] = max == 0 ? 1 : max / (sum / cnt) (the reference's fp64
+// ops, IEEE-rounded like the host) and the count of blocks whose near-zero
+// share reaches sigma (an exact integer sum). The host adds the terms in
+// block order, so the score stays bit-identical.
+__global__ void k5_block_terms(const double* __restrict__ sums, const float* __restrict__ maxs,
+                               const uint32_t* __restrict__ counts, uint32_t k, uint32_t n, uint32_t block, float sigma,
+                               double* __restrict__ terms, uint32_t* __restrict__ sparse) {
+    uint32_t local = 0;
+    const size_t kk = (size_t)k * k;
+    for (size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x; b < kk; b += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t bi = (uint32_t)(b / k), bj = (uint32_t)(b % k);
+        const uint32_t r0 = bi * block, c0 = bj * block;
+        const uint32_t rn = min(n, r0 + block) - r0, cn = min(n, c0 + block) - c0;
+        const double cnt = (double)((size_t)rn * cn);
+        if (__ddiv_rn((double)counts[b], cnt) >= (double)sigma)
+            ++local;
+        const double mx = (double)maxs[b];
+        terms[b] = mx == 0.0 ? 1.0 : __ddiv_rn(mx, __ddiv_rn(sums[b], cnt));
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local)
+        atomicAdd(sparse, local);
+}
+
+cudaError_t launch_block_terms(const double* sums, const float* maxs, const uint32_t* counts, uint32_t k, uint32_t n,
+                               uint32_t block, float sigma, double* terms, uint32_t* sparse, cudaStream_t st) {
+    const size_t kk = (size_t)k * k;
+    const int grid = (int)((kk + 255) / 256 < 2048 ? (kk + 255) / 256 : 2048);
+    k5_block_terms<<<grid > 0 ? grid : 1, 256, 0, st>>>(sums, maxs, counts, k, n, block, sigma, terms, sparse);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, double* mean, cudaStream_t st) {
     const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     k5_late_mean<<<grid > 0 ? grid : 1, 256, 0, st>>>(sums, T, total, mean);

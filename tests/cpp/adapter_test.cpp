@@ -124,6 +124,25 @@ static void gpu_tests() {
         CHECK(md / mo <= 1e-5);
         CHECK(res.zeroed_rows.empty());
     }
+    // dense text-token prefix (AttnInputs::dense_prefix): K4 + K3 through the adapter
+    for (size_t dp : {size_t(1), size_t(90), size_t(200)}) {
+        paro::AttnInputs inp{in.q, in.k, in.v, 0.0f, dp};
+        paro::QuantConfig qcfg{8, paro::QuantMode::Unsigned, paro::QuantGrouping::PerBlock, 64};
+        paro::AttnResult res = paro_b200::quantized_blocked_attention(inp, &mask, qcfg);
+        std::vector<float> ref(n * d);
+        std::vector<uint8_t> z(n);
+        oracle_stream_engine(in.q.data.data(), in.k.data.data(), in.v.data.data(), n, d, 0.0f, dp, 64,
+                             mask.bits.data(), 8, 1, ref.data(), z.data());
+        double md = 0, mo = 0;
+        for (size_t i = 0; i < n * d; ++i) {
+            md = std::max(md, (double)std::fabs(res.output.data[i] - ref[i]));
+            mo = std::max(mo, (double)std::fabs(ref[i]));
+        }
+        std::printf("quantized_blocked_attention dense_prefix=%zu: max|dO|/max|O| = %.3e\n", dp, md / mo);
+        CHECK(md / mo <= 1e-4); // dense tiles: bf16 3-term split P.V (tests/test_gpu_parity.py PREFIX_TOL)
+    }
+    paro::AttnInputs all_dense{in.q, in.k, in.v, 0.0f, n};
+    CHECK_THROWS_AS(paro_b200::quantized_blocked_attention(all_dense, &mask, paro::QuantConfig{}), paro::ConfigError);
     paro::QuantConfig bad{16, paro::QuantMode::Unsigned, paro::QuantGrouping::PerBlock, 64};
     CHECK_THROWS_AS(paro_b200::quantized_blocked_attention(in, &mask, bad), paro::ConfigError);
     paro::AttnInputs short_v{in.q, in.k, randn(n - 1, d, 3), 0.0f, 0};
