@@ -85,7 +85,7 @@ struct K3Cfg {
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
     static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
     static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
-    static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 8) : 0); // + int2 S pairs
+    static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 16) : 0); // + int4 S pairs
     // exact path: per compute warp, its risky (owner lane, group) list (<= 32 x 16 entries)
     static constexpr uint32_t OFF_BAR = OFF_XLIST + NCW * 512 * 2;
     static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
@@ -379,6 +379,20 @@ __device__ __forceinline__ double logit128(double scale64, double a0, double a1,
     return __dmul_rn(scale64, __dadd_rn(__dmul_rn(a0, (double)s0), __dmul_rn(a1, (double)s1)));
 }
 
+// x[j] for a per-lane index j < 32 without local memory: a 5-level select tree
+__device__ __forceinline__ uint32_t sel32(const uint32_t (&x)[32], uint32_t j) {
+    uint32_t a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        a[i] = (j & 16u) ? x[i + 16] : x[i];
+#pragma unroll
+    for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i)
+            a[i] = (j & (uint32_t)w) ? a[i + w] : a[i];
+    return a[0];
+}
+
 // column-tagged fp32 logit: the low 6 mantissa bits carry the column, so a max /
 // min over keys also names its column (perturbation < 64 ulp, covered by kGapSlack)
 __device__ __forceinline__ float tagf(float y, uint32_t j) {
@@ -477,6 +491,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         }
         // SPLIT: each warp of the quadrant pair scans its 32 key columns; the pair
         // then exchanges its top-2 / bottom-2 through smem (one 64-thread barrier)
+        int32_t ls0x = 0, ls1x = 0, ls0n = 0, ls1n = 0; // SPLIT: (S_0, S_1) of this half's argmax / argmin
 #pragma unroll
         for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) {
             const int h2 = SPLIT ? (int)half : hh;
@@ -498,6 +513,15 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 N2[c] = fmin3(N2[c], fmaxf(N1[c], lo), hi);
                 N1[c] = fminf(N1[c], lo);
             }
+            if (SPLIT) { // the integer S of this half's argmax / argmin, still in registers
+                const float lmx = fmaxf(fmaxf(M1[0], M1[1]), fmaxf(M1[2], M1[3]));
+                const float lmn = fminf(fminf(N1[0], N1[1]), fminf(N1[2], N1[3]));
+                const uint32_t jx = __float_as_uint(lmx) & 31u, jn = __float_as_uint(lmn) & 31u;
+                ls0x = (int32_t)sel32(x0, jx);
+                ls1x = (int32_t)sel32(x1, jx);
+                ls0n = (int32_t)sel32(x0, jn);
+                ls1n = (int32_t)sel32(x1, jn);
+            }
         }
         // merge chains pairwise (same top-2 rule)
 #pragma unroll
@@ -510,33 +534,33 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         float mA = fmaxf(M1[0], M1[1]), mB = fmax3(fminf(M1[0], M1[1]), M2[0], M2[1]);
         float nA = fminf(N1[0], N1[1]), nB = fmin3(fmaxf(N1[0], N1[1]), N2[0], N2[1]);
         PROF_T(tq0);
-        if (SPLIT) {
+        int32_t s0x, s1x, s0n, s1n;
+        if (SPLIT) { // one exchange: top-2 / bottom-2 and the S pairs of each half's extremes
+            int4* xs = reinterpret_cast<int4*>(xch + 2 * 2 * 64);
             xch[(half * 2 + side) * 64 + r] = make_float4(mA, mB, nA, nB);
+            xs[(half * 2 + side) * 64 + r] = make_int4(ls0x, ls1x, ls0n, ls1n);
             ptx::named_bar_sync(2 + r / 16, 64); // the quadrant's two warps
             const float4 o = xch[((half ^ 1) * 2 + side) * 64 + r];
-            // merge in half order so both warps get bit-identical results
+            const int4 os = xs[((half ^ 1) * 2 + side) * 64 + r];
+            // merge in half order so both warps get bit-identical results (tags
+            // name distinct columns, so the extremes never tie across halves)
             const float4 a = half ? o : make_float4(mA, mB, nA, nB), b = half ? make_float4(mA, mB, nA, nB) : o;
+            const int4 sa = half ? os : make_int4(ls0x, ls1x, ls0n, ls1n),
+                       sb = half ? make_int4(ls0x, ls1x, ls0n, ls1n) : os;
             mA = fmaxf(a.x, b.x);
             mB = fmax3(fminf(a.x, b.x), a.y, b.y);
             nA = fminf(a.z, b.z);
             nB = fmin3(fmaxf(a.z, b.z), a.w, b.w);
+            const bool xa = a.x >= b.x, na = a.z <= b.z;
+            s0x = xa ? sa.x : sb.x;
+            s1x = xa ? sa.y : sb.y;
+            s0n = na ? sa.z : sb.z;
+            s1n = na ? sa.w : sb.w;
         }
         PROF_T(tq1);
         const float slack = kErrS * (c0 + c1) * kSBound + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
         const bool unsure = !(mA - mB > slack) || !(nB - nA > slack);
-        int32_t s0x, s1x, s0n, s1n;
-        if (SPLIT) { // half 0 takes the argmax column, half 1 the argmin column, then swap
-            int32_t u0, u1;
-            dot_row128(qtile, ktile, r, __float_as_uint(half ? nA : mA) & 63u, u0, u1);
-            int2* xs = reinterpret_cast<int2*>(xch + 2 * 2 * 64);
-            xs[(half * 2 + side) * 64 + r] = make_int2(u0, u1);
-            ptx::named_bar_sync(2 + r / 16, 64);
-            const int2 o = xs[((half ^ 1) * 2 + side) * 64 + r];
-            s0x = half ? o.x : u0;
-            s1x = half ? o.y : u1;
-            s0n = half ? u0 : o.x;
-            s1n = half ? u1 : o.y;
-        } else {
+        if (!SPLIT) {
             dot2_row128(qtile, ktile, r, __float_as_uint(mA) & 63u, __float_as_uint(nA) & 63u, s0x, s1x, s0n, s1n);
         }
         double tmax64 = logit128(scale64, a64, a64b, s0x, s1x);
