@@ -82,6 +82,27 @@ int paro_serialize_mask(const uint8_t* bits, uint32_t k_rows, uint32_t k_cols, u
 int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_rows, uint32_t* k_cols,
                      uint32_t* block, uint8_t* bits);
 
+/* ---- PAT1 / PARQ interchange (golden and fixture exchange).
+ * In-memory, byte-exact with save_tensor / load_tensor (tensor_io.cpp:45-120) and
+ * save_quant_tensor / load_quant_tensor (quant.cpp:219-326); FormatError (PARO_E_FORMAT)
+ * messages carry the byte offset like the reference's. Encoders: out NULL -> *size = bytes
+ * needed; otherwise *size is the capacity on entry and the byte count on return. */
+int paro_tensor_encode(const uint32_t* shape, uint32_t ndim, const float* values, uint8_t* out, size_t* size);
+/* shape: room for 255 extents; values NULL -> header check only */
+int paro_tensor_decode(const uint8_t* data, size_t size, uint32_t* ndim, uint32_t* shape, float* values);
+typedef struct {
+    unsigned bits;
+    int mode;     /* 0 unsigned, 1 symmetric (quant.hpp:15-18) */
+    int grouping; /* 0 per block, 1 per row (quant.hpp:20-23) */
+    uint32_t block, rows, cols, groups;
+} paro_quant_header;
+/* offsets read only in unsigned mode */
+int paro_quant_encode(unsigned bits, int mode, int grouping, uint32_t block, uint32_t rows, uint32_t cols,
+                      const int32_t* codes, const float* scales, const float* offsets, uint8_t* out, size_t* size);
+/* codes / scales / offsets NULL -> header only */
+int paro_quant_decode(const uint8_t* data, size_t size, paro_quant_header* header, int32_t* codes, float* scales,
+                      float* offsets);
+
 /* gen_mask(sums, density, block, guard) -- host restatement of the offline mask
  * producer paro::gen_mask (mask.cpp:56-130), used to build bench/demo masks.
  * sums: k_rows*k_cols doubles; bits: k_rows*k_cols bytes out. */
@@ -244,6 +265,13 @@ typedef struct {
     uint32_t* forward; /* [H, N] */
 } paro_layer_buffers;
 int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out);
+
+/* One head's permuted codes of the last reorder_quantize as a PARQ blob (which: 0 Q, 1 K,
+ * 2 V), byte-identical to save_quant_tensor(quantize(apply_perm_rows(X, plan), {bits,
+ * Symmetric, PerBlock, 64})) (quant.cpp:60-104, 219-251): Q/K 8 bits, V the layer's V bits
+ * (d = 64 only: V groups span all d columns, PerBlock expresses that only at d = 64). */
+int paro_layer_export_parq(paro_layer* layer, paro_stream_t stream, uint32_t head, int which, uint8_t* out,
+                           size_t* size);
 
 /* K2 output: per head, per q-block kept-count (kept[H*k]), total kept tiles */
 int paro_layer_mask_stats(paro_layer* layer, uint32_t* kept_per_qblock, uint64_t* total_kept);

@@ -226,6 +226,55 @@ class Reference:
                                                SZ(len(fwd)), _ptr(out)))
         return out
 
+    def save_tensor_bytes(self, values, tmpdir):
+        """save_tensor (tensor_io.cpp:45-71) -> the file's bytes."""
+        v = np.ascontiguousarray(values, np.float32)
+        shape = np.asarray(v.shape, np.uint32)
+        path = os.path.join(str(tmpdir), "t.pat")
+        self._chk(self.lib.ref_save_tensor(_ptr(shape), SZ(v.ndim), _ptr(v), path.encode()))
+        with open(path, "rb") as f:
+            return f.read()
+
+    def load_tensor_error(self, data: bytes, tmpdir):
+        """load_tensor on raw bytes -> (exit code, message) (0, '' when it loads)."""
+        path = os.path.join(str(tmpdir), "l.pat")
+        with open(path, "wb") as f:
+            f.write(data)
+        nd = U32()
+        shape = np.zeros(256, np.uint32)
+        rc = self.lib.ref_load_tensor(path.encode(), ctypes.byref(nd), _ptr(shape), None)
+        return rc, (self.lib.ref_last_error().decode() if rc else "")
+
+    def save_quant_bytes(self, m, bits, mode, block, tmpdir):
+        """save_quant_tensor(quantize(m, {bits, mode, PerBlock, block})) -> the file's bytes."""
+        m = np.ascontiguousarray(m, np.float32)
+        path = os.path.join(str(tmpdir), "q.parq")
+        self._chk(self.lib.ref_save_quant_tensor(_ptr(m), SZ(m.shape[0]), SZ(m.shape[1]), ctypes.c_uint(bits),
+                                                 ctypes.c_int(mode), SZ(block), path.encode()))
+        with open(path, "rb") as f:
+            return f.read()
+
+    def save_quant_codes_bytes(self, bits, mode, grouping, block, codes, scales, offsets, tmpdir):
+        codes = np.ascontiguousarray(codes, np.int32)
+        scales = np.ascontiguousarray(scales, np.float32)
+        offsets = np.ascontiguousarray(offsets if offsets is not None and len(offsets) else np.zeros(1), np.float32)
+        path = os.path.join(str(tmpdir), "c.parq")
+        self._chk(self.lib.ref_save_quant_codes(ctypes.c_uint(bits), ctypes.c_int(mode), ctypes.c_int(grouping),
+                                                SZ(block), SZ(codes.shape[0]), SZ(codes.shape[1]), _ptr(codes),
+                                                _ptr(scales), _ptr(offsets), path.encode()))
+        with open(path, "rb") as f:
+            return f.read()
+
+    def load_quant_error(self, data: bytes, tmpdir):
+        path = os.path.join(str(tmpdir), "l.parq")
+        with open(path, "wb") as f:
+            f.write(data)
+        bits, mode = ctypes.c_uint(), ctypes.c_int()
+        rows, cols, ng = SZ(), SZ(), SZ()
+        rc = self.lib.ref_load_quant_tensor(path.encode(), ctypes.byref(bits), ctypes.byref(mode), ctypes.byref(rows),
+                                            ctypes.byref(cols), None, None, ctypes.byref(ng))
+        return rc, (self.lib.ref_last_error().decode() if rc else "")
+
     def quantize(self, m, bits, mode, grouping, block):
         m = np.ascontiguousarray(m, np.float32)
         rows, cols = m.shape

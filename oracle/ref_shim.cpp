@@ -32,6 +32,7 @@
 #include "paro/reorder.hpp"
 #include "paro/synth.hpp"
 #include "paro/tensor.hpp"
+#include "paro/tensor_io.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -131,6 +132,58 @@ int ref_quantize(const float* m, size_t rows, size_t cols, unsigned bits, int mo
         if (offsets)
             std::copy(q.offsets.begin(), q.offsets.end(), offsets);
         *ngroups = q.scales.size();
+    });
+}
+
+// PAT1 / PARQ files through the reference's own writers / readers (tensor_io.cpp, quant.cpp:219-326)
+int ref_save_tensor(const uint32_t* shape, size_t ndim, const float* values, const char* path) {
+    return guarded([&] {
+        paro::TensorData t;
+        t.shape.assign(shape, shape + ndim);
+        t.values.assign(values, values + t.element_count());
+        paro::save_tensor(t, path);
+    });
+}
+
+int ref_load_tensor(const char* path, uint32_t* ndim, uint32_t* shape, float* values) {
+    return guarded([&] {
+        paro::TensorData t = paro::load_tensor(path);
+        *ndim = (uint32_t)t.shape.size();
+        std::copy(t.shape.begin(), t.shape.end(), shape);
+        if (values)
+            std::copy(t.values.begin(), t.values.end(), values);
+    });
+}
+
+int ref_save_quant_codes(unsigned bits, int mode, int grouping, size_t block, size_t rows, size_t cols,
+                         const int32_t* codes, const float* scales, const float* offsets, const char* path) {
+    return guarded([&] {
+        paro::QuantBlockTensor q;
+        q.rows = rows;
+        q.cols = cols;
+        q.config = paro::QuantConfig{bits, static_cast<paro::QuantMode>(mode), static_cast<paro::QuantGrouping>(grouping),
+                                     block};
+        q.codes.assign(codes, codes + rows * cols);
+        q.scales.assign(scales, scales + q.group_count());
+        if (mode == 0)
+            q.offsets.assign(offsets, offsets + q.group_count());
+        paro::save_quant_tensor(q, path);
+    });
+}
+
+int ref_load_quant_tensor(const char* path, unsigned* bits, int* mode, size_t* rows, size_t* cols, int32_t* codes,
+                          float* scales, size_t* ngroups) {
+    return guarded([&] {
+        paro::QuantBlockTensor q = paro::load_quant_tensor(path);
+        *bits = q.config.bits;
+        *mode = (int)q.config.mode;
+        *rows = q.rows;
+        *cols = q.cols;
+        *ngroups = q.scales.size();
+        if (codes)
+            std::copy(q.codes.begin(), q.codes.end(), codes);
+        if (scales)
+            std::copy(q.scales.begin(), q.scales.end(), scales);
     });
 }
 

@@ -18,6 +18,8 @@ like the reference's own tests:
   gen_mask (mask.hpp:47)                          gen_mask
   quantized_blocked_attention (attention.hpp:52)  Context.quantized_blocked_attention [GPU]
   cmd_run's per-head chain, H heads (main.cpp)    Layer                     [GPU]
+  save/load_tensor PAT1 (tensor_io.hpp)          encode_tensor / decode_tensor / load_matrix
+  save/load_quant_tensor PARQ (quant.hpp:68-74)  encode_quant / decode_quant, Layer.export_parq
 
 Errors raise the reference's exception classes (error.hpp:11-40) with the same
 exit codes. There is no CPU fallback: without the built library, importing this
@@ -310,6 +312,81 @@ class QuantBlockTensor:
     codes: np.ndarray
     scales: np.ndarray
     offsets: np.ndarray
+
+
+# ----------------------------------------------------------------------------- PAT1 / PARQ interchange
+
+
+class _QuantHeader(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_uint), ("mode", ctypes.c_int), ("grouping", ctypes.c_int), ("block", U32),
+                ("rows", U32), ("cols", U32), ("groups", U32)]
+
+
+def _buf(data: bytes) -> np.ndarray:
+    return np.frombuffer(data, np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+
+
+def encode_tensor(values: np.ndarray) -> bytes:
+    """save_tensor's PAT1 bytes (tensor_io.cpp:45-71) of an fp32 array of any rank 1..255."""
+    v = np.ascontiguousarray(values, np.float32)
+    shape = np.asarray(v.shape if v.ndim else (1,), np.uint32)
+    size = SZ()
+    _check(_lib.paro_tensor_encode(P(_ptr(shape)), U32(v.ndim), P(_ptr(v)), None, ctypes.byref(size)))
+    out = np.empty(size.value, np.uint8)
+    _check(_lib.paro_tensor_encode(P(_ptr(shape)), U32(v.ndim), P(_ptr(v)), P(_ptr(out)), ctypes.byref(size)))
+    return out.tobytes()
+
+
+def decode_tensor(data: bytes) -> np.ndarray:
+    """load_tensor (tensor_io.cpp:73-120): FormatError names the byte offset."""
+    buf = _buf(data)
+    nd = U32()
+    shape = np.zeros(255, np.uint32)
+    _check(_lib.paro_tensor_decode(P(_ptr(buf)), SZ(len(data)), ctypes.byref(nd), P(_ptr(shape)), None))
+    out = np.empty(tuple(int(x) for x in shape[:nd.value]), np.float32)
+    _check(_lib.paro_tensor_decode(P(_ptr(buf)), SZ(len(data)), ctypes.byref(nd), P(_ptr(shape)), P(_ptr(out))))
+    return out
+
+
+def load_matrix(data: bytes) -> np.ndarray:
+    """load_matrix (tensor_io.cpp:130-137): a 2-D tensor of finite values."""
+    t = decode_tensor(data)
+    if t.ndim != 2:
+        raise FormatError(f"expected a 2D tensor, found ndim={t.ndim}")
+    bad = np.flatnonzero(~np.isfinite(t))
+    if bad.size:
+        raise InvariantError(f"non-finite value at flat index {int(bad[0])}")
+    return t
+
+
+def encode_quant(q: "QuantBlockTensor") -> bytes:
+    """save_quant_tensor's PARQ bytes (quant.cpp:219-251)."""
+    codes = np.ascontiguousarray(q.codes, np.int32).reshape(-1)
+    scales = np.ascontiguousarray(q.scales, np.float32)
+    offs = np.ascontiguousarray(q.offsets if q.offsets is not None and len(q.offsets) else np.zeros(1), np.float32)
+    c = q.config
+    args = (ctypes.c_uint(c.bits), ctypes.c_int(c.mode), ctypes.c_int(c.grouping), U32(c.block), U32(q.rows),
+            U32(q.cols), P(_ptr(codes)), P(_ptr(scales)), P(_ptr(offs)))
+    size = SZ()
+    _check(_lib.paro_quant_encode(*args, None, ctypes.byref(size)))
+    out = np.empty(size.value, np.uint8)
+    _check(_lib.paro_quant_encode(*args, P(_ptr(out)), ctypes.byref(size)))
+    return out.tobytes()
+
+
+def decode_quant(data: bytes) -> "QuantBlockTensor":
+    """load_quant_tensor (quant.cpp:253-326)."""
+    buf = _buf(data)
+    h = _QuantHeader()
+    _check(_lib.paro_quant_decode(P(_ptr(buf)), SZ(len(data)), ctypes.byref(h), None, None, None))
+    codes = np.empty(max(1, h.rows * h.cols), np.int32)
+    scales = np.empty(max(1, h.groups), np.float32)
+    offs = np.empty(max(1, h.groups), np.float32)
+    _check(_lib.paro_quant_decode(P(_ptr(buf)), SZ(len(data)), ctypes.byref(h), P(_ptr(codes)), P(_ptr(scales)),
+                                  P(_ptr(offs))))
+    cfg = QuantConfig(h.bits, h.mode, h.grouping, h.block)
+    return QuantBlockTensor(h.rows, h.cols, cfg, codes[:h.rows * h.cols].reshape(h.rows, h.cols),
+                            scales[:h.groups], offs[:h.groups] if h.mode == UNSIGNED else np.zeros(0, np.float32))
 
 
 @dataclass
@@ -659,6 +736,17 @@ class Layer:
             "kblocks": b.kblocks,
             "kblocks_padded": kb2,
         }
+
+    def export_parq(self, head: int, which: str, stream=None) -> bytes:
+        """PARQ blob of one head's permuted Q / K / V codes of the last reorder_quantize,
+        byte-identical to the reference's save_quant_tensor(quantize(apply_perm_rows(X)))."""
+        w = {"q": 0, "k": 1, "v": 2}[which.lower()]
+        size = SZ()
+        _check(_lib.paro_layer_export_parq(P(self.ptr), P(stream), U32(head), ctypes.c_int(w), None, ctypes.byref(size)))
+        out = np.empty(size.value, np.uint8)
+        _check(_lib.paro_layer_export_parq(P(self.ptr), P(stream), U32(head), ctypes.c_int(w), P(_ptr(out)),
+                                           ctypes.byref(size)))
+        return out.tobytes()
 
     def mask_stats(self):
         kept = np.empty((self.heads, self.kb), np.uint32)

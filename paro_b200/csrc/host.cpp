@@ -526,6 +526,216 @@ int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_r
     });
 }
 
+// ---------------------------------------------------------------- PAT1 / PARQ interchange
+// Byte-exact restatements of save_tensor / load_tensor (tensor_io.cpp:45-120,
+// layout tensor_io.hpp:13-26) and save_quant_tensor / load_quant_tensor
+// (quant.cpp:219-326, layout quant.hpp:68-72), in memory; FormatError messages
+// name the byte offset of the first violation like the reference's.
+namespace {
+void put_u32(std::vector<uint8_t>& o, uint32_t v) {
+    for (int i = 0; i < 4; ++i)
+        o.push_back((uint8_t)(v >> (8 * i)));
+}
+void put_f32(std::vector<uint8_t>& o, float f) {
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    put_u32(o, b);
+}
+float get_f32(const uint8_t* p) {
+    const uint32_t b = get_u32(p);
+    float f;
+    std::memcpy(&f, &b, 4);
+    return f;
+}
+void emit(const std::vector<uint8_t>& bytes, uint8_t* out, size_t* size) {
+    if (out) {
+        if (*size < bytes.size())
+            fail(PARO_E_SHAPE, "output buffer holds " + std::to_string(*size) + " bytes, need " +
+                                   std::to_string(bytes.size()));
+        std::memcpy(out, bytes.data(), bytes.size());
+    }
+    *size = bytes.size();
+}
+[[noreturn]] void format_at(size_t off, const std::string& why) {
+    fail(PARO_E_FORMAT, why + " (at byte offset " + std::to_string(off) + ")");
+}
+size_t quant_groups(int grouping, uint32_t block, uint32_t rows, uint32_t cols) {
+    if (grouping == 1)
+        return rows;
+    return (size_t)((rows + block - 1) / block) * ((cols + block - 1) / block);
+}
+void quant_validate(unsigned bits, uint32_t block) { // QuantConfig::validate (quant.cpp:15-19)
+    if (bits != 4 && bits != 8)
+        fail(PARO_E_CONFIG, "quantization bitwidth must be 4 or 8, got " + std::to_string(bits));
+    if (block < 1)
+        fail(PARO_E_CONFIG, "quantization block must be >= 1");
+}
+std::vector<uint8_t> parq_bytes(unsigned bits, int mode, int grouping, uint32_t block, uint32_t rows, uint32_t cols,
+                                const int32_t* codes, const float* scales, size_t ngroups, const float* offsets) {
+    std::vector<uint8_t> o;
+    const size_t count = (size_t)rows * cols;
+    o.reserve(24 + 8 * ngroups + count);
+    o.insert(o.end(), {'P', 'A', 'R', 'Q', 1, (uint8_t)bits, (uint8_t)mode, (uint8_t)grouping});
+    put_u32(o, block);
+    put_u32(o, rows);
+    put_u32(o, cols);
+    put_u32(o, (uint32_t)ngroups);
+    for (size_t g = 0; g < ngroups; ++g)
+        put_f32(o, scales[g]);
+    if (mode == 0 && offsets)
+        for (size_t g = 0; g < ngroups; ++g)
+            put_f32(o, offsets[g]);
+    if (bits == 8) {
+        for (size_t i = 0; i < count; ++i)
+            o.push_back((uint8_t)(codes[i] & 0xff));
+    } else { // two per byte, low nibble first (quant.cpp:237-243)
+        for (size_t i = 0; i < count; i += 2) {
+            const unsigned lo = (unsigned)codes[i] & 0xfu, hi = i + 1 < count ? (unsigned)codes[i + 1] & 0xfu : 0u;
+            o.push_back((uint8_t)(lo | hi << 4));
+        }
+    }
+    return o;
+}
+} // namespace
+
+int paro_tensor_encode(const uint32_t* shape, uint32_t ndim, const float* values, uint8_t* out, size_t* size) {
+    return guarded([&] {
+        if (ndim == 0 || ndim > 255)
+            fail(PARO_E_CONFIG, "tensor ndim must be in [1,255]");
+        size_t count = 1;
+        for (uint32_t a = 0; a < ndim; ++a)
+            count *= shape[a];
+        std::vector<uint8_t> o{'P', 'A', 'R', 'O', 1, 0, (uint8_t)ndim, 0};
+        for (uint32_t a = 0; a < ndim; ++a)
+            put_u32(o, shape[a]);
+        const size_t h = o.size();
+        o.resize(h + count * 4);
+        if (count)
+            std::memcpy(o.data() + h, values, count * 4); // little-endian binary32
+        emit(o, out, size);
+    });
+}
+
+int paro_tensor_decode(const uint8_t* p, size_t size, uint32_t* ndim_out, uint32_t* shape, float* values) {
+    return guarded([&] {
+        if (size < 8)
+            format_at(size, "truncated header, need 8 bytes");
+        if (std::memcmp(p, "PARO", 4) != 0)
+            format_at(0, "bad magic, expected \"PARO\"");
+        if (p[4] != 1)
+            format_at(4, "unsupported version " + std::to_string(p[4]));
+        if (p[5] != 0)
+            format_at(5, "unsupported dtype " + std::to_string(p[5]));
+        const size_t ndim = p[6];
+        if (ndim == 0)
+            format_at(6, "ndim must be >= 1");
+        if (p[7] != 0)
+            format_at(7, "reserved byte must be 0");
+        const size_t header = 8 + 4 * ndim;
+        if (size < header)
+            format_at(size, "truncated extents, need " + std::to_string(header) + " header bytes");
+        size_t count = 1;
+        for (size_t a = 0; a < ndim; ++a) {
+            const uint32_t e = get_u32(p + 8 + 4 * a);
+            if (e == 0)
+                format_at(8 + 4 * a, "zero extent");
+            if (shape)
+                shape[a] = e;
+            count *= e;
+        }
+        const size_t payload = count * 4;
+        if (size != header + payload)
+            format_at(size, "payload length mismatch, expected " + std::to_string(payload) + " bytes, found " +
+                                std::to_string(size - header));
+        *ndim_out = (uint32_t)ndim;
+        if (values)
+            std::memcpy(values, p + header, payload);
+    });
+}
+
+int paro_quant_encode(unsigned bits, int mode, int grouping, uint32_t block, uint32_t rows, uint32_t cols,
+                      const int32_t* codes, const float* scales, const float* offsets, uint8_t* out, size_t* size) {
+    return guarded([&] {
+        quant_validate(bits, block);
+        if (mode != 0 && mode != 1)
+            fail(PARO_E_CONFIG, "quantization mode must be 0 (unsigned) or 1 (symmetric)");
+        if (grouping != 0 && grouping != 1)
+            fail(PARO_E_CONFIG, "quantization grouping must be 0 (per block) or 1 (per row)");
+        const size_t ng = quant_groups(grouping, block, rows, cols);
+        emit(parq_bytes(bits, mode, grouping, block, rows, cols, codes, scales, ng, mode == 0 ? offsets : nullptr), out,
+             size);
+    });
+}
+
+int paro_quant_decode(const uint8_t* p, size_t size, paro_quant_header* hdr, int32_t* codes, float* scales,
+                      float* offsets) {
+    return guarded([&] {
+        if (size < 24)
+            format_at(size, "truncated header");
+        if (std::memcmp(p, "PARQ", 4) != 0)
+            format_at(0, "bad magic, expected \"PARQ\"");
+        if (p[4] != 1)
+            format_at(4, "unsupported version " + std::to_string(p[4]));
+        const unsigned bits = p[5];
+        if (p[6] > 1)
+            format_at(6, "bad mode byte");
+        if (p[7] > 1)
+            format_at(7, "bad grouping byte");
+        const uint32_t block = get_u32(p + 8);
+        quant_validate(bits, block);
+        const uint32_t rows = get_u32(p + 12), cols = get_u32(p + 16), ng = get_u32(p + 20);
+        const int mode = p[6], grouping = p[7];
+        if (ng != quant_groups(grouping, block, rows, cols))
+            format_at(20, "group count " + std::to_string(ng) + " does not match shape");
+        size_t off = 24;
+        auto need = [&](size_t n, const char* what) {
+            if (size < off + n)
+                format_at(off, std::string("truncated ") + what);
+        };
+        need(4ull * ng, "scales");
+        if (scales)
+            for (uint32_t g = 0; g < ng; ++g)
+                scales[g] = get_f32(p + off + 4ull * g);
+        off += 4ull * ng;
+        if (mode == 0) {
+            need(4ull * ng, "offsets");
+            if (offsets)
+                for (uint32_t g = 0; g < ng; ++g)
+                    offsets[g] = get_f32(p + off + 4ull * g);
+            off += 4ull * ng;
+        }
+        const size_t count = (size_t)rows * cols;
+        const size_t packed = bits == 8 ? count : (count + 1) / 2;
+        need(packed, "codes");
+        if (codes) {
+            for (size_t i = 0; i < count; ++i) {
+                int32_t v;
+                if (bits == 8) {
+                    v = p[off + i];
+                    if (mode == 1 && v >= 128)
+                        v -= 256;
+                } else {
+                    const unsigned byte = p[off + i / 2];
+                    v = (int32_t)((i % 2 == 0) ? (byte & 0xfu) : (byte >> 4));
+                    if (mode == 1 && v >= 8)
+                        v -= 16;
+                }
+                codes[i] = v;
+            }
+        }
+        off += packed;
+        if (off != size)
+            format_at(off, std::to_string(size - off) + " trailing bytes");
+        hdr->bits = bits;
+        hdr->mode = mode;
+        hdr->grouping = grouping;
+        hdr->block = block;
+        hdr->rows = rows;
+        hdr->cols = cols;
+        hdr->groups = ng;
+    });
+}
+
 int paro_gen_mask(const double* sums, uint32_t kr, uint32_t kc, double density, uint32_t block, uint32_t guard,
                   uint8_t* bits, uint32_t* repaired_rows) {
     return guarded([&] {
@@ -1197,6 +1407,51 @@ int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out) {
         out->tile_meta = L.meta;
         out->inverse = layer->inv;
         out->forward = layer->fwd;
+    });
+}
+
+int paro_layer_export_parq(paro_layer* layer, paro_stream_t stream, uint32_t head, int which, uint8_t* out,
+                           size_t* size) {
+    return guarded([&] {
+        check_layer(layer);
+        const LayerDev& L = layer->L;
+        if (head >= L.H)
+            fail(PARO_E_SHAPE, "head " + std::to_string(head) + " out of range (" + std::to_string(L.H) + " heads)");
+        if (which < 0 || which > 2)
+            fail(PARO_E_CONFIG, "which must be 0 (Q), 1 (K) or 2 (V)");
+        if (layer->last_v_bits == 0)
+            fail(PARO_E_CONFIG, "reorder_quantize must run before export");
+        if (which == 2 && L.D != 64)
+            fail(PARO_E_CONFIG, "V codes are grouped per key tile over all d columns; PARQ's per-block grouping "
+                                "expresses that only at d = 64");
+        set_device(layer->ctx);
+        const cudaStream_t st = (cudaStream_t)stream;
+        const size_t rows = L.N, d = L.D;
+        std::vector<int8_t> c8(rows * d);
+        const int8_t* src = (which == 0 ? L.q : which == 1 ? L.k : L.v) + (size_t)head * L.kb2 * 64 * d;
+        cuda_check(cudaMemcpyAsync(c8.data(), src, rows * d, cudaMemcpyDeviceToHost, st), "export codes");
+        std::vector<float> meta((size_t)L.kb * paro::meta_stride(L.D)), qs((size_t)L.kb * L.G);
+        cuda_check(cudaMemcpyAsync(meta.data(), L.meta + (size_t)head * L.kb2 * paro::meta_stride(L.D),
+                                   meta.size() * 4, cudaMemcpyDeviceToHost, st),
+                   "export scales");
+        cuda_check(cudaMemcpyAsync(qs.data(), L.qsc + (size_t)head * L.kb2 * L.G, qs.size() * 4,
+                                   cudaMemcpyDeviceToHost, st),
+                   "export scales");
+        cuda_check(cudaStreamSynchronize(st), "export");
+        std::vector<int32_t> codes(c8.begin(), c8.end());
+        // group order: row blocks x column blocks, row-major (quant.cpp:45-56)
+        std::vector<float> scales;
+        for (uint32_t b = 0; b < L.kb; ++b) {
+            if (which == 2)
+                scales.push_back(meta[(size_t)b * paro::meta_stride(L.D) + 2]);
+            else
+                for (uint32_t g = 0; g < L.G; ++g)
+                    scales.push_back(which == 0 ? qs[(size_t)b * L.G + g] : meta[(size_t)b * paro::meta_stride(L.D) + g]);
+        }
+        const unsigned bits = which == 2 ? (unsigned)layer->last_v_bits : 8u;
+        emit(parq_bytes(bits, 1, 0, 64, (uint32_t)rows, (uint32_t)d, codes.data(), scales.data(), scales.size(),
+                        nullptr),
+             out, size);
     });
 }
 
