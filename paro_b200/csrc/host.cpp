@@ -302,7 +302,19 @@ struct paro_layer {
 
 namespace {
 
-constexpr uint32_t kDefaultChunks = 8; // host-buffer pipeline depth (paro_layer_set_pipeline_chunks)
+// Host-buffer pipeline depth (paro_layer_set_pipeline_chunks overrides): at
+// least 8 chunks, and no chunk uploading more than ~96 MB of Q/K/V, so the
+// un-overlapped first upload and last download stay short when the layer is
+// compute-bound (c5: 40 chunks, e2e 152 -> 141 ms) while PCIe-bound layers keep
+// chunks big enough to amortise launches (c2 8, c4 8; measured sweeps).
+constexpr uint32_t kMinChunks = 8;
+constexpr size_t kChunkBytes = 96u << 20;
+uint32_t default_heads_per_chunk(uint32_t heads, size_t tokens, uint32_t d) {
+    const size_t per_head = tokens * d * 4 * 3;
+    const uint32_t by_count = (heads + kMinChunks - 1) / kMinChunks;
+    const uint32_t by_bytes = (uint32_t)std::max<size_t>(1, kChunkBytes / per_head);
+    return std::max(1u, std::min(by_count, by_bytes));
+}
 
 void set_device(const paro_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
@@ -1207,7 +1219,7 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
             L.qb_count = dalloc<uint32_t>((size_t)heads * L.kb2);
             L.order = dalloc<uint32_t>((size_t)heads * L.np);
             L.order_chunk = dalloc<uint32_t>((size_t)heads * L.np);
-            L.hpc = (heads + kDefaultChunks - 1) / kDefaultChunks;
+            L.hpc = default_heads_per_chunk(heads, N, head_dim);
             L.work_counter = dalloc<uint32_t>(1);
             l->fwd = dalloc<uint32_t>((size_t)heads * N);
             l->inv = dalloc<uint32_t>((size_t)heads * N);
