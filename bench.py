@@ -161,6 +161,16 @@ class ClockSampler:
                 "samples": len(sms)}
 
 
+def ncu_traffic(cfg, kernel):
+    """DRAM bytes per launch of `kernel` at config `cfg` from a committed ncu capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            v = json.load(f).get(cfg, {}).get(kernel)
+        return float(v) if v is not None else None
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -521,13 +531,16 @@ def main():
         "kernels_ms": {"k2_mask_lists": k2_ms, "k1_reorder_quantize": k1_ms, "k3_attention": k3_ms},
         "roofline": {
             "bound": "tensor", "kernel": "k3_attention", "achieved": k3_tops, "peak": int8_peak, "unit": "TOPS",
-            "frac": k3_tops / int8_peak, "traffic": None,
+            "frac": k3_tops / int8_peak,
+            "traffic": None if args.dense_prefix else ncu_traffic(args.config, "k3_attention"),
             "peak_source": f"2x bf16_tflops {bf16_peak} ({peak_src}, MEASURED_PEAKS.json): dense INT8 tcgen05 rate",
             "algorithmic_ops_per_launch": my_ops,
         },
         "roofline_k1": {"bound": "hbm", "kernel": "k1_reorder_quantize", "achieved": k1_gbs, "peak": hbm_peak,
-                        "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes},
-        "gpu_launches": 4 * args.steps,
+                        "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes,
+                        "traffic": ncu_traffic(args.config, "k1_reorder_quantize")},
+        # per step: K2 (3 kernels) + K1 + K3, plus K4 + combine with a dense prefix
+        "gpu_launches": (5 + (2 if args.dense_prefix else 0)) * args.steps,
         "clocks": clk,
         "e2e": e2e,
     }
