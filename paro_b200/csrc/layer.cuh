@@ -35,15 +35,16 @@ struct PermDesc {
     uint32_t prefix;
 };
 
+// Branch-free on purpose: with a branch per row, K1 no longer issues all its
+// gathered row loads back to back (d=128 K1 0.96 -> 1.66 ms measured).
 __host__ __device__ inline uint32_t perm_src(const PermDesc& pd, uint32_t i) {
-    if (i < pd.prefix)
-        return i;
-    i -= pd.prefix;
-    const uint32_t c2 = i % pd.pext[2];
-    const uint32_t t = i / pd.pext[2];
+    const uint32_t j = i - pd.prefix; // wraps for prefix rows; that result is discarded
+    const uint32_t c2 = j % pd.pext[2];
+    const uint32_t t = j / pd.pext[2];
     const uint32_t c1 = t % pd.pext[1];
     const uint32_t c0 = t / pd.pext[1];
-    return pd.prefix + c0 * pd.ostride[0] + c1 * pd.ostride[1] + c2 * pd.ostride[2];
+    const uint32_t g = pd.prefix + c0 * pd.ostride[0] + c1 * pd.ostride[1] + c2 * pd.ostride[2];
+    return i < pd.prefix ? i : g;
 }
 
 struct LayerDev {

@@ -124,22 +124,29 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(Laye
 
     __shared__ float s_amax[3][8][2];
     __shared__ int s_colsum[8][D];
+    __shared__ uint32_t s_src[64]; // original token of each row of the block (one div/mod per row, not per thread)
 
-    const PermDesc pd = L.perm[h];
     const size_t head_in = (size_t)h * L.N * D;
+    if (tid < 64) {
+        const PermDesc pd = L.perm[h];
+        const uint32_t i = b * 64 + tid;
+        // rows past N: K takes the block's first row (padding duplicates), Q/V are zero
+        s_src[tid] = i < L.N ? perm_src(pd, i) : (b * 64 < L.N ? perm_src(pd, b * 64) : 0xffffffffu);
+    }
+    __syncthreads();
     float4 xq[PASSES], xk[PASSES], xv[PASSES];
 #pragma unroll
     for (int j = 0; j < PASSES; ++j) {
-        const uint32_t i = b * 64 + r0 + RPP * j;
+        const uint32_t rr = r0 + RPP * j, i = b * 64 + rr, src = s_src[rr];
+        const size_t off = head_in + (size_t)src * D + c4 * 4;
         if (i < L.N) {
-            const size_t off = head_in + (size_t)perm_src(pd, i) * D + c4 * 4;
             xq[j] = ld_stream(q + off);
             xk[j] = ld_stream(k + off);
             xv[j] = ld_stream(v + off);
         } else {
             xq[j] = xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            xk[j] = b * 64 < L.N ? ld_stream(k + head_in + (size_t)perm_src(pd, b * 64) * D + c4 * 4)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f); // the even-count filler block stays zero
+            xk[j] = src != 0xffffffffu ? ld_stream(k + off)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f); // the even-count filler block stays zero
         }
     }
 
