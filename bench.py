@@ -171,6 +171,11 @@ def ncu_traffic(cfg, kernel):
         return None
 
 
+def _scaled(v, f):
+    """A whole-layer capture scaled to this rank's head shard (per launch, like `achieved`)."""
+    return None if v is None else v * f
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -388,13 +393,20 @@ def main():
 
     import paro_b200 as paro
 
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; PARO_BENCH_BACKEND=gloo lets several ranks share one
+    # GPU to exercise the multi-rank path on a single-GPU box (test only)
+    backend = os.environ.get("PARO_BENCH_BACKEND", "nccl")
+    dev = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    ctx = paro.Context(local_rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    ctx = paro.Context(dev)
     g = paro.parse_grid(grid_text)
     N = g.token_count() + args.dense_prefix
     kb = (N + 63) // 64
@@ -440,7 +452,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev)
     if not args.profile:
         clocks.start()
         time.sleep(0.2)
@@ -532,13 +544,13 @@ def main():
         "roofline": {
             "bound": "tensor", "kernel": "k3_attention", "achieved": k3_tops, "peak": int8_peak, "unit": "TOPS",
             "frac": k3_tops / int8_peak,
-            "traffic": None if args.dense_prefix else ncu_traffic(args.config, "k3_attention"),
+            "traffic": None if args.dense_prefix else _scaled(ncu_traffic(args.config, "k3_attention"), hpr / H),
             "peak_source": f"2x bf16_tflops {bf16_peak} ({peak_src}, MEASURED_PEAKS.json): dense INT8 tcgen05 rate",
             "algorithmic_ops_per_launch": my_ops,
         },
         "roofline_k1": {"bound": "hbm", "kernel": "k1_reorder_quantize", "achieved": k1_gbs, "peak": hbm_peak,
                         "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes,
-                        "traffic": ncu_traffic(args.config, "k1_reorder_quantize")},
+                        "traffic": _scaled(ncu_traffic(args.config, "k1_reorder_quantize"), hpr / H)},
         # per step: K2 (3 kernels) + K1 + K3, plus K4 + combine with a dense prefix
         "gpu_launches": (5 + (2 if args.dense_prefix else 0)) * args.steps,
         "clocks": clk,
