@@ -14,6 +14,8 @@
 
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace paro {
 
 // ---------------------------------------------------------------------------
@@ -203,6 +205,116 @@ __global__ void __launch_bounds__(K5S_THREADS) k5_perm_block_sums_staged(const f
                 maxs[(size_t)bi * k + bj] = tmx[q];
                 counts[(size_t)bi * k + bj] = tcnt[q];
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5a, TMA variant (block <= 64, n <= K5T_MAXN): same sums / stats and the same
+// fp64 order as the staged kernel, restructured so HBM streams while the sums
+// run: each original row arrives in shared memory by ONE 1-D bulk copy (three
+// row buffers, two rows in flight ahead of the one being reduced), and each
+// thread keeps its column block's source columns in registers (16-bit pairs)
+// instead of re-reading an inverse table per element. Measured at c2 (one
+// 1.23 GB map): 0.24 ms for the reordering candidates; the identity order is
+// 1.23 ms -- its 32 lanes (consecutive column blocks, 64 floats apart) read one
+// shared-memory bank per step. Splitting the row into padded 256-B bulk copies
+// removes that conflict but costs more than it saves (1.30 ms for every order:
+// small bulk copies are issue-bound), so the single copy stays.
+// ---------------------------------------------------------------------------
+constexpr int K5T_NBUF = 3;
+constexpr uint32_t K5T_MAXN = 18900; // 3 row buffers of (n + 8) floats within 227 KB
+
+template <bool STATS>
+__global__ void __launch_bounds__(512) k5_perm_block_sums_tma(const float* __restrict__ map, size_t ld, uint32_t n,
+                                                            const uint32_t* __restrict__ inv, uint32_t block,
+                                                            uint32_t k, float eps, double* __restrict__ sums,
+                                                            float* __restrict__ maxs,
+                                                            uint32_t* __restrict__ counts) {
+    extern __shared__ __align__(16) uint8_t k5t_smem[];
+    const uint32_t rb = ((n + 8) * 4 + 15) & ~15u; // bytes per row buffer
+    float* bufs = reinterpret_cast<float*>(k5t_smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(k5t_smem + K5T_NBUF * rb);
+    uint32_t* shift = reinterpret_cast<uint32_t*>(bars + K5T_NBUF);
+    const uint32_t sbase = ptx::smem_u32(k5t_smem), bar0 = ptx::smem_u32(bars);
+    const uint32_t bi = blockIdx.x, tid = threadIdx.x;
+    const uint32_t r0 = bi * block, r1 = min(n, r0 + block), rows = r1 - r0;
+    // this thread's column block: its permuted columns' original columns, 2 per word
+    const uint32_t bj = tid, c0 = bj * block;
+    const uint32_t len = bj < k ? min(n, c0 + block) - c0 : 0u;
+    uint32_t idx[32];
+#pragma unroll
+    for (int w = 0; w < 32; ++w) {
+        const uint32_t u = 2 * w;
+        const uint32_t a = u < len ? (inv ? __ldg(inv + c0 + u) : c0 + u) : 0u;
+        const uint32_t b = u + 1 < len ? (inv ? __ldg(inv + c0 + u + 1) : c0 + u + 1) : 0u;
+        idx[w] = a | b << 16;
+    }
+    // row r0 + j -> buffer j % NBUF (thread 0): the 16-B aligned body by one bulk
+    // copy from the row's aligned floor, the <= 3 trailing floats by plain loads
+    auto issue = [&](uint32_t j) {
+        const uint32_t orig = inv ? __ldg(inv + r0 + j) : r0 + j;
+        const float* src = map + (size_t)orig * ld;
+        const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+        const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a) / 4;
+        const uint32_t full = (sh + n) * 4, body = full & ~15u;
+        const uint32_t b = j % K5T_NBUF;
+        float* dst = bufs + (size_t)b * (rb / 4);
+        for (uint32_t c = body / 4; c < full / 4; ++c)
+            dst[c] = reinterpret_cast<const float*>(a)[c];
+        shift[b] = sh;
+        ptx::mbar_arrive_expect_tx(bar0 + 8 * b, body);
+        if (body)
+            ptx::bulk_load(sbase + b * rb, reinterpret_cast<const void*>(a), body, bar0 + 8 * b);
+    };
+    if (tid == 0) {
+        for (int b = 0; b < K5T_NBUF; ++b)
+            ptx::mbar_init(bar0 + 8 * b, 1);
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (uint32_t j = 0; j < min(rows, (uint32_t)K5T_NBUF); ++j)
+            issue(j);
+    double tot = 0.0;
+    float tmx = 0.f;
+    uint32_t tcnt = 0;
+    for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t b = j % K5T_NBUF;
+        ptx::mbar_wait(bar0 + 8 * b, (j / K5T_NBUF) & 1);
+        const float* cur = bufs + (size_t)b * (rb / 4) + shift[b];
+        if (len) {
+            double acc = 0.0; // the reference's per-row order (staged kernel), then tot += acc
+#pragma unroll
+            for (int w = 0; w < 32; ++w) {
+                if (2u * w < len) {
+                    const float v0 = cur[idx[w] & 0xffffu];
+                    acc = __dadd_rn(acc, fabs((double)v0));
+                    if (STATS) {
+                        tmx = fmaxf(tmx, fabsf(v0));
+                        tcnt += fabsf(v0) < eps ? 1u : 0u;
+                    }
+                }
+                if (2u * w + 1 < len) {
+                    const float v1 = cur[idx[w] >> 16];
+                    acc = __dadd_rn(acc, fabs((double)v1));
+                    if (STATS) {
+                        tmx = fmaxf(tmx, fabsf(v1));
+                        tcnt += fabsf(v1) < eps ? 1u : 0u;
+                    }
+                }
+            }
+            tot = __dadd_rn(tot, acc);
+        }
+        __syncthreads(); // buffer b free
+        if (tid == 0 && j + K5T_NBUF < rows)
+            issue(j + K5T_NBUF);
+    }
+    if (len) {
+        sums[(size_t)bi * k + bj] = tot;
+        if (STATS) {
+            maxs[(size_t)bi * k + bj] = tmx;
+            counts[(size_t)bi * k + bj] = tcnt;
         }
     }
 }
@@ -417,6 +529,17 @@ cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, con
     if (block > (uint32_t)K5_MAXBLOCK || k > 65535u * K5_WARPS)
         return cudaErrorInvalidValue;
     const bool stats = maxs != nullptr;
+    if (block <= 64 && n <= K5T_MAXN && k <= 512 && n < 65536) {
+        const uint32_t rb = ((n + 8) * 4 + 15) & ~15u;
+        const size_t tsmem = (size_t)K5T_NBUF * rb + K5T_NBUF * 8 + K5T_NBUF * 4;
+        auto kern = stats ? k5_perm_block_sums_tma<true> : k5_perm_block_sums_tma<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        if (e != cudaSuccess)
+            return e;
+        const uint32_t threads = (k + 31) / 32 * 32;
+        kern<<<k, threads, tsmem, st>>>(map, ld, n, inv, block, k, eps, sums, maxs, counts);
+        return cudaGetLastError();
+    }
     const size_t smem = ((size_t)2 * n + (size_t)k * block) * 4;
     if (smem <= 227 * 1024 && n <= (uint32_t)K5S_PF * K5S_THREADS && k <= (uint32_t)K5S_MAXB * K5S_THREADS) {
         auto kern = stats ? k5_perm_block_sums_staged<true> : k5_perm_block_sums_staged<false>;
