@@ -282,6 +282,9 @@ constexpr double kLog2e = 1.4426950408889634;
 // round to the same integer, else it is recomputed exactly in fp64.
 // Measured on c2/c3 (8M sampled elements each): kappa 0 leaves code flips
 // (max|dO|/max|O| 5.8e-4 INT8, 6.4e-3 INT4); 4e-7 and 8e-7 are exact.
+#ifndef PARO_RED_MBAR
+#define PARO_RED_MBAR 1
+#endif
 #ifndef PARO_KAPPA
 #define PARO_KAPPA 6e-7f
 #endif
@@ -430,8 +433,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              RowStat* rs_w, const RowStat* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
-                                             uint32_t half, float4* xch, uint16_t* xlist,
-                                             unsigned long long (&prof)[14]) {
+                                             uint32_t half, float4* xch, uint16_t* xlist, uint32_t red_bar,
+                                             uint32_t red_par, unsigned long long (&prof)[14]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -636,32 +639,11 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     }
     if ((!SPLIT || half == 0) && (lane & 15) == 0)
         *red_w = make_float2(pmin_r, pmax_r);
-    ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
-    float lo = red_r[0].x, hi = red_r[0].y;
-#pragma unroll
-    for (int q = 1; q < 4; ++q) {
-        lo = fminf(lo, red_r[2 * q].x);
-        hi = fmaxf(hi, red_r[2 * q].y);
-    }
-    float pscale = __fdiv_rn(hi - lo, p_qmax);
-    if (pscale == 0.f)
-        pscale = 1.f;
-    const float inv = __frcp_rn(pscale);
-    PROF_T(tp2);
-    PROF_ADD(2, tp2 - tp1);
     // -------- pass 2: p, row sum, codes (two perturbed variants per element)
-    const float kap = kKappa;
-    const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
-    const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
-    const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
     const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
     uint64_t sum2 = pk(0.f, 0.f);
     const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
-    uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
-#pragma unroll
-    for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) { // the warp's key-column half (SPLIT) or both
-        const int h2 = SPLIT ? (int)half : hh;
-        float pv[32];
+    auto compute_p = [&](int h2, float (&pv)[32]) { // p of the row's 32 columns of half h2, + row sum
         if (G == 1) {
             uint32_t x[32];
             ptx::tmem_ld32(s_addr + h2 * 32, x);
@@ -703,6 +685,41 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             sum2 = add2(sum2, pk(pv[2 * k], pv[2 * k + 1]));
+    };
+    // SPLIT (d=128): publish this warp's extremes and keep going -- the p values
+    // of the warp's column half need only the row's own max, so they overlap the
+    // wait for the other compute warps (an mbarrier, so arriving never blocks;
+    // c5 132.7 -> 129.0 ms). At d=64 holding 32 p values across the wait spills
+    // (96 registers) and measured slower, so it keeps bar.sync.
+    constexpr bool kOverlap = SPLIT && PARO_RED_MBAR;
+    float pv0[32];
+    if constexpr (kOverlap) {
+        __syncwarp();
+        if (lane == 0)
+            ptx::mbar_arrive(red_bar);
+        compute_p((int)half, pv0);
+        ptx::mbar_wait(red_bar, red_par);
+    } else {
+        ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
+    }
+    float lo = red_r[0].x, hi = red_r[0].y;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+        lo = fminf(lo, red_r[2 * q].x);
+        hi = fmaxf(hi, red_r[2 * q].y);
+    }
+    float pscale = __fdiv_rn(hi - lo, p_qmax);
+    if (pscale == 0.f)
+        pscale = 1.f;
+    const float inv = __frcp_rn(pscale);
+    PROF_T(tp2);
+    PROF_ADD(2, tp2 - tp1);
+    const float kap = kKappa;
+    const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
+    const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
+    const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
+    uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
+    auto quantize_store = [&](int h2, const float (&pv)[32]) {
         uint32_t whi[8];
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
@@ -732,6 +749,17 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const int chunk = h2 * 2 + c;
             *reinterpret_cast<uint4*>(prow + ((chunk ^ ((r >> 1) & 3)) << 4)) =
                 make_uint4(whi[4 * c], whi[4 * c + 1], whi[4 * c + 2], whi[4 * c + 3]);
+        }
+    };
+    if constexpr (kOverlap) {
+        quantize_store((int)half, pv0);
+    } else {
+#pragma unroll
+        for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) { // the warp's key-column half (SPLIT) or both
+            const int h2 = SPLIT ? (int)half : hh;
+            float pv[32];
+            compute_p(h2, pv);
+            quantize_store(h2, pv);
         }
     }
     if (!valid)
@@ -932,6 +960,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_init(bar(BR::OFULL + b), 1);
             ptx::mbar_init(bar(BR::OEMPTY + b), C::NCW);
         }
+        ptx::mbar_init(bar(BR::RED), C::NCW); // P-group extremes published (one arrival per compute warp)
         ptx::mbar_init(bar(BR::LFULL), 4); // !SPLIT: softmax -> epilogue row sums
         ptx::mbar_init(bar(BR::LEMPTY), 4);
         ptx::fence_barrier_init();
@@ -1128,7 +1157,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
                                 gamma, lo, pscale, 0u, nullptr,
-                                reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 2) * 512, prof);
+                                reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 2) * 512, bar(BR::RED),
+                                T & 1, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1393,7 +1423,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                       tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r,
                                       side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half,
                                       reinterpret_cast<float4*>(smem + C::OFF_XCH),
-                                      reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512, prof);
+                                      reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512,
+                                      bar(BR::RED), T & 1, prof);
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
