@@ -1006,8 +1006,9 @@ int paro_select_permutation_device(paro_ctx* ctx, paro_stream_t stream, const fl
                 const size_t sl = p * count + c;
                 // strip_prefix (reorder.cpp:119-127): the image-token submap
                 const float* sub = maps + (size_t)c * nf * nf + (size_t)dense_prefix * nf + dense_prefix;
-                cuda_check(paro::launch_perm_block_stats(sub, nf, (uint32_t)n, dinv + p * n, block, eps, dsum, dmax,
-                                                         dcnt, st),
+                // the identity order needs no table (and K5a reads its contiguous blocks vectorised)
+                const uint32_t* pinv = ords[p] == ident ? nullptr : dinv + p * n;
+                cuda_check(paro::launch_perm_block_stats(sub, nf, (uint32_t)n, pinv, block, eps, dsum, dmax, dcnt, st),
                            "select_permutation");
                 cuda_check(paro::launch_block_terms(dsum, dmax, dcnt, k, (uint32_t)n, block, sigma, dterms + sl * kk,
                                                     dsparse + sl, st),

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "ptx.cuh"
 
@@ -283,7 +284,48 @@ __global__ void __launch_bounds__(512) k5_perm_block_sums_tma(const float* __res
         const uint32_t b = j % K5T_NBUF;
         ptx::mbar_wait(bar0 + 8 * b, (j / K5T_NBUF) & 1);
         const float* cur = bufs + (size_t)b * (rb / 4) + shift[b];
-        if (len) {
+        if (len && !inv && len == 64) {
+            // identity order: the block's 64 columns are contiguous -> 16-B loads
+            // (4 values per shared-memory wavefront where scalar gathers get 1;
+            // the warp's blocks are 256 B apart, one bank group)
+            const uint32_t sh = shift[b];
+            const float4* base = reinterpret_cast<const float4*>(bufs + (size_t)b * (rb / 4)) + ((c0 + sh) >> 2);
+            double acc = 0.0;
+            auto add = [&](float v) {
+                acc = __dadd_rn(acc, fabs((double)v));
+                if (STATS) {
+                    tmx = fmaxf(tmx, fabsf(v));
+                    tcnt += fabsf(v) < eps ? 1u : 0u;
+                }
+            };
+            auto run = [&](auto off_c) { // columns c0 .. c0+63 start at word `off` of base[0]
+                constexpr int OFF = decltype(off_c)::value;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { // 16 columns per quarter
+                    float f[20];
+#pragma unroll
+                    for (int t = 0; t < 5; ++t) {
+                        if (t == 4 && OFF == 0)
+                            break;
+                        const float4 x = base[q * 4 + t];
+                        f[4 * t] = x.x;
+                        f[4 * t + 1] = x.y;
+                        f[4 * t + 2] = x.z;
+                        f[4 * t + 3] = x.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        add(f[OFF + i]);
+                }
+            };
+            switch ((c0 + sh) & 3u) {
+            case 0: run(std::integral_constant<int, 0>{}); break;
+            case 1: run(std::integral_constant<int, 1>{}); break;
+            case 2: run(std::integral_constant<int, 2>{}); break;
+            default: run(std::integral_constant<int, 3>{}); break;
+            }
+            tot = __dadd_rn(tot, acc);
+        } else if (len) {
             double acc = 0.0; // the reference's per-row order (staged kernel), then tot += acc
 #pragma unroll
             for (int w = 0; w < 32; ++w) {
