@@ -330,3 +330,19 @@ def test_single_head_api_dense_prefix(paro, ctx, oracle, dp):
     assert res.zeroed_rows == list(np.nonzero(z)[0])
     with pytest.raises(paro.ConfigError):
         ctx.quantized_blocked_attention(paro.AttnInputs(q, k, v, dense_prefix=n), mask, paro.QuantConfig(8))
+
+
+@pytest.mark.parametrize("grid,d", [("H:3,W:5", 64), ("H:8,W:8", 64), ("H:5,W:13", 128), ("H:1,W:65", 64),
+                                    ("F:1,H:9,W:14", 128), ("F:2,H:1,W:1", 64)])
+@pytest.mark.parametrize("pv_bits", [8, 4])
+def test_tiny_and_edge_shapes(paro, ctx, oracle, grid, d, pv_bits):
+    """N < 64 (one partial block: K padding only), N = 64 (one full block, the
+    unpaired q-block), N = 65 (a one-row tail block), one-token extents, N = 2."""
+    g = paro.parse_grid(grid)
+    N = g.token_count()
+    kb = (N + 63) // 64
+    orders = paro.enumerate_orders(g)[:2]
+    H = len(orders)
+    masks = np.ones((H, kb, kb), np.uint8)
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv_bits, 101 + N) <= tol(d)
+    assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, None, pv_bits, 102 + N) <= tol(d)
