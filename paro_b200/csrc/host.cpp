@@ -1370,9 +1370,10 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
             layer->ev.push_back(e);
         }
         cudaEvent_t* ev = layer->ev.data();
-        // the copy streams start after everything already queued on the caller's stream (K2)
+        // uploads start at once: the staging buffers are idle (every forward_host
+        // returns synchronised) and nothing queued on the caller's stream (K2 of
+        // set_masks) feeds them; K1/K3 of each chunk still run on that stream after it
         cuda_check(cudaEventRecord(ev[0], st), "event record");
-        cuda_check(cudaStreamWaitEvent(layer->s_in, ev[0], 0), "stream wait");
         cuda_check(cudaStreamWaitEvent(layer->s_out, ev[0], 0), "stream wait");
         layer->last_v_bits = pv_bits;
         layer->last_v = layer->dv;
