@@ -244,6 +244,35 @@ __device__ __forceinline__ void mbar_wait2(uint32_t b0, uint32_t p0, uint32_t b1
     if (!r1)
         ptx::mbar_wait(b1, p1);
 }
+// Waits of roles with slack (producer: 3-stage ring; epilogue: double-buffered
+// O) back off with __nanosleep between probes so their spinning leaves the issue
+// slots to the softmax and MMA warps on the same sub-partition.
+#ifndef PARO_LAZY_NS
+#define PARO_LAZY_NS 512
+#endif
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t b, uint32_t p) {
+    if (PARO_LAZY_NS == 0) {
+        ptx::mbar_wait(b, p);
+        return;
+    }
+    while (!ptx::mbar_try_wait(b, p))
+        __nanosleep(PARO_LAZY_NS);
+}
+// The MMA issuer has a step of slack too (S and P are double-buffered; a
+// softmax step is ~5k cycles). Measured at c2 (K3 ms): spin everywhere 4.87;
+// producer + epilogue 512 ns back-off 4.75; + MMA 500 ns 4.61 (1000: 4.61,
+// 2000: 4.65); c5 unchanged within noise. Only the softmax waits stay hot.
+#ifndef PARO_LAZY_MMA_NS
+#define PARO_LAZY_MMA_NS 500
+#endif
+__device__ __forceinline__ void mbar_wait_mma(uint32_t b, uint32_t p) {
+    if (PARO_LAZY_MMA_NS == 0) {
+        ptx::mbar_wait(b, p);
+        return;
+    }
+    while (!ptx::mbar_try_wait(b, p))
+        __nanosleep(PARO_LAZY_MMA_NS);
+}
 __device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
                                            uint32_t p2) {
     const bool r0 = ptx::mbar_try_wait(b0, p0);
@@ -1008,7 +1037,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                     ptx::tma_load_2d(qbuf(I) + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
                 for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS;
-                    ptx::mbar_wait(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
+                    mbar_wait_lazy(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
                     const bool ha = t < x.na, hb = t < x.nb;
                     ptx::mbar_arrive_expect_tx(bar(BR::KVFULL + s),
                                                (ha + hb) * (2 * C::KV_BYTES + C::META_BYTES));
@@ -1040,8 +1069,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             auto issue_pv = [&](uint32_t U, bool ha, bool hb) {
                 const uint32_t s = U % NS, b = U & 1, ph = (U >> 1) & 1;
                 PROF_T(tm0);
-                ptx::mbar_wait(bar(BR::PFULL + b), ph);
-                ptx::mbar_wait(bar(BR::OEMPTY + b), ph ^ 1);
+                mbar_wait_mma(bar(BR::PFULL + b), ph);
+                mbar_wait_mma(bar(BR::OEMPTY + b), ph ^ 1);
                 ptx::tc_fence_after();
                 PROF_T(tm1);
                 PROF_ADD(1, tm1 - tm0);
@@ -1070,8 +1099,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 for (uint32_t t = 0; t < x.n; ++t, ++T) {
                     const uint32_t s = T % NS, b = T & 1;
                     PROF_T(tm2);
-                    ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
-                    ptx::mbar_wait(bar(BR::SEMPTY + b), ((T >> 1) & 1) ^ 1);
+                    mbar_wait_mma(bar(BR::KVFULL + s), (T / NS) & 1);
+                    mbar_wait_mma(bar(BR::SEMPTY + b), ((T >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
                     PROF_T(tm3);
                     PROF_ADD(0, tm3 - tm2);
@@ -1234,7 +1263,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t b = T & 1, ph = (T >> 1) & 1;
                 PROF_T(te0);
-                mbar_wait2(bar(BR::OFULL + b), ph, bar(BR::PFULL + b), ph);
+                mbar_wait_lazy(bar(BR::OFULL + b), ph);
+                mbar_wait_lazy(bar(BR::PFULL + b), ph);
                 ptx::tc_fence_after();
                 PROF_T(te1);
                 PROF_ADD(0, te1 - te0);

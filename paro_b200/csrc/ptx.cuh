@@ -90,10 +90,10 @@ static __device__ unsigned long long g_watchdog_ns = 4000000000ull;
 
 // Wait for the phase with `parity` to complete. A pipeline bug must not hang
 // the GPU: after the watchdog time the kernel traps (a launch error, not a hang).
-// (Measured: the probe loop below -- one L1 load of the limit and a clock read
-// between probes -- beats both a tighter spin (c2 +14%, c5 +7%) and a
-// __nanosleep(32..400) back-off (+1..4%): the extra latency per probe acts as a
-// mild back-off without giving the barrier phase away.)
+// (Measured for the latency-critical waits: the probe loop below -- one L1 load
+// of the limit and a clock read between probes -- beats both a tighter spin (c2
+// +14%, c5 +7%) and a __nanosleep(32..400) back-off (+1..4%). Roles with slack
+// use a sleeping wait instead: attention_kernel.cu mbar_wait_lazy / _mma.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity))
         return;
