@@ -409,8 +409,10 @@ __global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
 }
 
 // K2c. Counting sort of work items by step count, longest first (LPT order
-// for K3's snake distribution). Ties are ordered by (h, p) via a stable
-// in-bucket rank, so the order is deterministic. Block 0 sorts all H*np items
+// for K3's snake distribution): block-wide scan of the descending histogram,
+// then atomic placement (the order of equal-count items is unspecified -- each
+// item's result is independent of when it runs, so outputs are unaffected; a
+// single-warp stable placement cost 48 us at c2). Block 0 sorts all H*np items
 // into L.order; block c >= 1 sorts the items of heads [(c-1)*hpc, c*hpc) into
 // the same span of L.order_chunk (the chunked host-buffer pipeline runs K3
 // once per chunk).
@@ -432,32 +434,53 @@ __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x)
         atomicAdd(&s_hist[key_of[i]], 1u);
     __syncthreads();
-    if (threadIdx.x == 0) { // exclusive offsets, descending key
-        uint32_t run = 0;
-        for (int key = (int)L.kb; key >= 0; --key) {
-            const uint32_t c = s_hist[key];
-            s_hist[key] = run;
-            run += c;
-        }
-    }
+    // exclusive offsets in descending key order: block-wide scan over the
+    // reversed histogram, 1024 buckets per pass
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    if (threadIdx.x == 0)
+        s_carry = 0;
     __syncthreads();
-    // stable placement by one warp walking the items in (h, p) order
-    if (threadIdx.x < 32) {
-        const uint32_t lane = threadIdx.x;
-        for (uint32_t base = 0; base < total; base += 32) {
-            const uint32_t i = base + lane;
-            const bool valid = i < total;
-            const uint32_t key = valid ? key_of[i] : 0xffffffffu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-            const uint32_t pos = valid ? s_hist[key] + rank : 0;
-            __syncwarp();
-            if (valid && lane == (uint32_t)(__ffs(peers) - 1))
-                s_hist[key] += __popc(peers);
-            __syncwarp();
-            if (valid)
-                out[pos] = ((h0 + i / L.np) << 16) | (i % L.np);
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t base = 0; base <= L.kb; base += blockDim.x) {
+        const uint32_t j = base + threadIdx.x;            // position in descending order
+        const int key = (int)L.kb - (int)j;               // bucket
+        const uint32_t c = j <= L.kb ? s_hist[key] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o)
+                incl += v;
         }
+        if (lane == 31)
+            s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = lane < blockDim.x / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= (uint32_t)o)
+                    w += v;
+            }
+            s_warp[lane] = w; // inclusive warp totals
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        const uint32_t excl = carry + (wid ? s_warp[wid - 1] : 0u) + incl - c;
+        __syncthreads(); // every thread has read s_carry / s_warp
+        if (j <= L.kb)
+            s_hist[key] = excl;
+        if (threadIdx.x == blockDim.x - 1)
+            s_carry = carry + s_warp[blockDim.x / 32 - 1];
+        __syncthreads();
+    }
+    // placement: the items of a key in any order (each item's result is
+    // independent of when it runs; only the LPT key order matters)
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+        const uint32_t pos = atomicAdd(&s_hist[key_of[i]], 1u);
+        out[pos] = ((h0 + i / L.np) << 16) | (i % L.np);
     }
 }
 
