@@ -18,14 +18,15 @@
 //     row, and k4_combine merges the CB partials;
 //   * every other q-block, one unit over its nd dense tiles, writing K3's
 //     initial state directly.
-// Per tile (cp.async, prefetched one tile ahead: K codes + permuted fp32 V rows):
+// Per tile (cp.async, prefetched one tile ahead: K codes + the split V^T tile):
 //   S = Q.K^T with mma.sync m16n8k32 s8 (exact int32 per 64-column group);
 //   the row max is found on fp32 approximations, and the candidates within the
 //   fp32 error bound are re-evaluated in fp64 in the reference's order, so m is
 //   exact; p = exp2(c . (S - S_argmax) + (m_tile - m) log2e) from integer
 //   differences; P.V with mma.sync m16n8k16 bf16 in a 3-term split
-//   (x = hi + lo, 16 significant bits; hi.hi + hi.lo + lo.hi). The raw V tile
-//   is split once per CTA into a transposed bf16 copy read by ldmatrix.
+//   (x = hi + lo, 16 significant bits; hi.hi + hi.lo + lo.hi). V is split once
+//   per layer by K4a into transposed bf16 hi / lo tiles in HBM (permuted order),
+//   which each CTA stages with cp.async and reads with ldmatrix.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -41,22 +42,6 @@ __device__ __forceinline__ float ex2f(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-
-template <int D>
-struct K4Cfg {
-    static constexpr int KS = D + 16;   // K code row stride, bytes (conflict-free B fragments)
-    static constexpr int RS = D + 4;    // raw fp32 V row stride, floats (conflict-free transpose reads)
-    static constexpr int TS = 64 + 8;   // transposed bf16 V row stride, elements (conflict-free ldmatrix)
-    static constexpr int K_BYTES = 64 * KS;
-    static constexpr int RAW_BYTES = 64 * RS * 4;
-    static constexpr int T_BYTES = D * TS * 2;
-    static constexpr int OFF_K = 0;                      // 2 buffers
-    static constexpr int OFF_RAW = 2 * K_BYTES;          // 1 buffer (prefetched while the split copy is read)
-    static constexpr int OFF_HI = OFF_RAW + RAW_BYTES;   // V^T hi
-    static constexpr int OFF_LO = OFF_HI + T_BYTES;      // V^T lo
-    static constexpr int OFF_SRC = OFF_LO + T_BYTES;     // original token of each key row of the next tile
-    static constexpr int SMEM = OFF_SRC + 64 * 4;
-};
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
@@ -95,6 +80,40 @@ __device__ __forceinline__ void bf16_split2(float x0, float x1, uint32_t& hi, ui
     lo = l;
 }
 
+template <int D>
+struct K4Cfg {
+    static constexpr int KS = D + 16;   // K code row stride, bytes (conflict-free B fragments)
+    static constexpr int TS = 64 + 8;   // transposed bf16 V row stride, elements (conflict-free ldmatrix)
+    static constexpr int K_BYTES = 64 * KS;
+    static constexpr int T_BYTES = D * TS * 2;
+    static constexpr int STAGE = K_BYTES + 2 * T_BYTES; // K codes, V^T hi, V^T lo of one tile
+    static constexpr int SMEM = 2 * STAGE;               // double-buffered
+};
+
+// K4a: the permuted V of the layer's heads as transposed bf16 hi / lo tiles
+// ([H][kb2][D][64] each, key pairs packed low-first) -- split once per layer
+// instead of once per (q-block, tile) in every K4 CTA.
+template <int D>
+__global__ void __launch_bounds__(256) k4_vsplit(LayerDev L, const float* __restrict__ v, uint32_t head_begin) {
+    __shared__ float tile[64][D + 1];
+    const uint32_t bj = blockIdx.x, h = head_begin + blockIdx.y, tid = threadIdx.x;
+    const PermDesc pd = L.perm[h];
+    for (uint32_t e = tid; e < 64 * D; e += 256) {
+        const uint32_t j = e / D, c = e % D, kj = bj * 64 + j;
+        tile[j][c] = kj < L.N ? v[((size_t)h * L.N + perm_src(pd, kj)) * D + c] : 0.f;
+    }
+    __syncthreads();
+    uint32_t* hi = reinterpret_cast<uint32_t*>(L.vsplit_hi) + ((size_t)h * L.kb2 + bj) * D * 32;
+    uint32_t* lo = reinterpret_cast<uint32_t*>(L.vsplit_lo) + ((size_t)h * L.kb2 + bj) * D * 32;
+    for (uint32_t e = tid; e < D * 32; e += 256) {
+        const uint32_t c = e / 32, jp = e % 32;
+        uint32_t wh, wl;
+        bf16_split2(tile[2 * jp][c], tile[2 * jp + 1][c], wh, wl);
+        hi[e] = wh;
+        lo[e] = wl;
+    }
+}
+
 // exact logit of one (row, key): scale * sum_g (sq_g*sk_g) * S_g in fp64, reference order
 template <int G>
 __device__ __forceinline__ double k4_exact(double scale64, const double (&a)[G], const int32_t (&sv)[G]) {
@@ -129,10 +148,8 @@ __global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restr
         t0 = 0;
         t1 = L.nd;
     }
-    const PermDesc pd = L.perm[h];
     const size_t row0 = (size_t)h * L.kb2 * 64;
     const uint32_t rows[2] = {qb * 64 + warp * 16 + gq, qb * 64 + warp * 16 + gq + 8};
-    uint32_t* src_tab = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_SRC);
 
     uint32_t qa[KSTEPS][4]; // Q codes, A fragments (row gq / gq+8, k = 4tq.. / 16+4tq..)
     {
@@ -158,57 +175,31 @@ __global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restr
     for (int n = 0; n < NT; ++n)
         acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
 
-    // tile bj -> K codes (buffer bj & 1) and raw fp32 V rows (permuted order), async
+    // tile bj -> stage bj & 1: K codes and the pre-split V^T hi / lo rows (K4a), async
     auto issue = [&](uint32_t bj) {
-        const uint32_t sk = smem_base + C::OFF_K + (bj & 1) * C::K_BYTES, sr = smem_base + C::OFF_RAW;
+        const uint32_t st = smem_base + (bj & 1) * C::STAGE;
         const uint8_t* ksrc = reinterpret_cast<const uint8_t*>(L.k) + (row0 + (size_t)bj * 64) * D;
 #pragma unroll
         for (int e = tid; e < 64 * D / 16; e += 128) {
             const int j = e / (D / 16), w = e % (D / 16);
-            cp_async16(sk + j * C::KS + w * 16, ksrc + (size_t)j * D + w * 16, 16);
+            cp_async16(st + j * C::KS + w * 16, ksrc + (size_t)j * D + w * 16, 16);
         }
+        const size_t toff = ((size_t)h * L.kb2 + bj) * D * 64; // bf16 elements
+        const uint8_t* vh = reinterpret_cast<const uint8_t*>(L.vsplit_hi) + toff * 2;
+        const uint8_t* vl = reinterpret_cast<const uint8_t*>(L.vsplit_lo) + toff * 2;
 #pragma unroll 4
-        for (int e = tid; e < 64 * D / 4; e += 128) {
-            const int j = e / (D / 4), w = e % (D / 4);
-            const uint32_t s = src_tab[j];
-            const bool ok = s != 0xffffffffu;
-            const float* src = ok ? v + ((size_t)h * L.N + s) * D + 4 * w : v;
-            cp_async16(sr + (j * C::RS + 4 * w) * 4, src, ok ? 16u : 0u);
+        for (int e = tid; e < D * 8; e += 128) { // D rows of 64 bf16 = 8 x 16 B
+            const int c = e / 8, w = e % 8;
+            cp_async16(st + C::K_BYTES + c * C::TS * 2 + w * 16, vh + (size_t)c * 128 + w * 16, 16);
+            cp_async16(st + C::K_BYTES + C::T_BYTES + c * C::TS * 2 + w * 16, vl + (size_t)c * 128 + w * 16, 16);
         }
         cp_async_commit();
     };
-    auto fill_src = [&](uint32_t bj) {
-        if (tid < 64)
-            src_tab[tid] = bj * 64 + tid < L.N ? perm_src(pd, bj * 64 + tid) : 0xffffffffu;
-    };
 
-    fill_src(t0);
-    __syncthreads();
     issue(t0);
     for (uint32_t bj = t0; bj < t1; ++bj) {
         cp_async_wait_all();
-        __syncthreads(); // tile bj landed; every warp is done with tile bj-1
-        { // raw V (key-major fp32) -> V^T hi / lo (column-major bf16 pairs along keys)
-            const float* raw = reinterpret_cast<const float*>(k4_smem + C::OFF_RAW);
-            uint32_t* thi = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_HI);
-            uint32_t* tlo = reinterpret_cast<uint32_t*>(k4_smem + C::OFF_LO);
-            const uint32_t jl = lane >> 3, cl = lane & 7;
-#pragma unroll
-            for (int jb = 0; jb < 2; ++jb) {
-                const uint32_t jp = warp * 8 + jb * 4 + jl; // key pair (2jp, 2jp+1)
-#pragma unroll 4
-                for (int cb = 0; cb < D / 8; ++cb) {
-                    const uint32_t c = cb * 8 + cl;
-                    uint32_t hi, lo;
-                    bf16_split2(raw[(2 * jp) * C::RS + c], raw[(2 * jp + 1) * C::RS + c], hi, lo);
-                    thi[c * (C::TS / 2) + jp] = hi;
-                    tlo[c * (C::TS / 2) + jp] = lo;
-                }
-            }
-        }
-        if (bj + 1 < t1)
-            fill_src(bj + 1);
-        __syncthreads(); // V^T ready, raw buffer and next sources free
+        __syncthreads(); // tile bj landed; every warp is done with tile bj-1 (its stage is reissued next)
         if (bj + 1 < t1)
             issue(bj + 1);
         bool act[2];
@@ -217,7 +208,7 @@ __global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restr
             act[x] = rows[x] < L.N && (rows[x] < L.dp || bj < L.nd);
         if (!__any_sync(0xffffffffu, act[0] || act[1]))
             continue;
-        const uint8_t* sk = k4_smem + C::OFF_K + (bj & 1) * C::K_BYTES;
+        const uint8_t* sk = k4_smem + (bj & 1) * C::STAGE;
         const uint32_t kn = min(64u, L.N - bj * 64);
         // ---- S = Q.K^T (exact int32 per group)
         int32_t S[G][8][4];
@@ -377,7 +368,7 @@ __global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restr
                 lp[x] += p;
             }
         // ---- acc += P.V: bf16 m16n8k16, 3-term split (hi.hi + hi.lo + lo.hi)
-        const uint32_t thi = smem_base + C::OFF_HI, tlo = smem_base + C::OFF_LO;
+        const uint32_t thi = smem_base + (bj & 1) * C::STAGE + C::K_BYTES, tlo = thi + C::T_BYTES;
         const uint32_t lrow = (lane & 7) + ((lane >> 4) << 3); // ldmatrix row: n within a pair of n-tiles
         const uint32_t lk = ((lane >> 3) & 1) * 8;              // k half of the 16-key chunk
 #pragma unroll
@@ -523,6 +514,11 @@ cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* ou
         return cudaSuccess;
     const dim3 grid(L.nd * L.k4_cb + (L.kb - L.nd), head_count);
     const dim3 cgrid(L.nd, head_count);
+    const dim3 vgrid(L.kb, head_count);
+    if (L.D == 64)
+        k4_vsplit<64><<<vgrid, 256, 0, st>>>(L, v, head_begin);
+    else
+        k4_vsplit<128><<<vgrid, 256, 0, st>>>(L, v, head_begin);
     if (L.D == 64) {
         constexpr size_t smem = K4Cfg<64>::SMEM;
         cudaFuncSetAttribute(k4_dense<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -366,6 +366,8 @@ void free_layer(paro_layer* l) {
     cudaFree(l->L.part_m);
     cudaFree(l->L.part_l);
     cudaFree(l->L.part_acc);
+    cudaFree(l->L.vsplit_hi);
+    cudaFree(l->L.vsplit_lo);
     for (cudaEvent_t e : l->ev)
         cudaEventDestroy(e);
     if (l->s_in)
@@ -1207,6 +1209,8 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
                 L.part_m = dalloc<double>(parts);
                 L.part_l = dalloc<float>(parts);
                 L.part_acc = dalloc<float>(parts * head_dim);
+                L.vsplit_hi = dalloc<uint16_t>(rows * head_dim);
+                L.vsplit_lo = dalloc<uint16_t>(rows * head_dim);
             }
             L.perm = dalloc<PermDesc>(heads);
             L.q = dalloc<int8_t>(rows * head_dim);

@@ -74,6 +74,9 @@ struct LayerDev {
     double* part_m;
     float* part_l;
     float* part_acc;
+    // K4a: permuted V as transposed bf16 hi / lo tiles [H][kb2][D][64] (bf16 bits)
+    uint16_t* vsplit_hi;
+    uint16_t* vsplit_lo;
 };
 
 __host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }
