@@ -551,8 +551,8 @@ def main():
         "roofline_k1": {"bound": "hbm", "kernel": "k1_reorder_quantize", "achieved": k1_gbs, "peak": hbm_peak,
                         "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes,
                         "traffic": _scaled(ncu_traffic(args.config, "k1_reorder_quantize"), hpr / H)},
-        # per step: K2 (3 kernels) + K1 + K3, plus K4 + combine with a dense prefix
-        "gpu_launches": (5 + (2 if args.dense_prefix else 0)) * args.steps,
+        # per step: K2 (3 kernels) + K1 + K3, plus K4a + K4 + combine with a dense prefix
+        "gpu_launches": (5 + (3 if args.dense_prefix else 0)) * args.steps,
         "clocks": clk,
         "e2e": e2e,
     }
