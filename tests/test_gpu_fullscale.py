@@ -13,7 +13,7 @@ from conftest import rel_err
 pytestmark = pytest.mark.gpu
 
 OUT_TOL = 1e-3
-EXACT_TOL = 1e-5  # d=64: bit-exact P codes (see test_gpu_parity.py)
+EXACT_TOL = 1e-5  # bit-exact P codes (see test_gpu_parity.py)
 
 FULL = [
     # grid, heads (run), d, density, pv_bits, q-blocks sampled per head
@@ -65,4 +65,4 @@ def test_full_size_sampled_rows(paro, ctx, oracle, grid, H, d, density, pv_bits,
         ref = np.concatenate([r[2] for r in res if r[0] == h])
         err = rel_err(got, ref)
         print(f"{grid} d={d} pv={pv_bits} head {h}: max|dO|/max|O| = {err:.3e}")
-        assert err <= (EXACT_TOL if d == 64 else OUT_TOL), err
+        assert err <= EXACT_TOL, err  # bit-exact P codes at d=64 and d=128

@@ -19,7 +19,9 @@ EXACT_TOL = 1e-5
 
 
 def tol(d):
-    return EXACT_TOL if d == 64 else OUT_TOL
+    # d=128 P codes are bit-exact too (exact row extremes via the tagged
+    # argmax + fp64 rescan); OUT_TOL stays the north_star bar
+    return EXACT_TOL
 
 # (grid, heads, d, orders) -- c1 from BASELINE.configs[0] plus ragged / 2-D / d=128 shapes
 CASES = [
