@@ -348,3 +348,13 @@ def test_tiny_and_edge_shapes(paro, ctx, oracle, grid, d, pv_bits):
     masks = np.ones((H, kb, kb), np.uint8)
     assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv_bits, 101 + N) <= tol(d)
     assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, None, pv_bits, 102 + N) <= tol(d)
+
+
+@pytest.mark.parametrize("d,scale", [(64, 0.5), (64, 0.01), (128, 0.3), (128, 2.0)])
+def test_explicit_scale(paro, ctx, oracle, d, scale):
+    """AttnInputs::scale != 0 (attention.cpp:26-28): sharp (2.0) and flat (0.01)
+    softmax regimes exercise the exact row extremes and the P-group range."""
+    grid, H, orders = "F:3,H:7,W:11", 2, ["WHF", "HFW"]
+    masks = random_masks(H, 4, 0.5, 17)
+    for pv in (8, 4):
+        assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv, 200 + d, scale=scale) <= tol(d)
