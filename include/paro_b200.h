@@ -221,6 +221,10 @@ int paro_layer_destroy(paro_layer* layer);
  * The _device variant reads device bytes. */
 int paro_layer_set_masks(paro_layer* layer, paro_stream_t stream, const uint8_t* host_bits);
 int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const uint8_t* device_bits);
+/* The same from one serialized PMSK blob per head (deserialize_mask, mask.cpp:217-244): block 64,
+ * a ceil(N/64)^2 grid; errors name the head. */
+int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uint8_t* const* blobs,
+                              const size_t* sizes);
 
 /* K1: permuted gather + per-block quantization into layer-owned buffers. */
 int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,

@@ -685,6 +685,15 @@ class Layer:
         _check(_lib.paro_layer_set_masks(P(self.ptr), P(stream), P(_ptr(b))))
         _check(_lib.paro_stream_sync(P(stream)))
 
+    def set_masks_pmsk(self, blobs: Sequence[bytes], stream=None) -> None:
+        """One serialized PMSK mask per head (deserialize_mask, mask.cpp:217-244)."""
+        if len(blobs) != self.heads:
+            raise ShapeError(f"{len(blobs)} PMSK blobs for {self.heads} heads")
+        bufs = [np.frombuffer(b, np.uint8).copy() if len(b) else np.zeros(1, np.uint8) for b in blobs]
+        ptrs = (ctypes.c_void_p * self.heads)(*[_ptr(x) for x in bufs])
+        sizes = (ctypes.c_size_t * self.heads)(*[len(b) for b in blobs])
+        _check(_lib.paro_layer_set_masks_pmsk(P(self.ptr), P(stream), ptrs, sizes))
+
     def set_masks_device(self, dptr: Optional[int], stream=None) -> None:
         _check(_lib.paro_layer_set_masks_device(P(self.ptr), P(stream), P(dptr) if dptr else None))
 

@@ -1281,6 +1281,31 @@ int paro_layer_set_masks(paro_layer* layer, paro_stream_t stream, const uint8_t*
     return guarded([&] { set_masks_impl(layer, (cudaStream_t)stream, host_bits, true); });
 }
 
+int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uint8_t* const* blobs,
+                              const size_t* sizes) {
+    return guarded([&] {
+        check_layer(layer);
+        const LayerDev& L = layer->L;
+        if (!blobs || !sizes)
+            fail(PARO_E_CONFIG, "null PMSK blob list");
+        const size_t kk = (size_t)L.kb * L.kb;
+        std::vector<uint8_t> bits((size_t)L.H * kk);
+        for (uint32_t h = 0; h < L.H; ++h) {
+            uint32_t kr = 0, kc = 0, block = 0;
+            decode_pmsk(blobs[h], sizes[h], &kr, &kc, &block, nullptr); // header + size checks
+            if (block != 64)
+                fail(PARO_E_CONFIG, "head " + std::to_string(h) + ": mask block " + std::to_string(block) +
+                                        ", the B200 path runs block 64");
+            if (kr != L.kb || kc != L.kb)
+                fail(PARO_E_SHAPE, "head " + std::to_string(h) + ": mask grid " + std::to_string(kr) + "x" +
+                                       std::to_string(kc) + " does not cover " + std::to_string(L.kb) + "x" +
+                                       std::to_string(L.kb) + " blocks");
+            decode_pmsk(blobs[h], sizes[h], &kr, &kc, &block, bits.data() + (size_t)h * kk);
+        }
+        set_masks_impl(layer, (cudaStream_t)stream, bits.data(), true);
+    });
+}
+
 int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const uint8_t* device_bits) {
     return guarded([&] { set_masks_impl(layer, (cudaStream_t)stream, device_bits, false); });
 }

@@ -358,3 +358,26 @@ def test_explicit_scale(paro, ctx, oracle, d, scale):
     masks = random_masks(H, 4, 0.5, 17)
     for pv in (8, 4):
         assert run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, orders, masks, pv, 200 + d, scale=scale) <= tol(d)
+
+
+def test_set_masks_from_pmsk_blobs(paro, ctx):
+    """paro_layer_set_masks_pmsk == set_masks on the deserialized bits (bit-identical
+    output), and the reference's error classes for a bad blob / grid / block."""
+    grid, H, d = "F:3,H:7,W:11", 2, 64
+    N, kb = 231, 4
+    q, k, v = make_inputs(H, N, d, 80)
+    masks = random_masks(H, kb, 0.5, 5)
+    blobs = [paro.serialize_mask(paro.BlockMask(kb, kb, 64, masks[h])) for h in range(H)]
+    layer = paro.Layer(ctx, H, d, grid, ["WHF", "HFW"])
+    layer.set_masks(masks)
+    ref, zref = layer.forward_host(q, k, v, 0.0, 8)
+    layer.set_masks_pmsk(blobs)
+    out, z = layer.forward_host(q, k, v, 0.0, 8)
+    assert np.array_equal(out, ref) and np.array_equal(z, zref)
+    with pytest.raises(paro.FormatError):
+        layer.set_masks_pmsk([blobs[0][:-1], blobs[1]])
+    with pytest.raises(paro.ShapeError):
+        layer.set_masks_pmsk([paro.serialize_mask(paro.BlockMask(3, 3, 64, np.ones((3, 3), np.uint8)))] * H)
+    with pytest.raises(paro.ConfigError):
+        layer.set_masks_pmsk([paro.serialize_mask(paro.BlockMask(kb, kb, 32, masks[0]))] * H)
+    layer.close()
