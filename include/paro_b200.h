@@ -244,7 +244,8 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
 
 /* End to end from HOST buffers (pinned for full speed): H2D of Q/K/V, K1, K3,
  * D2H of O (and zeroed if non-NULL), synchronised before returning. Heads are
- * processed in chunks (default: at least 8, at most ~96 MB of Q/K/V each) whose
+ * processed in chunks (default: at least 8, at most ~96 MB of Q/K/V each, the last
+ * one tapered into halving pieces so little work follows the final upload) whose
  * uploads, kernels and downloads are pipelined on three streams. */
 int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
                             float scale, int pv_bits, float* out, uint8_t* zeroed);

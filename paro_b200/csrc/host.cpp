@@ -316,6 +316,40 @@ uint32_t default_heads_per_chunk(uint32_t heads, size_t tokens, uint32_t d) {
     return std::max(1u, std::min(by_count, by_bytes));
 }
 
+// Chunk table of the host-buffer pipeline: chunks of hpc heads, the last one
+// tapered into halving pieces (hpc/2, hpc/4, ..., 1) when `taper`: what runs
+// after the final upload (its kernels and download) shrinks to about one head's
+// worth (c2: the last chunk's 0.67 ms kernels + 0.5 ms download were the tail).
+void set_chunks(paro::LayerDev& L, uint32_t hpc, bool taper) {
+    std::vector<uint32_t> sizes;
+    uint32_t left = L.H;
+    while (left > 0) {
+        const uint32_t n = std::min(hpc, left);
+        sizes.push_back(n);
+        left -= n;
+    }
+    if (taper && sizes.back() > 1) {
+        uint32_t last = sizes.back();
+        sizes.pop_back();
+        while (last > 1) {
+            const uint32_t piece = (last + 1) / 2;
+            sizes.push_back(piece);
+            last -= piece;
+        }
+        sizes.push_back(last);
+    }
+    while (sizes.size() > paro::kMaxChunks) { // merge the leading chunks pairwise
+        std::vector<uint32_t> merged;
+        for (size_t i = 0; i < sizes.size(); i += 2)
+            merged.push_back(sizes[i] + (i + 1 < sizes.size() ? sizes[i + 1] : 0));
+        sizes = merged;
+    }
+    L.nchunks = (uint32_t)sizes.size();
+    L.chunk_start[0] = 0;
+    for (uint32_t c = 0; c < L.nchunks; ++c)
+        L.chunk_start[c + 1] = L.chunk_start[c] + sizes[c];
+}
+
 void set_device(const paro_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
 template <typename T>
@@ -1224,7 +1258,7 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
             L.qb_count = dalloc<uint32_t>((size_t)heads * L.kb2);
             L.order = dalloc<uint32_t>((size_t)heads * L.np);
             L.order_chunk = dalloc<uint32_t>((size_t)heads * L.np);
-            L.hpc = default_heads_per_chunk(heads, N, head_dim);
+            set_chunks(L, default_heads_per_chunk(heads, N, head_dim), true);
             L.work_counter = dalloc<uint32_t>(1);
             l->fwd = dalloc<uint32_t>((size_t)heads * N);
             l->inv = dalloc<uint32_t>((size_t)heads * N);
@@ -1357,14 +1391,14 @@ int paro_layer_set_pipeline_chunks(paro_layer* layer, paro_stream_t stream, uint
             fail(PARO_E_CONFIG, "pipeline chunk count must be >= 1");
         set_device(layer->ctx);
         LayerDev& L = layer->L;
-        const uint32_t c = std::min(chunks, L.H);
-        L.hpc = (L.H + c - 1) / c;
+        const uint32_t c = std::min(std::min(chunks, L.H), paro::kMaxChunks);
+        set_chunks(L, (L.H + c - 1) / c, false);
         if (layer->masks_set) // re-sort the per-chunk work lists for the new split
             cuda_check(paro::launch_k2_order(L, (cudaStream_t)stream), "k2 order launch");
     });
 }
 
-// Host-buffer forward. Heads are split into chunks of L.hpc; chunk c's Q/K/V
+// Host-buffer forward. Heads are split into the chunks of L.chunk_start; chunk c's Q/K/V
 // upload (stream s_in), K1 + K3 (caller's stream) and output download
 // (stream s_out) are event-chained so PCIe traffic in both directions
 // overlaps the kernels of the neighbouring chunks. Returns when `out` (and
@@ -1392,10 +1426,12 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
             cuda_check(cudaStreamCreateWithFlags(&layer->s_in, cudaStreamNonBlocking), "stream create");
             cuda_check(cudaStreamCreateWithFlags(&layer->s_out, cudaStreamNonBlocking), "stream create");
         }
-        const uint32_t nchunks = (L.H + L.hpc - 1) / L.hpc;
+        const uint32_t nchunks = L.nchunks;
         while (layer->ev.size() < 1 + 3 * (size_t)nchunks) {
             cudaEvent_t e;
-            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+            cuda_check(cudaEventCreateWithFlags(&e, getenv("PARO_E2E_TRACE") ? cudaEventDefault
+                                                                             : cudaEventDisableTiming),
+                       "event create");
             layer->ev.push_back(e);
         }
         cudaEvent_t* ev = layer->ev.data();
@@ -1407,7 +1443,7 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
         layer->last_v_bits = pv_bits;
         layer->last_v = layer->dv;
         for (uint32_t c = 0; c < nchunks; ++c) {
-            const uint32_t h0 = c * L.hpc, hn = std::min(L.hpc, L.H - h0);
+            const uint32_t h0 = L.chunk_start[c], hn = L.chunk_start[c + 1] - h0;
             const size_t off = (size_t)h0 * head_elems, bytes = (size_t)hn * head_elems * 4;
             cudaEvent_t e_in = ev[1 + 3 * c], e_k = ev[2 + 3 * c], e_out = ev[3 + 3 * c];
             cuda_check(cudaMemcpyAsync(layer->dq + off, q + off, bytes, cudaMemcpyHostToDevice, layer->s_in), "H2D q");
@@ -1429,6 +1465,16 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
         }
         cuda_check(cudaStreamWaitEvent(st, ev[3 * nchunks], 0), "stream wait");
         cuda_check(cudaStreamSynchronize(st), "forward_host sync");
+        if (getenv("PARO_E2E_TRACE")) { // per chunk: upload done / kernels done / download done (ms from start)
+            cudaEvent_t* e = layer->ev.data();
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                float a = 0, b = 0, d = 0;
+                cudaEventElapsedTime(&a, e[0], e[1 + 3 * c]);
+                cudaEventElapsedTime(&b, e[0], e[2 + 3 * c]);
+                cudaEventElapsedTime(&d, e[0], e[3 + 3 * c]);
+                fprintf(stderr, "[e2e] chunk %u: in %.3f  kern %.3f  out %.3f\n", c, a, b, d);
+            }
+        }
         layer->last_launches = 2 * (int)nchunks;
     });
 }

@@ -23,6 +23,7 @@
 namespace paro {
 
 constexpr int kBlock = 64;
+constexpr uint32_t kMaxChunks = 64;
 
 // Permuted index i -> original token: decompose i row-major over the permuted
 // extents (pext), then recombine with the original strides of those axes.
@@ -58,8 +59,9 @@ struct LayerDev {
     uint32_t* pair_count;
     uint32_t* qb_count;
     uint32_t* order;       // [H*np] global LPT order (h << 16 | p)
-    uint32_t* order_chunk; // [H*np] per-chunk LPT order, chunk c = heads [c*hpc, (c+1)*hpc)
-    uint32_t hpc;          // heads per chunk of the host-buffer pipeline
+    uint32_t* order_chunk; // [H*np] per-chunk LPT order, chunk c = heads [chunk_start[c], chunk_start[c+1])
+    uint32_t nchunks;      // host-buffer pipeline chunks (<= kMaxChunks)
+    uint32_t chunk_start[65];
     uint32_t* work_counter;
     // dense text-token prefix (AttnInputs::dense_prefix): dp rows / tokens, nd =
     // ceil(dp/64) dense key tiles; K4 hands K3 each non-dense row's running

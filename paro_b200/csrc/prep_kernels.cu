@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
 // then atomic placement (the order of equal-count items is unspecified -- each
 // item's result is independent of when it runs, so outputs are unaffected; a
 // single-warp stable placement cost 48 us at c2). Block 0 sorts all H*np items
-// into L.order; block c >= 1 sorts the items of heads [(c-1)*hpc, c*hpc) into
+// into L.order; block c >= 1 sorts the items of chunk c-1's heads into
 // the same span of L.order_chunk (the chunked host-buffer pipeline runs K3
 // once per chunk).
 __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
     uint32_t h0 = 0, h1 = L.H;
     uint32_t* out = L.order;
     if (blockIdx.x > 0) {
-        h0 = (blockIdx.x - 1) * L.hpc;
-        h1 = min(L.H, h0 + L.hpc);
+        h0 = L.chunk_start[blockIdx.x - 1];
+        h1 = L.chunk_start[blockIdx.x];
         out = L.order_chunk;
     }
     const uint32_t first = h0 * L.np, total = (h1 - h0) * L.np;
@@ -538,8 +538,7 @@ cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
 }
 
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st) {
-    const uint32_t nchunks = (L.H + L.hpc - 1) / L.hpc;
-    k2_work_order<<<1 + nchunks, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    k2_work_order<<<1 + L.nchunks, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
     return cudaGetLastError();
 }
 
