@@ -1392,7 +1392,10 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             auto dequant = [&](uint32_t U) {
                 const uint32_t b = U & 1, ph = (U >> 1) & 1;
                 PROF_T(te0);
-                ptx::mbar_wait(bar(BR::OFULL + b), ph);
+                // PFULL(U) (already complete: every compute warp arrived) orders the
+                // half-0 warp's rowmeta / column-offset writes before these reads
+                // directly, not only through the MMA's commit of O
+                mbar_wait2(bar(BR::OFULL + b), ph, bar(BR::PFULL + b), ph);
                 ptx::tc_fence_after();
                 PROF_T(te1);
                 PROF_ADD(5, te1 - te0);
