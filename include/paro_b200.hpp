@@ -17,6 +17,7 @@
 // an InvariantError (exit code 4). There is no CPU fallback.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -173,5 +174,93 @@ inline paro::AttnResult quantized_blocked_attention(const paro::AttnInputs& in, 
             res.zeroed_rows.push_back((uint32_t)i);
     return res;
 }
+
+// cmd_run's per-head chain (tools/main.cpp:276-305) for a whole layer of H
+// heads in one call: per-head orders (PermPlan::with_prefix when dense_prefix >
+// 0), per-head masks, Q/K/V per head in original token order, outputs and
+// zeroed rows per head -- the reference's types in and out, the B200 layer
+// (K1, K2, K3 and, with a prefix, K4) underneath.
+class Layer {
+public:
+    Layer(const paro::TokenGrid& grid, size_t heads, size_t head_dim, const std::vector<std::string>& orders,
+          size_t dense_prefix = 0)
+        : heads_(heads), head_dim_(head_dim), tokens_(grid.token_count() + dense_prefix) {
+        if (orders.size() != heads)
+            throw paro::ShapeError(std::to_string(orders.size()) + " orders for " + std::to_string(heads) +
+                                   " heads");
+        std::string labels, ords;
+        for (const auto& a : grid.axes)
+            labels += a.label;
+        std::string text;
+        for (const auto& a : grid.axes)
+            text += (text.empty() ? "" : ",") + std::string(1, a.label) + ":" + std::to_string(a.extent);
+        for (const auto& o : orders) {
+            if (o.size() != labels.size())
+                throw paro::ConfigError("order '" + o + "' does not name the grid's " + std::to_string(labels.size()) +
+                                        " axes");
+            ords += o;
+        }
+        check(paro_layer_create_prefix(context(), (uint32_t)heads, (uint32_t)head_dim, text.c_str(), ords.c_str(),
+                                       (uint32_t)dense_prefix, &layer_));
+    }
+    Layer(const Layer&) = delete;
+    Layer& operator=(const Layer&) = delete;
+    ~Layer() {
+        if (layer_)
+            paro_layer_destroy(layer_);
+    }
+    // one k x k mask per head (block 64), the grid over the permuted tokens
+    void set_masks(const std::vector<paro::BlockMask>& masks) {
+        if (masks.size() != heads_)
+            throw paro::ShapeError(std::to_string(masks.size()) + " masks for " + std::to_string(heads_) + " heads");
+        const size_t kb = (tokens_ + 63) / 64;
+        std::vector<uint8_t> bits;
+        bits.reserve(heads_ * kb * kb);
+        for (const auto& m : masks) {
+            if (m.block != 64)
+                throw paro::ConfigError("the B200 path runs block 64, got " + std::to_string(m.block));
+            if (m.k_rows != kb || m.k_cols != kb)
+                throw paro::ShapeError("mask grid " + std::to_string(m.k_rows) + "x" + std::to_string(m.k_cols) +
+                                       " does not cover " + std::to_string(kb) + "x" + std::to_string(kb) + " blocks");
+            bits.insert(bits.end(), m.bits.begin(), m.bits.end());
+        }
+        check(paro_layer_set_masks(layer_, nullptr, bits.data()));
+    }
+    // all heads' attention (scale 0 -> 1/sqrt(d)); pv_bits 8 or 4
+    std::vector<paro::AttnResult> forward(const std::vector<paro::Matrix>& q, const std::vector<paro::Matrix>& k,
+                                          const std::vector<paro::Matrix>& v, float scale, unsigned pv_bits) {
+        const size_t per = tokens_ * head_dim_;
+        if (q.size() != heads_ || k.size() != heads_ || v.size() != heads_)
+            throw paro::ShapeError("Q/K/V need one matrix per head");
+        std::vector<float> hq(heads_ * per), hk(heads_ * per), hv(heads_ * per), ho(heads_ * per);
+        std::vector<uint8_t> hz(heads_ * tokens_);
+        for (size_t h = 0; h < heads_; ++h) {
+            for (const paro::Matrix* m : {&q[h], &k[h], &v[h]})
+                if (m->rows != tokens_ || m->cols != head_dim_)
+                    throw paro::ShapeError("head " + std::to_string(h) + ": expected " + std::to_string(tokens_) +
+                                           "x" + std::to_string(head_dim_) + ", got " + std::to_string(m->rows) +
+                                           "x" + std::to_string(m->cols));
+            std::copy(q[h].data.begin(), q[h].data.end(), hq.begin() + h * per);
+            std::copy(k[h].data.begin(), k[h].data.end(), hk.begin() + h * per);
+            std::copy(v[h].data.begin(), v[h].data.end(), hv.begin() + h * per);
+        }
+        check(paro_layer_forward_host(layer_, nullptr, hq.data(), hk.data(), hv.data(), scale, (int)pv_bits,
+                                      ho.data(), hz.data()));
+        std::vector<paro::AttnResult> res(heads_);
+        for (size_t h = 0; h < heads_; ++h) {
+            res[h].output = paro::Matrix(tokens_, head_dim_);
+            std::copy(ho.begin() + h * per, ho.begin() + (h + 1) * per, res[h].output.data.begin());
+            for (size_t i = 0; i < tokens_; ++i)
+                if (hz[h * tokens_ + i])
+                    res[h].zeroed_rows.push_back((uint32_t)i);
+        }
+        return res;
+    }
+    size_t tokens() const { return tokens_; }
+
+private:
+    size_t heads_, head_dim_, tokens_;
+    paro_layer* layer_ = nullptr;
+};
 
 } // namespace paro_b200

@@ -143,6 +143,51 @@ static void gpu_tests() {
     }
     paro::AttnInputs all_dense{in.q, in.k, in.v, 0.0f, n};
     CHECK_THROWS_AS(paro_b200::quantized_blocked_attention(all_dense, &mask, paro::QuantConfig{}), paro::ConfigError);
+    // a whole layer (cmd_run's per-head chain for H heads): per-head orders, masks,
+    // optional text prefix (PermPlan::with_prefix) vs the reference's permutation +
+    // the restated engine + the reference's inverse permutation, head by head
+    for (size_t dp : {size_t(0), size_t(20)}) {
+        paro::TokenGrid g = paro::parse_grid("F:3,H:7,W:11");
+        const std::vector<std::string> orders{"WHF", "HFW"};
+        const size_t H = 2, d2 = 64, N = g.token_count() + dp, kb2 = (N + 63) / 64;
+        paro_b200::Layer layer(g, H, d2, orders, dp);
+        CHECK(layer.tokens() == N);
+        std::vector<paro::BlockMask> masks;
+        std::vector<paro::Matrix> q, k, v;
+        for (size_t h = 0; h < H; ++h) {
+            paro::BlockMask mk(kb2, kb2, 64, false);
+            for (size_t i = 0; i < kb2; ++i)
+                for (size_t j = 0; j < kb2; ++j)
+                    mk.set(i, j, i == j || ((i * 5 + j * 3 + h) % 4) < 2);
+            masks.push_back(mk);
+            q.push_back(randn(N, d2, 40 + h));
+            k.push_back(randn(N, d2, 50 + h));
+            v.push_back(randn(N, d2, 60 + h));
+        }
+        layer.set_masks(masks);
+        const std::vector<paro::AttnResult> out = layer.forward(q, k, v, 0.0f, 8);
+        for (size_t h = 0; h < H; ++h) {
+            paro::PermPlan plan = paro::make_perm(g, orders[h]);
+            if (dp)
+                plan = plan.with_prefix(dp);
+            const paro::Matrix qp = paro::apply_perm_rows(q[h], plan), kp = paro::apply_perm_rows(k[h], plan),
+                               vp = paro::apply_perm_rows(v[h], plan);
+            paro::Matrix refp(N, d2);
+            std::vector<uint8_t> z(N);
+            oracle_stream_engine(qp.data.data(), kp.data.data(), vp.data.data(), N, d2, 0.0f, dp, 64,
+                                 masks[h].bits.data(), 8, 1, refp.data.data(), z.data());
+            const paro::Matrix ref = paro::apply_perm_rows(refp, plan.inverted());
+            double md = 0, mo = 0;
+            for (size_t i = 0; i < N * d2; ++i) {
+                md = std::max(md, (double)std::fabs(out[h].output.data[i] - ref.data[i]));
+                mo = std::max(mo, (double)std::fabs(ref.data[i]));
+            }
+            std::printf("Layer head %zu dense_prefix=%zu: max|dO|/max|O| = %.3e\n", h, dp, md / mo);
+            CHECK(md / mo <= (dp ? 1e-4 : 1e-5));
+            CHECK(out[h].zeroed_rows.empty());
+        }
+        CHECK_THROWS_AS(layer.set_masks({masks[0]}), paro::ShapeError);
+    }
     paro::QuantConfig bad{16, paro::QuantMode::Unsigned, paro::QuantGrouping::PerBlock, 64};
     CHECK_THROWS_AS(paro_b200::quantized_blocked_attention(in, &mask, bad), paro::ConfigError);
     paro::AttnInputs short_v{in.q, in.k, randn(n - 1, d, 3), 0.0f, 0};
