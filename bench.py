@@ -489,8 +489,10 @@ def main():
         hv.array[...] = v
         hout = paro.HostBuffer(q.shape, np.float32)
         hz = paro.HostBuffer((hpr, N), np.uint8)
-        layer.set_masks_device(dmask.data_ptr(), sp)
+        hm = paro.HostBuffer(masks.shape, np.uint8) # the step's masks come from the host too
+        hm.array[...] = masks
         for _ in range(2):
+            layer.set_masks(hm.array, sp, sync=False)
             layer.forward_host(hq.array, hk.array, hv.array, 0.0, pv_bits, hout.array, hz.array, sp)
         e_steps = max(3, min(args.steps, 10))
         if dist:
@@ -499,7 +501,7 @@ def main():
         a, b = ev(), ev()
         a.record(stream)
         for _ in range(e_steps):
-            layer.set_masks_device(dmask.data_ptr(), sp)
+            layer.set_masks(hm.array, sp, sync=False)
             layer.forward_host(hq.array, hk.array, hv.array, 0.0, pv_bits, hout.array, hz.array, sp)
         b.record(stream)
         torch.cuda.synchronize()
@@ -509,7 +511,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": total_ops / (e_ms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_layer": e_ms,
-               "h2d_bytes_per_step": int(3 * q.nbytes) * world, "d2h_bytes_per_step": int(q.nbytes + hz.array.nbytes) * world}
+               "h2d_bytes_per_step": int(3 * q.nbytes + masks.nbytes) * world,
+               "d2h_bytes_per_step": int(q.nbytes + hz.array.nbytes) * world}
 
     # rooflines (rank-0 numbers; per launch = per layer shard)
     hbm_peak, bf16_peak, peak_src = measured_peaks()

@@ -675,7 +675,9 @@ class Layer:
         except Exception:
             pass
 
-    def set_masks(self, bits: Optional[np.ndarray], stream=None) -> None:
+    def set_masks(self, bits: Optional[np.ndarray], stream=None, sync: bool = True) -> None:
+        """Host mask bytes [H][k][k] (None = all kept). sync=False leaves the upload and K2
+        queued on `stream` (then `bits` must stay alive, e.g. a pinned HostBuffer)."""
         if bits is None:
             _check(_lib.paro_layer_set_masks(P(self.ptr), P(stream), None))
             return
@@ -683,7 +685,8 @@ class Layer:
         if b.size != self.heads * self.kb * self.kb:
             raise ShapeError(f"masks must be {self.heads}x{self.kb}x{self.kb} bytes, got {b.shape}")
         _check(_lib.paro_layer_set_masks(P(self.ptr), P(stream), P(_ptr(b))))
-        _check(_lib.paro_stream_sync(P(stream)))
+        if sync or b is not bits:
+            _check(_lib.paro_stream_sync(P(stream)))
 
     def set_masks_pmsk(self, blobs: Sequence[bytes], stream=None) -> None:
         """One serialized PMSK mask per head (deserialize_mask, mask.cpp:217-244)."""
