@@ -36,3 +36,22 @@ def test_random_layer_matches_oracle(paro, ctx, oracle, seed):
     masks = random_masks(H, kb, density, seed, empty_row=(kb - 1 if density == 0.15 else None))
     err = run_layer_vs_oracle(paro, ctx, oracle, grid, H, d, ords, masks, pv, 500 + seed, scale=scale)
     assert err <= EXACT_TOL, (grid, d, pv, density, scale, err)
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_random_dense_prefix_layer_matches_oracle(paro, ctx, oracle, seed):
+    """Random text-prefix lengths (K4a / K4 / combine + K3 from K4's state)."""
+    from test_gpu_parity import PREFIX_TOL, run_prefix_layer_vs_oracle
+
+    grid, d, pv, density, _ = case(2000 + seed)
+    g = paro.parse_grid(grid)
+    rng = np.random.default_rng(seed + 77)
+    dp = int(rng.integers(1, 300))
+    N = g.token_count() + dp
+    kb = (N + 63) // 64
+    orders = paro.enumerate_orders(g)
+    H = int(rng.integers(1, 3))
+    ords = [orders[int(rng.integers(0, len(orders)))] for _ in range(H)]
+    masks = random_masks(H, kb, max(density, 0.1), seed + 5)
+    err = run_prefix_layer_vs_oracle(paro, ctx, oracle, grid, H, d, ords, dp, masks, pv, 700 + seed)
+    assert err <= PREFIX_TOL, (grid, dp, d, pv, err)
