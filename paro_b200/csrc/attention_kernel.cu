@@ -49,6 +49,9 @@
 
 namespace paro {
 
+#ifndef PARO_DYNAMIC
+#define PARO_DYNAMIC 1
+#endif
 template <int D>
 struct K3Cfg {
     static constexpr int G = D / 64;
@@ -88,7 +91,8 @@ struct K3Cfg {
     static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 16) : 0); // + int4 S pairs
     // exact path: per compute warp, its risky (owner lane, group) list (<= 32 x 16 entries)
     static constexpr uint32_t OFF_BAR = OFF_XLIST + NCW * 512 * 2;
-    static constexpr uint32_t NBAR = 2 + 2 * NS + 17; // == Bars<NS>::COUNT (static_assert below)
+    static constexpr uint32_t NBAR = 2 + 2 * NS + 21; // == Bars<NS>::COUNT (static_assert below)
+    static constexpr uint32_t NCONS = 9; // warps reading the item queue: MMA + 8 (softmax + epilogue | compute)
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
     // swizzle: rows of D int8 -> 64B (D=64) or 128B (D=128) swizzle atoms of 8 rows
@@ -105,7 +109,8 @@ struct Bars {
     static constexpr uint32_t KVFULL = 2, KVEMPTY = 2 + NS, SFULL = 2 + 2 * NS, SEMPTY = SFULL + 2,
                               PFULL = SEMPTY + 2, PEMPTY = PFULL + 2, OFULL = PEMPTY + 2, OEMPTY = OFULL + 2,
                               LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1,
-                              QFULL1 = RED + 1, QEMPTY1 = RED + 2, COUNT = QEMPTY1 + 1;
+                              QFULL1 = RED + 1, QEMPTY1 = RED + 2, ITEMFULL = QEMPTY1 + 1, ITEMEMPTY = ITEMFULL + 2,
+                              COUNT = ITEMEMPTY + 2;
 };
 static_assert(Bars<K3Cfg<64>::NS>::COUNT == K3Cfg<64>::NBAR && Bars<K3Cfg<128>::NS>::COUNT == K3Cfg<128>::NBAR,
               "mbarrier block must hold every barrier (the TMEM pointer slot follows it)");
@@ -204,6 +209,7 @@ struct K3Params {
     uint8_t* zeroed;  // [H][N] or null
     const uint32_t* order; // LPT-sorted work items (h << 16 | p) of this launch
     uint32_t n_items;
+    uint32_t* work_counter; // next index into `order` (zeroed before the launch; DYNAMIC)
     unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
 };
 
@@ -990,6 +996,10 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_init(bar(BR::OEMPTY + b), C::NCW);
         }
         ptx::mbar_init(bar(BR::RED), C::NCW); // P-group extremes published (one arrival per compute warp)
+        for (int i = 0; i < 2; ++i) { // item queue: producer -> the other roles
+            ptx::mbar_init(bar(BR::ITEMFULL + i), 1);
+            ptx::mbar_init(bar(BR::ITEMEMPTY + i), C::NCONS);
+        }
         ptx::mbar_init(bar(BR::LFULL), 4); // !SPLIT: softmax -> epilogue row sums
         ptx::mbar_init(bar(BR::LEMPTY), 4);
         ptx::fence_barrier_init();
@@ -1008,6 +1018,25 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         const uint32_t idx = r * G_cta + ((r & 1) ? (G_cta - 1 - blockIdx.x) : blockIdx.x);
         return idx < P.n_items ? (int)P.order[idx] : -1;
     };
+    // DYNAMIC: the producer takes the next LPT item from a global counter (a CTA
+    // that finishes early takes more: greedy LPT instead of a static deal -- the
+    // tail matters at a few items per CTA) and hands it to the other roles
+    // through a 2-slot queue; -1 ends the CTA's work
+    volatile int* ring = reinterpret_cast<volatile int*>(smem + C::OFF_TMEMPTR + 8);
+    auto next_item = [&](uint32_t k, bool lazy) -> int { // consumers: the CTA's k-th item
+        if (!PARO_DYNAMIC)
+            return k < rounds ? item_at(k) : -1;
+        const uint32_t slot = k & 1;
+        if (lazy)
+            mbar_wait_lazy(bar(BR::ITEMFULL + slot), (k >> 1) & 1);
+        else
+            ptx::mbar_wait(bar(BR::ITEMFULL + slot), (k >> 1) & 1);
+        return ring[slot];
+    };
+    auto release_item = [&](uint32_t k) { // one arrival per consumer warp (caller: one lane)
+        if (PARO_DYNAMIC)
+            ptx::mbar_arrive(bar(BR::ITEMEMPTY + (k & 1)));
+    };
     auto stage = [&](uint32_t s) { return sbase + C::OFF_STAGE + s * C::STAGE_BYTES; };
     auto qfull = [&](uint32_t i) { return bar((i & 1) ? BR::QFULL1 : (uint32_t)B_QFULL); };
     auto qempty = [&](uint32_t i) { return bar((i & 1) ? BR::QEMPTY1 : (uint32_t)B_QEMPTY); };
@@ -1022,10 +1051,24 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::prefetch_tmap(&tm_k);
             ptx::prefetch_tmap(&tm_v);
             uint32_t T = 0, I = 0;
-            for (uint32_t r = 0; r < rounds; ++r) {
-                const int it = item_at(r);
-                if (it < 0)
-                    continue;
+            for (uint32_t r = 0;; ++r) {
+                int it;
+                if (PARO_DYNAMIC) {
+                    const uint32_t idx = atomicAdd(P.work_counter, 1u);
+                    it = idx < P.n_items ? (int)P.order[idx] : -1;
+                    const uint32_t slot = r & 1;
+                    mbar_wait_lazy(bar(BR::ITEMEMPTY + slot), ((r >> 1) & 1) ^ 1);
+                    ring[slot] = it;
+                    ptx::mbar_arrive(bar(BR::ITEMFULL + slot));
+                    if (it < 0)
+                        break;
+                } else {
+                    if (r >= rounds)
+                        break;
+                    it = item_at(r);
+                    if (it < 0)
+                        continue;
+                }
                 const Item x = load_item(L, (uint32_t)it);
                 const uint16_t* la = L.items + ((size_t)x.h * L.kb + x.qa) * L.kb;
                 const uint16_t* lb = L.items + ((size_t)x.h * L.kb + (x.qb != 0xffffu ? x.qb : 0)) * L.kb;
@@ -1089,10 +1132,16 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 ptx::mma_commit(bar(BR::KVEMPTY + s));
                 ptx::mma_commit(bar(BR::PEMPTY + b));
             };
-            for (uint32_t r = 0; r < rounds; ++r) {
-                const int it = item_at(r);
-                if (it < 0)
+            for (uint32_t r = 0;; ++r) {
+                if (!PARO_DYNAMIC && r >= rounds)
+                    break;
+                const int it = next_item(r, true);
+                release_item(r);
+                if (it < 0) {
+                    if (PARO_DYNAMIC)
+                        break;
                     continue;
+                }
                 const Item x = load_item(L, (uint32_t)it);
                 ptx::mbar_wait(qfull(I), (I >> 1) & 1);
                 ptx::tc_fence_after();
@@ -1141,10 +1190,18 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         const uint32_t tail = L.N & 63;
         uint32_t T = 0, I = 0;
         unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t rr = 0; rr < rounds; ++rr) {
-            const int it = item_at(rr);
-            if (it < 0)
+        for (uint32_t rr = 0;; ++rr) {
+            if (!PARO_DYNAMIC && rr >= rounds)
+                break;
+            const int it = next_item(rr, false);
+            __syncwarp();
+            if (lane == 0)
+                release_item(rr);
+            if (it < 0) {
+                if (PARO_DYNAMIC)
+                    break;
                 continue;
+            }
             const Item x = load_item(L, (uint32_t)it);
             const bool has_qb = side ? x.qb != 0xffffu : true;
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
@@ -1241,10 +1298,18 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         const float* lsm = reinterpret_cast<const float*>(smem + C::OFF_L);
         uint32_t T = 0, I = 0;
         unsigned long long prof[4] = {0, 0, 0, 0};
-        for (uint32_t rr = 0; rr < rounds; ++rr) {
-            const int it = item_at(rr);
-            if (it < 0)
+        for (uint32_t rr = 0;; ++rr) {
+            if (!PARO_DYNAMIC && rr >= rounds)
+                break;
+            const int it = next_item(rr, true);
+            __syncwarp();
+            if (lane == 0)
+                release_item(rr);
+            if (it < 0) {
+                if (PARO_DYNAMIC)
+                    break;
                 continue;
+            }
             const Item x = load_item(L, (uint32_t)it);
             const bool has_qb = side ? x.qb != 0xffffu : true;
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
@@ -1357,10 +1422,18 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         constexpr int DH = D / 2; // O columns per warp
         uint32_t T = 0, I = 0;
         unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t rr = 0; rr < rounds; ++rr) {
-            const int it = item_at(rr);
-            if (it < 0)
+        for (uint32_t rr = 0;; ++rr) {
+            if (!PARO_DYNAMIC && rr >= rounds)
+                break;
+            const int it = next_item(rr, false);
+            __syncwarp();
+            if (lane == 0)
+                release_item(rr);
+            if (it < 0) {
+                if (PARO_DYNAMIC)
+                    break;
                 continue;
+            }
             const Item x = load_item(L, (uint32_t)it);
             const bool has_qb = side ? x.qb != 0xffffu : true;
             const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
@@ -1636,6 +1709,12 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
     p.order = (chunked ? L.order_chunk : L.order) + (size_t)head_begin * L.np;
     p.n_items = head_count * L.np;
     p.stats = nullptr;
+    p.work_counter = L.work_counter;
+    if (PARO_DYNAMIC) {
+        const cudaError_t e = cudaMemsetAsync(L.work_counter, 0, sizeof(uint32_t), st);
+        if (e != cudaSuccess)
+            return e;
+    }
 #ifdef PARO_K3_STATS
     static unsigned long long* dstats = nullptr;
     if (!dstats) {
