@@ -25,7 +25,9 @@
 // lanes 16-31 (the M=64 datapath layout at lane offset 0 / 16). Step t runs
 // tile A.list[t] and tile B.list[t] side by side, so every softmax lane works
 // on a kept tile (no union of mask rows) and the pair costs max(nA, nB) steps.
-// Units are LPT-sorted by K2 and dealt to persistent CTAs in snake order.
+// Units are LPT-sorted by K2; each persistent CTA takes the next one from a
+// global counter when its producer is ready (greedy LPT), and hands it to its
+// other roles through a 2-slot mbarrier queue.
 //
 // Warp roles (320 threads; 2 CTAs/SM at d=64, 1 at d=128):
 //   warp 0     TMA producer: Q tiles, per step the K/V tiles + meta of A and B
@@ -1013,7 +1015,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
 
     const uint32_t G_cta = gridDim.x;
     const uint32_t rounds = (P.n_items + G_cta - 1) / G_cta;
-    // snake dealing of the LPT-sorted work list
+    // static snake dealing of the LPT-sorted work list (PARO_DYNAMIC=0 builds)
     auto item_at = [&](uint32_t r) -> int {
         const uint32_t idx = r * G_cta + ((r & 1) ? (G_cta - 1 - blockIdx.x) : blockIdx.x);
         return idx < P.n_items ? (int)P.order[idx] : -1;

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
 }
 
 // K2c. Counting sort of work items by step count, longest first (LPT order
-// for K3's snake distribution): block-wide scan of the descending histogram,
+// for K3's greedy dynamic distribution): block-wide scan of the descending histogram,
 // then atomic placement (the order of equal-count items is unspecified -- each
 // item's result is independent of when it runs, so outputs are unaffected; a
 // single-warp stable placement cost 48 us at c2). Block 0 sorts all H*np items
