@@ -273,7 +273,7 @@ def maskgen_main(args):
     peak = measured_peaks()[0]
     line = {"metric": "K5 mask producer: permuted block_sums of one calibration map (GB/s of map read)",
             "value": bytes_ / ms / 1e6, "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 in, fp64 sums",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "dtype_detail": "fp32 map in, fp64 block sums (reference order)",
             "data": "synthetic U[0,1) map on the device", "config": {"workload": f"N={N} (F:13,H:30,W:45) order WHF, block 64"},
             "roofline": {"bound": "hbm", "achieved": bytes_ / ms / 1e6, "peak": peak, "unit": "GB/s",
                          "frac": (bytes_ / ms / 1e6) / peak if peak else None, "traffic": None},
@@ -333,7 +333,7 @@ def permsel_main(args):
     peak = measured_peaks()[0]
     line = {"metric": "select_permutation of one c2 calibration map, all candidate orders (ms, wall incl. host reductions)",
             "value": ms, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 map, fp64 statistics",
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "dtype_detail": "fp32 map in, fp64 statistics",
             "data": "synthetic U[0,1) map on the device",
             "config": {"workload": f"N={N} ({grid}), {nperm.value} orders, block 64, eps 1e-3, sigma 0.9, alpha 0.5"},
             "roofline": {"bound": "hbm", "achieved": bytes_ / ms / 1e6, "peak": peak, "unit": "GB/s",
@@ -380,7 +380,7 @@ def main():
             "impl": "reference", "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
             "value": r["value"], "unit": "TOPS", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
             "ms_per_step": r["layer_seconds_extrapolated"] * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "fp64 QK / int8 P,V (reference CPU semantics)", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64", "dtype_detail": "reference CPU semantics: fp64 QK, int8/int4 P,V", "data": "synthetic",
             "config": {"workload": desc, "heads": H, "grid": grid_text, "head_dim": d, "density": density,
                        "pv_bits": pv_bits, "mask_family": "random"},
             "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
@@ -533,7 +533,8 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "int8 (QK s8*s8->s32, PV u8*s8->s32 on tcgen05; fp32 softmax/dequant)",
+        "dtype": "int8",
+        "dtype_detail": "QK s8*s8->s32 and PV u8(u4 codes)*s8->s32 on tcgen05; fp32 softmax / dequant, fp64 row extremes",
         "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), gen_mask masks",
         "config": {
             "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
