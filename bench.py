@@ -186,8 +186,11 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- CPU baseline (reference)
-def cpu_reference_sample(cfg_name, threads, max_heads=None):
-    """The reference's own CPU chain (oracle/_ref) on a bounded sample of heads."""
+def cpu_reference_sample(cfg_name, threads, max_heads=None, steps=1, warmup=0, budget_s=120.0):
+    """The reference's own CPU chain (oracle/_ref) on a bounded sample of heads
+    (about one head per thread), repeated: `warmup` untimed samples (at most 1)
+    and up to `steps` timed ones, stopping once `budget_s` of timed work is
+    done so the whole run stays within a few minutes."""
     from oracle.pyoracle import Reference, have_reference
 
     import paro_b200 as paro
@@ -206,17 +209,25 @@ def cpu_reference_sample(cfg_name, threads, max_heads=None):
     heads = list(range(n_run))
     q, k, v, masks = build_inputs(paro, heads, N, d, density, "random")
     orders = head_orders(paro, g, H)[:n_run]
-    _, secs = ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
-    ops = sum(kept_ops(masks[i], N, d) for i in range(n_run))
-    per_head_ops = ops / n_run
+    for _ in range(min(warmup, 1)):
+        ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
+    secs, done = 0.0, 0
+    while done < max(1, steps) and (done == 0 or secs < budget_s):
+        _, t = ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
+        secs += t
+        done += 1
+    ops = done * sum(kept_ops(masks[i], N, d) for i in range(n_run))
+    per_head_ops = ops / (done * n_run)
     return {
         "value": ops / secs / 1e12,
         "unit": "TOPS",
         "cores": threads,
         "kind": "reference",
-        "sample": f"{n_run} of {H} heads ({cfg_name}) on {threads} threads, {secs:.1f} s wall; "
-                  f"layer time extrapolated {H * per_head_ops / (ops / secs):.1f} s",
+        "sample": f"{n_run} of {H} heads ({cfg_name}) on {threads} threads per step, {done} step(s), "
+                  f"{secs:.1f} s wall; layer time extrapolated {H * per_head_ops / (ops / secs):.1f} s",
         "seconds": secs,
+        "steps": done,
+        "warmup": min(warmup, 1),
         "layer_seconds_extrapolated": H * per_head_ops / (ops / secs),
     }
 
@@ -372,13 +383,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference_sample(args.config, args.cpu_threads, None)
+        r = cpu_reference_sample(args.config, args.cpu_threads, None, args.steps, args.warmup)
         if r is None:
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparo_ref.so not built"}))
             return
         line = {
             "impl": "reference", "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
-            "value": r["value"], "unit": "TOPS", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "value": r["value"], "unit": "TOPS", "n_gpus": args.gpus, "steps": r["steps"], "warmup": r["warmup"],
             "ms_per_step": r["layer_seconds_extrapolated"] * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "dtype_detail": "reference CPU semantics: fp64 QK, int8/int4 P,V", "data": "synthetic",
             "config": {"workload": desc, "heads": H, "grid": grid_text, "head_dim": d, "density": density,
