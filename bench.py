@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
     ap.add_argument("--dense-prefix", type=int, default=0,
                     help="diagnostic: text tokens in front of the grid (K4 + K3); BASELINE configs use 0")
+    ap.add_argument("--rope", action="store_true",
+                    help="diagnostic: rotary embedding fused into K1 (paro_layer_set_rope); BASELINE configs do not rotate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
@@ -435,6 +437,10 @@ def main():
         total_ops = float(t.item())
 
     layer = paro.Layer(ctx, hpr, d, g, [orders_all[h] for h in my_heads], dense_prefix=args.dense_prefix)
+    if args.rope:  # diffusers-style real tables, one row per grid token (L2-resident across heads)
+        ang = np.repeat(np.arange(g.token_count(), dtype=np.float64)[:, None]
+                        * (10000.0 ** (-np.arange(d // 2) / (d // 2)))[None, :], 2, axis=1)
+        layer.set_rope(np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32))
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     dq = torch.from_numpy(q).cuda()
@@ -551,6 +557,7 @@ def main():
             "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
             "kept_density": round(density_kept, 5), "pv_bits": pv_bits, "mask_family": args.mask_family,
             **({"dense_prefix": args.dense_prefix} if args.dense_prefix else {}),
+            **({"rope": "fused into K1 (cos/sin tables read per row)"} if args.rope else {}),
             "parallelism": f"head-shard x{world} (no data-path collective)",
             "l2": f"inputs {3 * q.nbytes * world / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
         },

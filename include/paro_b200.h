@@ -226,6 +226,16 @@ int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const u
 int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uint8_t* const* blobs,
                               const size_t* sizes);
 
+/* Rotary embedding fused into K1 (the permutation and quantisation
+ * folded into the producer's last elementwise op). cos / sin: [N - dense_prefix][d] fp32 per
+ * ORIGINAL grid token (the DiT's real-valued freqs, e.g. diffusers' freqs_cos / freqs_sin),
+ * host or device memory, copied into the layer on `stream`. Q and K rows of grid tokens become
+ *   x'[2i] = x[2i] cos[2i] - x[2i+1] sin[2i],  x'[2i+1] = x[2i+1] cos[2i+1] + x[2i] sin[2i+1]
+ * (each product and sum rounded separately, fp32) before the reference quantizer; the text
+ * prefix and V are untouched. Both NULL turns it off. The same numbers as rotating the fp32
+ * inputs first and calling the layer without it (tests/test_gpu_parity.py). */
+int paro_layer_set_rope(paro_layer* layer, paro_stream_t stream, const float* cos, const float* sin);
+
 /* K1: permuted gather + per-block quantization into layer-owned buffers. */
 int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,
                                 const float* v, int v_bits);

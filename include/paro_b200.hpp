@@ -184,7 +184,7 @@ class Layer {
 public:
     Layer(const paro::TokenGrid& grid, size_t heads, size_t head_dim, const std::vector<std::string>& orders,
           size_t dense_prefix = 0)
-        : heads_(heads), head_dim_(head_dim), tokens_(grid.token_count() + dense_prefix) {
+        : heads_(heads), head_dim_(head_dim), tokens_(grid.token_count() + dense_prefix), prefix_(dense_prefix) {
         if (orders.size() != heads)
             throw paro::ShapeError(std::to_string(orders.size()) + " orders for " + std::to_string(heads) +
                                    " heads");
@@ -226,6 +226,19 @@ public:
         }
         check(paro_layer_set_masks(layer_, nullptr, bits.data()));
     }
+    // rotary embedding fused into the reorder+quantize pass (paro_layer_set_rope): cos / sin are
+    // [grid tokens x d] per original grid token (the text prefix is not rotated); empty = off
+    void set_rope(const paro::Matrix& cos, const paro::Matrix& sin) {
+        if (cos.data.empty() && sin.data.empty()) {
+            check(paro_layer_set_rope(layer_, nullptr, nullptr, nullptr));
+            return;
+        }
+        const size_t rows = tokens_ - prefix_;
+        if (cos.rows != rows || cos.cols != head_dim_ || !cos.same_shape(sin))
+            throw paro::ShapeError("rope tables must be " + std::to_string(rows) + "x" + std::to_string(head_dim_));
+        check(paro_layer_set_rope(layer_, nullptr, cos.data.data(), sin.data.data()));
+        check(paro_stream_sync(nullptr));
+    }
     // all heads' attention (scale 0 -> 1/sqrt(d)); pv_bits 8 or 4
     std::vector<paro::AttnResult> forward(const std::vector<paro::Matrix>& q, const std::vector<paro::Matrix>& k,
                                           const std::vector<paro::Matrix>& v, float scale, unsigned pv_bits) {
@@ -259,7 +272,7 @@ public:
     size_t tokens() const { return tokens_; }
 
 private:
-    size_t heads_, head_dim_, tokens_;
+    size_t heads_, head_dim_, tokens_, prefix_;
     paro_layer* layer_ = nullptr;
 };
 

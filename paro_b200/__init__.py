@@ -697,6 +697,22 @@ class Layer:
         sizes = (ctypes.c_size_t * self.heads)(*[len(b) for b in blobs])
         _check(_lib.paro_layer_set_masks_pmsk(P(self.ptr), P(stream), ptrs, sizes))
 
+    def set_rope(self, cos: Optional[np.ndarray], sin: Optional[np.ndarray], stream=None) -> None:
+        """Rotary embedding fused into K1 (paro_layer_set_rope): cos / sin [N - dense_prefix, d]
+        fp32 per original grid token; None, None turns it off."""
+        if cos is None and sin is None:
+            _check(_lib.paro_layer_set_rope(P(self.ptr), P(stream), None, None))
+            return
+        if cos is None or sin is None:
+            raise ConfigError("rope: cos and sin must both be given or both be None")
+        shape = (self.N - self.dense_prefix, self.head_dim)
+        c = np.ascontiguousarray(cos, np.float32)
+        s = np.ascontiguousarray(sin, np.float32)
+        if c.shape != shape or s.shape != shape:
+            raise ShapeError(f"rope tables must be {shape}, got {c.shape} / {s.shape}")
+        _check(_lib.paro_layer_set_rope(P(self.ptr), P(stream), P(_ptr(c)), P(_ptr(s))))
+        _check(_lib.paro_stream_sync(P(stream)))
+
     def set_masks_device(self, dptr: Optional[int], stream=None) -> None:
         _check(_lib.paro_layer_set_masks_device(P(self.ptr), P(stream), P(dptr) if dptr else None))
 

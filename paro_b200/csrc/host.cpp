@@ -294,6 +294,7 @@ struct paro_layer {
     const float* last_v = nullptr; // fp32 V of the last reorder_quantize (K4 reads the dense tiles)
     CUtensorMap tm_q, tm_k, tm_v;
     // e2e staging
+    float* rope = nullptr; // [2][N - dp][D]: cos, sin (paro_layer_set_rope)
     float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
     uint8_t* dzero = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr; // H2D / D2H copy streams
@@ -388,6 +389,7 @@ void free_layer(paro_layer* l) {
     cudaFree(l->fwd);
     cudaFree(l->inv);
     cudaFree(l->mask_dev);
+    cudaFree(l->rope);
     cudaFree(l->dq);
     cudaFree(l->dk);
     cudaFree(l->dv);
@@ -1337,6 +1339,28 @@ int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uin
             decode_pmsk(blobs[h], sizes[h], &kr, &kc, &block, bits.data() + (size_t)h * kk);
         }
         set_masks_impl(layer, (cudaStream_t)stream, bits.data(), true);
+    });
+}
+
+int paro_layer_set_rope(paro_layer* layer, paro_stream_t stream, const float* cos, const float* sin) {
+    return guarded([&] {
+        check_layer(layer);
+        LayerDev& L = layer->L;
+        if (!cos != !sin)
+            fail(PARO_E_CONFIG, "rope: cos and sin must both be given or both be null");
+        if (!cos) {
+            L.rope_cos = L.rope_sin = nullptr;
+            return;
+        }
+        const size_t elems = (size_t)(L.N - L.dp) * L.D;
+        if (!layer->rope)
+            layer->rope = dalloc<float>(2 * elems);
+        const cudaStream_t st = (cudaStream_t)stream;
+        // host (pageable or pinned) or device tables: the copy kind is inferred (UVA)
+        cuda_check(cudaMemcpyAsync(layer->rope, cos, elems * 4, cudaMemcpyDefault, st), "rope cos copy");
+        cuda_check(cudaMemcpyAsync(layer->rope + elems, sin, elems * 4, cudaMemcpyDefault, st), "rope sin copy");
+        L.rope_cos = layer->rope;
+        L.rope_sin = layer->rope + elems;
     });
 }
 

@@ -79,6 +79,11 @@ struct LayerDev {
     // K4a: permuted V as transposed bf16 hi / lo tiles [H][kb2][D][64] (bf16 bits)
     uint16_t* vsplit_hi;
     uint16_t* vsplit_lo;
+    // rotary embedding fused into K1 (the producer's last elementwise op, SURVEY
+    // 8(f) rank 4): [N - dp][D] fp32 cos / sin per ORIGINAL grid token, applied
+    // to Q and K pairs (2i, 2i+1) before quantisation; nullptr = off
+    const float* rope_cos;
+    const float* rope_sin;
 };
 
 __host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }

@@ -149,6 +149,29 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(Laye
                                        : make_float4(0.f, 0.f, 0.f, 0.f); // the even-count filler block stays zero
         }
     }
+    if (L.rope_cos) {
+        // out[2i] = x[2i] cos[2i] - x[2i+1] sin[2i], out[2i+1] = x[2i+1] cos[2i+1] + x[2i] sin[2i+1],
+        // each product and sum rounded on its own (this TU is built with -fmad=false), i.e. the
+        // eager `x * cos + rotate_half(x) * sin` of the DiT's apply_rotary_emb in fp32
+        auto rot = [](float4 x, float4 c, float4 s) {
+            return make_float4(__fsub_rn(__fmul_rn(x.x, c.x), __fmul_rn(x.y, s.x)),
+                               __fadd_rn(__fmul_rn(x.y, c.y), __fmul_rn(x.x, s.y)),
+                               __fsub_rn(__fmul_rn(x.z, c.z), __fmul_rn(x.w, s.z)),
+                               __fadd_rn(__fmul_rn(x.w, c.w), __fmul_rn(x.z, s.w)));
+        };
+#pragma unroll
+        for (int j = 0; j < PASSES; ++j) {
+            const uint32_t rr = r0 + RPP * j, i = b * 64 + rr, src = s_src[rr];
+            if (src == 0xffffffffu || src < L.dp) // filler rows; text tokens carry no rotary embedding
+                continue;
+            const size_t t = (size_t)(src - L.dp) * D + c4 * 4;
+            const float4 c = __ldg(reinterpret_cast<const float4*>(L.rope_cos + t));
+            const float4 s = __ldg(reinterpret_cast<const float4*>(L.rope_sin + t));
+            xk[j] = rot(xk[j], c, s); // K padding rows repeat the block's first (rotated) row
+            if (i < L.N)
+                xq[j] = rot(xq[j], c, s);
+        }
+    }
 
     // per-thread amax: Q/K per column group, V over everything
     float aq = 0.f, ak = 0.f, av = 0.f;

@@ -187,6 +187,37 @@ static void gpu_tests() {
             CHECK(out[h].zeroed_rows.empty());
         }
         CHECK_THROWS_AS(layer.set_masks({masks[0]}), paro::ShapeError);
+        // rotary embedding fused into the reorder+quantize pass == rotating the fp32 rows first
+        paro::Matrix rc(N - dp, d2), rs(N - dp, d2);
+        for (size_t t = 0; t < N - dp; ++t)
+            for (size_t c = 0; c < d2; ++c) {
+                const double ang = (double)t * std::pow(10000.0, -(double)(c / 2) / (double)(d2 / 2));
+                rc.data[t * d2 + c] = (float)std::cos(ang);
+                rs.data[t * d2 + c] = (float)std::sin(ang);
+            }
+        std::vector<paro::Matrix> qr = q, kr = k;
+        for (size_t h = 0; h < H; ++h)
+            for (size_t t = dp; t < N; ++t)
+                for (size_t c = 0; c < d2; c += 2) {
+                    const size_t e = t * d2 + c, r = (t - dp) * d2 + c;
+                    for (paro::Matrix* m : {&qr[h], &kr[h]}) {
+                        const paro::Matrix& src = m == &qr[h] ? q[h] : k[h];
+                        const float a = src.data[e], b = src.data[e + 1];
+                        const float p0 = a * rc.data[r], p1 = b * rs.data[r];
+                        const float p2 = b * rc.data[r + 1], p3 = a * rs.data[r + 1];
+                        m->data[e] = p0 - p1;
+                        m->data[e + 1] = p2 + p3;
+                    }
+                }
+        const std::vector<paro::AttnResult> plain = layer.forward(qr, kr, v, 0.0f, 8);
+        layer.set_rope(rc, rs);
+        const std::vector<paro::AttnResult> fused = layer.forward(q, k, v, 0.0f, 8);
+        for (size_t h = 0; h < H; ++h)
+            CHECK(fused[h].output.data == plain[h].output.data);
+        std::printf("Layer dense_prefix=%zu: fused rotary embedding bit-identical to the fp32 pre-rotation\n", dp);
+        CHECK_THROWS_AS(layer.set_rope(paro::Matrix(N + 1, d2), paro::Matrix(N + 1, d2)), paro::ShapeError);
+        layer.set_rope(paro::Matrix(), paro::Matrix());
+        CHECK(layer.forward(qr, kr, v, 0.0f, 8)[0].output.data == plain[0].output.data);
     }
     paro::QuantConfig bad{16, paro::QuantMode::Unsigned, paro::QuantGrouping::PerBlock, 64};
     CHECK_THROWS_AS(paro_b200::quantized_blocked_attention(in, &mask, bad), paro::ConfigError);

@@ -381,3 +381,76 @@ def test_set_masks_from_pmsk_blobs(paro, ctx):
     with pytest.raises(paro.ConfigError):
         layer.set_masks_pmsk([paro.serialize_mask(paro.BlockMask(kb, kb, 32, masks[0]))] * H)
     layer.close()
+
+
+# ---- rotary embedding fused into K1 (paro_layer_set_rope)
+def rope_tables(n, d, seed, interleaved=True):
+    """3-axis-style rotary tables [n, d]: diffusers' real form (cos/sin repeated per pair) when
+    `interleaved`, else independent values per element (exercises the general formula)."""
+    rng = np.random.default_rng(seed)
+    if interleaved:
+        pos = np.arange(n, dtype=np.float64)[:, None]
+        freqs = 1.0 / (10000.0 ** (np.arange(d // 2, dtype=np.float64) / (d // 2)))
+        ang = np.repeat(pos * freqs[None, :] * (1.0 + rng.random((1, d // 2))), 2, axis=1)
+    else:
+        ang = rng.random((n, d)) * 6.3
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def np_rope(x, cos, sin, dp):
+    """x' = x*cos + rotate_half(x)*sin on the grid tokens, fp32, every op rounded (numpy)."""
+    y = x.copy()
+    g = x[:, dp:]
+    a, b = g[..., 0::2], g[..., 1::2]
+    y[:, dp:, 0::2] = a * cos[None, :, 0::2] - b * sin[None, :, 0::2]
+    y[:, dp:, 1::2] = b * cos[None, :, 1::2] + a * sin[None, :, 1::2]
+    return y
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("dp", [0, 40])
+@pytest.mark.parametrize("interleaved", [True, False])
+def test_rope_fused_equals_rotate_then_layer(paro, ctx, oracle, d, dp, interleaved):
+    grid, H, orders = ("F:3,H:7,W:11", 2, ["WHF", "FWH"])
+    g = paro.parse_grid(grid)
+    N = g.token_count() + dp
+    q, k, v = make_inputs(H, N, d, 77)
+    cos, sin = rope_tables(N - dp, d, 5, interleaved)
+    masks = random_masks(H, (N + 63) // 64, 0.6, 9)
+    a = paro.Layer(ctx, H, d, g, orders, dense_prefix=dp)
+    a.set_masks(masks)
+    a.set_rope(cos, sin)
+    out_a, z_a = a.forward_host(q, k, v, 0.0, 8)
+    b = paro.Layer(ctx, H, d, g, orders, dense_prefix=dp)
+    b.set_masks(masks)
+    qr, kr = np_rope(q, cos, sin, dp), np_rope(k, cos, sin, dp)
+    out_b, z_b = b.forward_host(qr, kr, v, 0.0, 8)
+    # bit-identical: the fused rotation rounds exactly like the fp32 pre-pass
+    assert np.array_equal(out_a, out_b) and np.array_equal(z_a, z_b)
+    # turning it off restores the plain layer
+    a.set_rope(None, None)
+    out_c, _ = a.forward_host(qr, kr, v, 0.0, 8)
+    assert np.array_equal(out_c, out_b)
+    a.close()
+    b.close()
+    if dp == 0:
+        worst = 0.0
+        for h in range(H):
+            fwd, inv = oracle.make_perm(g.labels, g.extents, orders[h])
+            ref, _ = oracle.paro_head(qr[h], kr[h], v[h], fwd, inv, masks[h], 8, qk_mode=1)
+            worst = max(worst, rel_err(out_a[h], ref))
+        assert worst <= EXACT_TOL, worst
+
+
+def test_rope_errors(paro, ctx):
+    g = paro.parse_grid("H:8,W:8")
+    layer = paro.Layer(ctx, 1, 64, g, ["HW"], dense_prefix=3)
+    cos, sin = rope_tables(67, 64, 1)
+    with pytest.raises(paro.ShapeError):
+        layer.set_rope(cos, sin)  # the tables cover the 64 grid tokens, not the 3 text tokens
+    cos, sin = rope_tables(64, 64, 1)
+    with pytest.raises(paro.ConfigError):
+        layer.set_rope(cos, None)
+    with pytest.raises(paro.ConfigError):  # the C ABI itself rejects half a table
+        paro._check(paro._lib.paro_layer_set_rope(paro.P(layer.ptr), None, paro.P(paro._ptr(cos)), None))
+    layer.close()
