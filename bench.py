@@ -42,6 +42,15 @@ CONFIGS = {
 }
 
 
+def _softmax_roofline(scores, k3_ms, clk):
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
+    achieved = scores / (k3_ms * 1e-3) / 1e12
+    peak = 16 * 148 * mhz * 1e6 / 1e12
+    return {"bound": "mufu_ex2", "kernel": "k3_attention", "achieved": achieved, "peak": peak,
+            "unit": "Tscores/s", "frac": achieved / peak, "scores_per_launch": int(scores),
+            "note": "kept (row, key) pairs / K3 time vs 16 ex2 / clk / SM x 148 SMs"}
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -570,6 +579,9 @@ def main():
             "peak_source": f"2x bf16_tflops {bf16_peak} ({peak_src}, MEASURED_PEAKS.json): dense INT8 tcgen05 rate",
             "algorithmic_ops_per_launch": my_ops,
         },
+        # the softmax ceiling the tensor-pipe fraction hides: one ex2 per kept score on the
+        # MUFU (16 / clk / SM), at the SM clock sampled during the run
+        "roofline_softmax": _softmax_roofline(my_ops / (4 * d), k3_ms, clk),
         "roofline_k1": {"bound": "hbm", "kernel": "k1_reorder_quantize", "achieved": k1_gbs, "peak": hbm_peak,
                         "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes,
                         "traffic": _scaled(ncu_traffic(args.config, "k1_reorder_quantize"), hpr / H)},

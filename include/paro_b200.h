@@ -232,7 +232,8 @@ int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uin
  * host or device memory, copied into the layer on `stream`. Q and K rows of grid tokens become
  *   x'[2i] = x[2i] cos[2i] - x[2i+1] sin[2i],  x'[2i+1] = x[2i+1] cos[2i+1] + x[2i] sin[2i+1]
  * (each product and sum rounded separately, fp32) before the reference quantizer; the text
- * prefix and V are untouched. Both NULL turns it off. The same numbers as rotating the fp32
+ * prefix and V are untouched. Both NULL turns it off. Pinned or device tables must stay valid
+ * until `stream` has passed the copy (pageable ones are staged before the call returns). The same numbers as rotating the fp32
  * inputs first and calling the layer without it (tests/test_gpu_parity.py). */
 int paro_layer_set_rope(paro_layer* layer, paro_stream_t stream, const float* cos, const float* sin);
 
