@@ -457,6 +457,14 @@ class DeviceBuffer:
             pass
 
 
+def _close(*bufs) -> None:
+    """Free temporaries now: the device allocations must not outlive the call
+    (compute-sanitizer --leak-check full found them alive at context teardown)."""
+    for b in bufs:
+        if b is not None:
+            b.close()
+
+
 def download_ptr(ptr: int, shape, dtype, stream=None) -> np.ndarray:
     out = np.empty(shape, dtype)
     _check(_lib.paro_memcpy(P(_ptr(out)), P(ptr), SZ(out.nbytes), P(stream)))
@@ -530,7 +538,9 @@ class Context:
         ds = DeviceBuffer(k * k * 8)
         _check(_lib.paro_perm_block_sums_device(P(self.ptr), None, P(dm.ptr), U32(n), P(dinv.ptr if dinv else None),
                                                 U32(block), P(ds.ptr)))
-        return ds.download((k, k), np.float64)
+        out = ds.download((k, k), np.float64)
+        _close(dm, dinv, ds)
+        return out
 
     def gen_mask(self, sums: np.ndarray, density: float, block: int, guard_blocks: int = 0):
         """gen_mask on the GPU for one [k, k] grid or a stack [count, k, k]
@@ -546,6 +556,7 @@ class Context:
                                          ctypes.c_double(density), U32(block), U32(guard_blocks), P(db.ptr),
                                          P(_ptr(rep))))
         bits = db.download((count, kr, kc), np.uint8)
+        _close(ds, db)
         masks = [BlockMask(kr, kc, block, bits[i]) for i in range(count)]
         return (masks, rep.tolist()) if stack else (masks[0], int(rep[0]))
 
@@ -562,6 +573,7 @@ class Context:
                                                ctypes.c_double(density), U32(block), U32(guard_blocks), P(dm.ptr),
                                                ctypes.byref(rep)))
         bits = dm.download((half + 1, kr, kc), np.uint8)
+        _close(ds, dm)
         return [BlockMask(kr, kc, block, bits[i]) for i in range(half + 1)], rep.value
 
     def select_permutation(self, maps, grid: "TokenGrid | str", block: int = 64, eps: float = 1e-3,
@@ -582,6 +594,7 @@ class Context:
                                                    U32(block), ctypes.c_float(eps), ctypes.c_float(sigma),
                                                    ctypes.c_float(alpha), U32(dense_prefix), orders, P(_ptr(scores)),
                                                    ctypes.byref(nperm), ctypes.byref(chosen)))
+        _close(dm)
         nd = len(orders.raw.rstrip(b"\0")) // nperm.value
         ords = [orders.raw[i * nd:(i + 1) * nd].decode() for i in range(nperm.value)]
         return ords, scores[:nperm.value], chosen.value
@@ -597,7 +610,9 @@ class Context:
         dout = DeviceBuffer(m.nbytes)
         _check(_lib.paro_apply_perm_rows_device(P(self.ptr), None, P(din.ptr), U32(m.shape[0]), U32(m.shape[1]),
                                                 P(dinv.ptr), P(dout.ptr)))
-        return dout.download(m.shape, np.float32)
+        out = dout.download(m.shape, np.float32)
+        _close(din, dinv, dout)
+        return out
 
     def quantize(self, m: np.ndarray, cfg: QuantConfig) -> QuantBlockTensor:
         """quantize(m, cfg) on the GPU for the hot path's configuration
@@ -614,7 +629,9 @@ class Context:
         _check(_lib.paro_quantize_sym_device(P(self.ptr), None, P(din.ptr), U32(rows), U32(cols), ctypes.c_int(cfg.bits),
                                              P(dc.ptr), P(ds.ptr)))
         codes = dc.download((rows, cols), np.int8).astype(np.int32)
-        return QuantBlockTensor(rows, cols, cfg, codes, ds.download((groups,), np.float32), np.zeros(0, np.float32))
+        scales = ds.download((groups,), np.float32)
+        _close(din, dc, ds)
+        return QuantBlockTensor(rows, cols, cfg, codes, scales, np.zeros(0, np.float32))
 
     def quantized_blocked_attention(self, inp: AttnInputs, mask: Optional[BlockMask], qcfg: QuantConfig) -> AttnResult:
         """quantized_blocked_attention (attention.hpp:52) with the INT8-QK stage, one head,
@@ -790,7 +807,9 @@ class Layer:
         ds = DeviceBuffer(t.shape[0] * G * 64 * 64 * 4)
         _check(_lib.paro_layer_debug_qk(P(self.ptr), None, U32(t.shape[0]), P(dt.ptr), P(ds.ptr)))
         _check(_lib.paro_stream_sync(None))
-        return ds.download((t.shape[0], G, 64, 64), np.int32)
+        out = ds.download((t.shape[0], G, 64, 64), np.int32)
+        _close(dt, ds)
+        return out
 
 
 def stream_sync(stream=None) -> None:
