@@ -31,6 +31,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)"
+
 CONFIGS = {
     # name: (grid, heads, d, density, pv_bits, description)
     "c1": ("F:2,H:8,W:8", 2, 64, 0.3, 8, "small synthetic F2xH8xW8, 2 heads, d=64, 30% (block 64 -> 50%), INT8/INT8"),
@@ -72,26 +74,28 @@ def parse_args():
 
 
 # ----------------------------------------------------------------------------- workload
-def head_orders(paro, grid, heads):
-    """Per-head order = enumerate_perms(grid)[head % ndim!]."""
-    orders = paro.enumerate_orders(grid)
-    return [orders[h % len(orders)] for h in range(heads)]
+# The same inputs in both arms, built by each arm's own library: the GPU arm
+# with the product (paro_b200: MT19937-64 stream, K5 gen_mask on the device),
+# the reference arm with the reference library only (oracle/_ref: its own
+# generator stream and gen_mask) -- the reference arm never loads libparo_b200.
+def grid_shape(grid_text):
+    """'F:13,H:30,W:45' -> (labels, extents, N) without any native library."""
+    labels, ext = "", []
+    for part in grid_text.split(","):
+        a, n = part.split(":")
+        labels += a.strip()
+        ext.append(int(n))
+    return labels, tuple(ext), int(np.prod(ext))
 
 
-def head_inputs(paro, h, N, d):
-    """Seeded N(0,1): MT19937-64 + Box-Muller, seed 1000 + 3*head + {0,1,2}."""
-    return [paro.synth_randn(1000 + 3 * h + i, N * d).reshape(N, d) for i in range(3)]
-
-
-def head_mask(paro, h, kb, density, family):
+def head_sums(h, kb, density, family):
+    """The calibration block sums gen_mask selects from."""
     rng = np.random.default_rng(7919 * (h + 1))
     if family == "random":  # M1: U[0,1) + 2*I (test_mask.cpp:28-37 shape)
-        sums = rng.random((kb, kb)) + 2.0 * np.eye(kb)
-    else:  # M2: exp(-|i-j|/w) + 0.05*U, w = density*k/2
-        w = max(density * kb / 2.0, 1.0)
-        i = np.arange(kb)
-        sums = np.exp(-np.abs(i[:, None] - i[None, :]) / w) + 0.05 * rng.random((kb, kb))
-    return paro.gen_mask(sums, density, 64)[0].bits
+        return rng.random((kb, kb)) + 2.0 * np.eye(kb)
+    w = max(density * kb / 2.0, 1.0)  # M2: exp(-|i-j|/w) + 0.05*U, w = density*k/2
+    i = np.arange(kb)
+    return np.exp(-np.abs(i[:, None] - i[None, :]) / w) + 0.05 * rng.random((kb, kb))
 
 
 def kept_ops(mask, N, d):
@@ -102,23 +106,82 @@ def kept_ops(mask, N, d):
     return int(4 * d * (ext[:, None] * ext[None, :] * (mask != 0)).sum())
 
 
-def build_inputs(paro, heads, N, d, density, family, threads=8):
+def workload_ours(paro, ctx, heads, grid_text, N, d, density, family):
+    """Per-head orders enumerate_perms(grid)[h % ndim!], seeded N(0,1) Q/K/V
+    (MT19937-64 + Box-Muller, seed 1000 + 3h + {0,1,2}), masks by K5 gen_mask on
+    the GPU over head_sums."""
     from concurrent.futures import ThreadPoolExecutor
 
+    g = paro.parse_grid(grid_text)
+    orders = paro.enumerate_orders(g)
     kb = (N + 63) // 64
     q = np.empty((len(heads), N, d), np.float32)
     k = np.empty_like(q)
     v = np.empty_like(q)
-    masks = np.empty((len(heads), kb, kb), np.uint8)
 
     def one(i):
         h = heads[i]
-        q[i], k[i], v[i] = head_inputs(paro, h, N, d)
-        masks[i] = head_mask(paro, h, kb, density, family)
+        q[i], k[i], v[i] = [paro.synth_randn(1000 + 3 * h + j, N * d).reshape(N, d) for j in range(3)]
 
-    with ThreadPoolExecutor(threads) as ex:
+    with ThreadPoolExecutor(8) as ex:
         list(ex.map(one, range(len(heads))))
-    return q, k, v, masks
+    ms, _ = ctx.gen_mask(np.stack([head_sums(h, kb, density, family) for h in heads]), density, 64)
+    masks = np.stack([m.bits for m in ms])
+    return [orders[h % len(orders)] for h in heads], q, k, v, masks
+
+
+def workload_reference(ref, heads, grid_text, N, d, density, family):
+    """The same workload from the reference library alone (oracle/_ref)."""
+    rc, labels, ext = ref.parse_grid(grid_text)
+    if rc:
+        raise RuntimeError(f"reference parse_grid failed ({rc})")
+    orders = ref.enumerate_orders(labels, ext)
+    kb = (N + 63) // 64
+    H = len(heads)
+    q = np.empty((H, N, d), np.float32)
+    k = np.empty_like(q)
+    v = np.empty_like(q)
+    for i, h in enumerate(heads):  # streams 3h, 3h+1, 3h+2 -> q, k, v
+        s = ref.synth_randn_streams(1000 + 3 * h, 1, 3, N * d)
+        q[i], k[i], v[i] = s[0].reshape(N, d), s[1].reshape(N, d), s[2].reshape(N, d)
+    masks = np.empty((H, kb, kb), np.uint8)
+    for i, h in enumerate(heads):
+        rc, bits, _ = ref.gen_mask(head_sums(h, kb, density, family), density, 64)
+        if rc:
+            raise RuntimeError(f"reference gen_mask failed ({rc})")
+        masks[i] = bits
+    return [orders[h % len(orders)] for h in heads], q, k, v, masks
+
+
+def bench_config(cfg_name, family, masks, world, dense_prefix=0, rope=False):
+    """The `config` object of the JSON line -- identical in both arms."""
+    grid_text, H, d, density, pv_bits, desc = CONFIGS[cfg_name]
+    N = grid_shape(grid_text)[2] + dense_prefix
+    return {
+        "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
+        "kept_density": round(float(np.mean(masks != 0)), 5), "pv_bits": pv_bits, "mask_family": family,
+        **({"dense_prefix": dense_prefix} if dense_prefix else {}),
+        **({"rope": "fused into K1 (cos/sin tables read per row)"} if rope else {}),
+        "parallelism": f"head-shard x{world} (no data-path collective)",
+        "l2": f"inputs {3 * H * N * d * 4 / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
+    }
+
+
+def cpu_info(threads):
+    model, flags = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                elif ln.startswith("flags"):
+                    flags = set(ln.split(":", 1)[1].split())
+                    break
+    except OSError:
+        pass
+    isa = [x for x in ("avx2", "fma", "avx512f", "avx512bw", "avx512_vnni", "amx_int8") if x in flags]
+    return {"nproc": os.cpu_count(), "threads_used": threads, "model": model, "isa": isa,
+            "reference_kernels": "PARO_KERNELS=auto (AVX2 TU when the CPU has avx2, kernels.cpp:17-39)"}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -197,49 +260,48 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- CPU baseline (reference)
-def cpu_reference_sample(cfg_name, threads, max_heads=None, steps=1, warmup=0, budget_s=120.0):
-    """The reference's own CPU chain (oracle/_ref) on a bounded sample of heads
-    (about one head per thread), repeated: `warmup` untimed samples (at most 1)
-    and up to `steps` timed ones, stopping once `budget_s` of timed work is
-    done so the whole run stays within a few minutes."""
+def reference_run(cfg_name, family, threads, steps, warmup):
+    """The reference's own CPU chain (cmd_run: apply_perm_rows x3 ->
+    quantized_blocked_attention -> inverse permute, main.cpp:276-305) from
+    oracle/_ref on the host cores, one std::thread per head. A step is a bounded
+    sample of the layer: `threads` heads (all H if H <= threads), cycling through
+    the layer's heads from step to step; `warmup` untimed steps first. Inputs and
+    masks come from the reference library itself (workload_reference). Returns
+    the measured time of what ran -- nothing is extrapolated into the value."""
     from oracle.pyoracle import Reference, have_reference
-
-    import paro_b200 as paro
 
     if not have_reference():
         return None
     grid_text, H, d, density, bits, _ = CONFIGS[cfg_name]
-    g = paro.parse_grid(grid_text)
-    N = g.token_count()
+    N = grid_shape(grid_text)[2]
     ref = Reference()
     ref.select_kernels("auto")
     threads = threads or os.cpu_count() or 1
-    # bounded sample: about one head per thread, sized for ~10-30 s of CPU work
-    per_head_ops = None
-    n_run = min(H, max_heads or threads)
-    heads = list(range(n_run))
-    q, k, v, masks = build_inputs(paro, heads, N, d, density, "random")
-    orders = head_orders(paro, g, H)[:n_run]
-    for _ in range(min(warmup, 1)):
-        ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
-    secs, done = 0.0, 0
-    while done < max(1, steps) and (done == 0 or secs < budget_s):
-        _, t = ref.run_heads(grid_text, q, k, v, orders, masks, bits, 0.0, threads)
-        secs += t
-        done += 1
-    ops = done * sum(kept_ops(masks[i], N, d) for i in range(n_run))
-    per_head_ops = ops / (done * n_run)
+    per = min(H, threads)
+    total = steps + warmup
+    sched = [[(s * per + j) % H for j in range(per)] for s in range(total)]
+    need = sorted({h for hs in sched for h in hs})
+    orders, q, k, v, masks = workload_reference(ref, need, grid_text, N, d, density, family)
+    kb = (N + 63) // 64
+    all_masks = np.empty((H, kb, kb), np.uint8)
+    for h in range(H):
+        all_masks[h] = ref.gen_mask(head_sums(h, kb, density, family), density, 64)[1]
+    idx = {h: i for i, h in enumerate(need)}
+    times, ops = [], 0
+    for s, hs in enumerate(sched):
+        sel = [idx[h] for h in hs]
+        _, t = ref.run_heads(grid_text, q[sel], k[sel], v[sel], [orders[i] for i in sel], masks[sel], bits, 0.0,
+                             threads)
+        if s >= warmup:
+            times.append(t)
+            ops += sum(kept_ops(masks[i], N, d) for i in sel)
+    secs = sum(times)
     return {
-        "value": ops / secs / 1e12,
-        "unit": "TOPS",
-        "cores": threads,
-        "kind": "reference",
-        "sample": f"{n_run} of {H} heads ({cfg_name}) on {threads} threads per step, {done} step(s), "
-                  f"{secs:.1f} s wall; layer time extrapolated {H * per_head_ops / (ops / secs):.1f} s",
-        "seconds": secs,
-        "steps": done,
-        "warmup": min(warmup, 1),
-        "layer_seconds_extrapolated": H * per_head_ops / (ops / secs),
+        "value": ops / secs / 1e12, "unit": "TOPS", "cores": threads, "kind": "reference",
+        "sample": f"{per} of {H} heads ({cfg_name}) per step, one per host thread, cycling through the layer; "
+                  f"{len(times)} timed step(s) after {warmup} warm-up, {secs:.1f} s timed",
+        "ms_per_step": secs / max(1, len(times)) * 1e3, "steps": len(times), "warmup": warmup,
+        "heads_per_step": per, "all_masks": all_masks, "cpu": cpu_info(threads),
     }
 
 
@@ -380,8 +442,23 @@ def permsel_main(args):
     print(json.dumps(line))
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: launch the N ranks (one per
+    GPU) through torch.distributed.run on 127.0.0.1 and pass rank 0's line on."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.config == "maskgen":
         return maskgen_main(args)
     if args.config == "permsel":
@@ -391,21 +468,27 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     grid_text, H, d, density, pv_bits, desc = CONFIGS[args.config]
 
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; run plain `python bench.py --gpus N` "
+                         "(it spawns the ranks) or torchrun with --nproc-per-node N")
+
     if args.impl == "reference":
-        if rank != 0:
+        if rank != 0:  # the reference is a host-CPU baseline: rank 0 alone runs it
             return
-        r = cpu_reference_sample(args.config, args.cpu_threads, None, args.steps, args.warmup)
+        r = reference_run(args.config, args.mask_family, args.cpu_threads, args.steps, args.warmup)
         if r is None:
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparo_ref.so not built"}))
             return
         line = {
-            "impl": "reference", "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
+            "impl": "reference", "metric": METRIC,
             "value": r["value"], "unit": "TOPS", "n_gpus": args.gpus, "steps": r["steps"], "warmup": r["warmup"],
-            "ms_per_step": r["layer_seconds_extrapolated"] * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "dtype_detail": "reference CPU semantics: fp64 QK, int8/int4 P,V", "data": "synthetic",
-            "config": {"workload": desc, "heads": H, "grid": grid_text, "head_dim": d, "density": density,
-                       "pv_bits": pv_bits, "mask_family": "random"},
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "dtype_detail": "reference CPU semantics: fp64 QK logits, int8/int4 P and V codes, fp64 accumulators",
+            "data": "synthetic N(0,1) Q/K/V (reference MT19937-64 Box-Muller stream), reference gen_mask masks",
+            "config": bench_config(args.config, args.mask_family, r["all_masks"], world),
             "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+            "cpu": r["cpu"], "heads_per_step": r["heads_per_step"],
             "e2e": {"value": r["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line))
@@ -436,16 +519,13 @@ def main():
 
     my_heads = shard_heads(H, world, rank)  # no data-path collective
     hpr = len(my_heads)
-    orders_all = head_orders(paro, g, H)
-    q, k, v, masks = build_inputs(paro, my_heads, N, d, density, args.mask_family)
+    my_orders, q, k, v, masks = workload_ours(paro, ctx, my_heads, grid_text, N, d, density, args.mask_family)
+    all_ms, _ = ctx.gen_mask(np.stack([head_sums(h, kb, density, args.mask_family) for h in range(H)]), density, 64)
+    all_masks = np.stack([m.bits for m in all_ms])
     my_ops = sum(kept_ops(masks[i], N, d) for i in range(hpr))
-    total_ops = my_ops
-    if dist:
-        t = torch.tensor([my_ops], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        total_ops = float(t.item())
+    total_ops = sum(kept_ops(all_masks[h], N, d) for h in range(H))
 
-    layer = paro.Layer(ctx, hpr, d, g, [orders_all[h] for h in my_heads], dense_prefix=args.dense_prefix)
+    layer = paro.Layer(ctx, hpr, d, g, my_orders, dense_prefix=args.dense_prefix)
     if args.rope:  # diffusers-style real tables, one row per grid token (L2-resident across heads)
         ang = np.repeat(np.arange(g.token_count(), dtype=np.float64)[:, None]
                         * (10000.0 ** (-np.arange(d // 2) / (d // 2)))[None, :], 2, axis=1)
@@ -546,10 +626,9 @@ def main():
     k3_tops = my_ops / (k3_ms * 1e-3) / 1e12
     k1_bytes = hpr * (3 * N * d * 4 + 3 * kb * 64 * d + kb * (4 + d) * 4 + kb * 4 * (d // 64))
     k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
-    density_kept = float(np.mean([m.mean() for m in masks]))
 
     line = {
-        "metric": "PARO attn ms/layer + effective INT8 TOPS (CogVideoX N=17550, 48h)",
+        "metric": METRIC,
         "value": total_ops / (ms_step * 1e-3) / 1e12,
         "unit": "TOPS",
         "n_gpus": world,
@@ -561,15 +640,8 @@ def main():
         "vs_baseline": None,
         "dtype": "int8",
         "dtype_detail": "QK s8*s8->s32 and PV u8(u4 codes)*s8->s32 on tcgen05; fp32 softmax / dequant, fp64 row extremes",
-        "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), gen_mask masks",
-        "config": {
-            "workload": desc, "grid": grid_text, "heads": H, "tokens": N, "head_dim": d, "density": density,
-            "kept_density": round(density_kept, 5), "pv_bits": pv_bits, "mask_family": args.mask_family,
-            **({"dense_prefix": args.dense_prefix} if args.dense_prefix else {}),
-            **({"rope": "fused into K1 (cos/sin tables read per row)"} if args.rope else {}),
-            "parallelism": f"head-shard x{world} (no data-path collective)",
-            "l2": f"inputs {3 * q.nbytes * world / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-        },
+        "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), K5 gen_mask masks (GPU)",
+        "config": bench_config(args.config, args.mask_family, all_masks, world, args.dense_prefix, args.rope),
         "ms_per_layer": ms_step,
         "kernels_ms": {"k2_mask_lists": k2_ms, "k1_reorder_quantize": k1_ms, "k3_attention": k3_ms},
         "roofline": {
@@ -593,12 +665,12 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
-            cb = cpu_reference_sample(args.config, args.cpu_threads)
+            cb = reference_run(args.config, args.mask_family, args.cpu_threads, 1, 0)
         except Exception as ex:  # the baseline must not kill the bench line
             cb = {"error": str(ex)}
         if cb is not None:
-            line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample") if k_ in cb} \
-                if "error" not in cb else cb
+            line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample", "cpu")
+                                    if k_ in cb} if "error" not in cb else cb
     if rank == 0:
         print(json.dumps(line))
     layer.close()

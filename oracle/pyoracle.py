@@ -405,6 +405,13 @@ class Reference:
                                    _ptr(out))
         return out
 
+    def synth_randn_streams(self, seed0, stride, nstreams, count, threads=0):
+        """[nstreams, count] N(0,1) values, stream s seeded seed0 + stride*s (synth.cpp:20-22, 173-182)."""
+        out = np.empty((nstreams, count), np.float32)
+        self.lib.ref_synth_randn_streams(ctypes.c_uint64(seed0), ctypes.c_uint64(stride), SZ(nstreams), SZ(count),
+                                         ctypes.c_int(threads or os.cpu_count() or 1), _ptr(out))
+        return out
+
     def test_values(self, state, count):
         out = np.empty(count, np.float32)
         self.lib.ref_test_values(ctypes.c_uint64(state), SZ(count), _ptr(out))

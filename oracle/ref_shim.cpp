@@ -305,6 +305,38 @@ void ref_test_values(uint64_t state, size_t count, float* out) {
         out[i] = oracle::test_value(state);
 }
 
+// N(0,1) stream of the reference's synthetic generator: std::mt19937_64 seeded
+// with `seed`, the documented uniform (rng() >> 11) * 2^-53 (synth.cpp:20-22) and
+// Box-Muller on (1 - u1, u2), one value per pair (synth.cpp:173-182; that
+// function's unit_uniform is file-local, so its two lines are restated here).
+// `count` values per stream, `nstreams` streams with seeds seed0 + stride * s,
+// generated on `threads` host threads -- bench.py's reference arm builds its
+// inputs with this, never with the product library.
+void ref_synth_randn_streams(uint64_t seed0, uint64_t stride, size_t nstreams, size_t count, int threads,
+                             float* out) {
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+        for (;;) {
+            const size_t s = next.fetch_add(1);
+            if (s >= nstreams)
+                break;
+            std::mt19937_64 rng(seed0 + stride * s);
+            auto unit = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+            float* o = out + s * count;
+            for (size_t i = 0; i < count; ++i) {
+                const double u1 = 1.0 - unit();
+                const double u2 = unit();
+                o[i] = static_cast<float>(std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2));
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t)
+        pool.emplace_back(worker);
+    for (auto& th : pool)
+        th.join();
+}
+
 // synth.cpp:136-184 gen_attention_inputs (spec: grid text, weights per axis)
 int ref_gen_attention_inputs(const char* grid_text, const float* weights, float bandwidth, float noise, uint64_t seed,
                              size_t head_dim, float* q, float* k, float* v) {
