@@ -103,12 +103,6 @@ int paro_quant_encode(unsigned bits, int mode, int grouping, uint32_t block, uin
 int paro_quant_decode(const uint8_t* data, size_t size, paro_quant_header* header, int32_t* codes, float* scales,
                       float* offsets);
 
-/* gen_mask(sums, density, block, guard) -- host restatement of the offline mask
- * producer paro::gen_mask (mask.cpp:56-130), used to build bench/demo masks.
- * sums: k_rows*k_cols doubles; bits: k_rows*k_cols bytes out. */
-int paro_gen_mask(const double* sums, uint32_t k_rows, uint32_t k_cols, double density, uint32_t block,
-                  uint32_t guard_blocks, uint8_t* bits, uint32_t* repaired_rows);
-
 /* ---------------------------------------------------------------------------
  * Mask producer on the GPU. Device pointers; the
  * calls validate like the reference and return its error classes.
@@ -237,7 +231,10 @@ int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uin
  * inputs first and calling the layer without it (tests/test_gpu_parity.py). */
 int paro_layer_set_rope(paro_layer* layer, paro_stream_t stream, const float* cos, const float* sin);
 
-/* K1: permuted gather + per-block quantization into layer-owned buffers. */
+/* K1: permuted gather + per-block quantization into layer-owned buffers (with a
+ * dense prefix also K4a: the bf16 hi/lo V^T tiles of the dense path). Q/K/V are
+ * read only by the kernels queued here: once they have run on `stream` the caller
+ * may free or reuse them -- attention works from the layer-owned buffers alone. */
 int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,
                                 const float* v, int v_bits);
 
@@ -299,6 +296,23 @@ int paro_layer_debug_qk(paro_layer* layer, paro_stream_t stream, uint32_t n_tile
 
 /* Launch accounting: number of kernels the last forward launched, and the
  * last K3 kernel's grid size. */
+/* Test hook: K1's quantizer arithmetic (reciprocal + FMA-residual quotient, no
+ * clamp) vs the reference quant_affine (IEEE x/scale, clamp, round half away) for
+ * every amax bit pattern in [bits_begin, bits_begin + bits_count) (finite), x =
+ * +-amax and nx pseudo-random |x| <= amax, qmax 127 and 7. *mismatches = count;
+ * first[5] = (amax bits, x bits, qmax, K1 code, reference code) of the first. */
+int paro_debug_k1_quant_proof(paro_ctx* ctx, uint32_t bits_begin, uint64_t bits_count, uint32_t nx, uint32_t seed,
+                              uint64_t* mismatches, uint32_t* first);
+
+/* Test hook: runs K3 (as paro_layer_attention, output discarded) and returns the
+ * FINAL P codes of every quantized tile of the n_targets (head, q-block) pairs
+ * (targets: 2*n u32), in each q-block's kept order: codes [n][kb][64][64] (rows x
+ * key columns; a tail tile's padded columns are 0 in the reference), meta
+ * [n][kb][4] = (lo, pscale, key block, 1) per tile (attention.cpp:201-228);
+ * unused tile slots are zero. Host pointers; synchronises. */
+int paro_layer_debug_pdump(paro_layer* layer, paro_stream_t stream, float scale, int pv_bits, uint32_t n_targets,
+                           const uint32_t* targets, uint8_t* codes, float* meta);
+
 int paro_layer_last_launches(const paro_layer* layer, int* kernels);
 
 #ifdef __cplusplus

@@ -217,9 +217,20 @@ static double dot_f(const float* a, const float* b, size_t n) {
 
 /* Rows of q-blocks [qb_begin, qb_end) only (the engine is independent per
  * q-tile, attention.cpp:134); other output rows are left untouched. */
-int oracle_stream_engine_range(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
-                               size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode,
-                               size_t qb_begin, size_t qb_end, float* out, uint8_t* zeroed) {
+/* Optional P-code dump of the quantized tiles of one q-block (test hook): per
+ * kept tile in the engine's order, the key block, the group's (lo, pscale) and
+ * the codes [block][block] (rows x true key columns, row-major, rest 0). */
+typedef struct {
+    size_t qb, max_tiles, ntiles;
+    uint8_t* codes;
+    float* lo;
+    float* pscale;
+    int32_t* bj;
+} pdump_t;
+
+static int engine_impl(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
+                       size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode,
+                       size_t qb_begin, size_t qb_end, float* out, uint8_t* zeroed, pdump_t* dump) {
     if (n == 0 || d == 0 || block < 1)
         return ORACLE_CONFIG;
     if (dense_prefix > n)
@@ -350,11 +361,23 @@ int oracle_stream_engine_range(const float* q, const float* k, const float* v, s
                 if (pscale == 0.0f)
                     pscale = 1.0f;
                 const float poffset = mn;
+                uint8_t* dcodes = NULL;
+                if (dump && qb == dump->qb && dump->ntiles < dump->max_tiles) {
+                    const size_t t = dump->ntiles++;
+                    dump->lo[t] = poffset;
+                    dump->pscale[t] = pscale;
+                    dump->bj[t] = (int32_t)bj;
+                    dcodes = dump->codes + t * block * block;
+                    memset(dcodes, 0, block * block);
+                }
                 for (size_t r = 0; r < qn; ++r) {
                     const size_t i = qs0 + r;
                     if (i < dp || (!tile_kept && i >= dp))
                         continue;
                     k_quant_affine(ptile + r * kn, kn, poffset, pscale, 0, (int32_t)qmax, pcodes);
+                    if (dcodes)
+                        for (size_t j = 0; j < kn; ++j)
+                            dcodes[r * block + j] = (uint8_t)pcodes[j];
                     const double ss = (double)pscale * (double)vscale[bj];
                     const double os = (double)poffset * (double)vscale[bj];
                     for (size_t c = 0; c < d; ++c) {
@@ -392,6 +415,25 @@ int oracle_stream_engine_range(const float* q, const float* k, const float* v, s
     free(vscale);
     free(vcolsum);
     return ORACLE_OK;
+}
+
+int oracle_stream_engine_range(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
+                               size_t dense_prefix, size_t block, const uint8_t* mask, int pv_bits, int qk_mode,
+                               size_t qb_begin, size_t qb_end, float* out, uint8_t* zeroed) {
+    return engine_impl(q, k, v, n, d, scale_in, dense_prefix, block, mask, pv_bits, qk_mode, qb_begin, qb_end, out,
+                       zeroed, NULL);
+}
+
+/* q-block qb's output rows plus its P-code dump (codes [max_tiles][block][block],
+ * lo / pscale / bj [max_tiles]); returns the number of quantized tiles in *ntiles */
+int oracle_stream_engine_pdump(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,
+                               size_t block, const uint8_t* mask, int pv_bits, size_t qb, size_t max_tiles,
+                               uint8_t* codes, float* lo, float* pscale, int32_t* bj, size_t* ntiles, float* out,
+                               uint8_t* zeroed) {
+    pdump_t dmp = {qb, max_tiles, 0, codes, lo, pscale, bj};
+    const int rc = engine_impl(q, k, v, n, d, scale_in, 0, block, mask, pv_bits, 1, qb, qb + 1, out, zeroed, &dmp);
+    *ntiles = dmp.ntiles;
+    return rc;
 }
 
 int oracle_stream_engine(const float* q, const float* k, const float* v, size_t n, size_t d, float scale_in,

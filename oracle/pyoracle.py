@@ -124,6 +124,35 @@ class Oracle:
         r0, r1 = qb_begin * 64, min(n, qb_end * 64)
         return out[r0:r1], zeroed[r0:r1].astype(bool)
 
+    def pdump(self, q, k, v, qb, mask=None, pv_bits=8, scale=0.0):
+        """q-block qb of the INT8-QK engine with its P-code dump: (out rows, zeroed,
+        bj[t], lo[t], pscale[t], codes[t][64][64]) for its quantized tiles in order."""
+        q = np.ascontiguousarray(q, np.float32)
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        n, d = q.shape
+        kb = (n + 63) // 64
+        out = np.zeros((n, d), np.float32)
+        zeroed = np.zeros(n, np.uint8)
+        codes = np.zeros((kb, 64, 64), np.uint8)
+        lo = np.zeros(kb, np.float32)
+        ps = np.zeros(kb, np.float32)
+        bj = np.zeros(kb, np.int32)
+        nt = SZ()
+        mp = None
+        if mask is not None:
+            mask = np.ascontiguousarray(mask, np.uint8)
+            mp = _ptr(mask)
+        rc = self.lib.oracle_stream_engine_pdump(_ptr(q), _ptr(k), _ptr(v), SZ(n), SZ(d), ctypes.c_float(scale),
+                                                 SZ(64), mp, ctypes.c_int(pv_bits), SZ(qb), SZ(kb), _ptr(codes),
+                                                 _ptr(lo), _ptr(ps), _ptr(bj), ctypes.byref(nt), _ptr(out),
+                                                 _ptr(zeroed))
+        if rc:
+            raise ValueError(f"oracle_stream_engine_pdump rc={rc}")
+        t = nt.value
+        r0, r1 = qb * 64, min(n, qb * 64 + 64)
+        return out[r0:r1], zeroed[r0:r1].astype(bool), bj[:t], lo[:t], ps[:t], codes[:t]
+
     def paro_head(self, q, k, v, fwd, inv, mask=None, pv_bits=8, qk_mode=1, scale=0.0):
         """cmd_run's chain for one head (main.cpp:276-305). zeroed in PERMUTED order."""
         q = np.ascontiguousarray(q, np.float32)

@@ -15,7 +15,7 @@ like the reference's own tests:
   quantize {Symmetric, PerBlock, 64} (quant.hpp)  Context.quantize          [GPU]
   BlockMask / (de)serialize_mask (mask.hpp)       BlockMask / (de)serialize_mask
   MaskSchedule::at / load_schedule                schedule_at
-  gen_mask (mask.hpp:47)                          gen_mask
+  gen_mask / build_schedule (mask.hpp:47-60)      Context.gen_mask / build_schedule [GPU]
   quantized_blocked_attention (attention.hpp:52)  Context.quantized_blocked_attention [GPU]
   cmd_run's per-head chain, H heads (main.cpp)    Layer                     [GPU]
   save/load_tensor PAT1 (tensor_io.hpp)          encode_tensor / decode_tensor / load_matrix
@@ -256,17 +256,6 @@ def schedule_at(data: bytes, t: int) -> BlockMask:
     _check(_lib.paro_schedule_at(P(_ptr(buf)), SZ(len(data)), U32(t), ctypes.byref(kr), ctypes.byref(kc),
                                  ctypes.byref(b), P(_ptr(bits))))
     return BlockMask(kr.value, kc.value, b.value, bits)
-
-
-def gen_mask(sums: np.ndarray, density: float, block: int, guard_blocks: int = 0):
-    """Returns (BlockMask, repaired_rows) (mask.cpp:56-130)."""
-    s = np.ascontiguousarray(sums, np.float64)
-    kr, kc = s.shape
-    bits = np.empty((kr, kc), np.uint8)
-    rep = U32()
-    _check(_lib.paro_gen_mask(P(_ptr(s)), U32(kr), U32(kc), ctypes.c_double(density), U32(block), U32(guard_blocks),
-                              P(_ptr(bits)), ctypes.byref(rep)))
-    return BlockMask(kr, kc, block, bits), rep.value
 
 
 def synth_randn(seed: int, count: int) -> np.ndarray:
@@ -542,6 +531,15 @@ class Context:
         _close(dm, dinv, ds)
         return out
 
+    def k1_quant_proof(self, bits_begin: int, bits_count: int, nx: int = 14, seed: int = 1):
+        """Test hook: K1's quantizer vs the reference quant_affine over amax bit patterns
+        (paro_debug_k1_quant_proof) -> (mismatches, first mismatch record or None)."""
+        bad = ctypes.c_uint64()
+        first = (U32 * 5)()
+        _check(_lib.paro_debug_k1_quant_proof(P(self.ptr), U32(bits_begin), ctypes.c_uint64(bits_count), U32(nx),
+                                              U32(seed), ctypes.byref(bad), first))
+        return bad.value, (tuple(first) if bad.value else None)
+
     def gen_mask(self, sums: np.ndarray, density: float, block: int, guard_blocks: int = 0):
         """gen_mask on the GPU for one [k, k] grid or a stack [count, k, k]
         (mask.cpp:56-130). Returns (BlockMask | list[BlockMask], repaired rows)."""
@@ -799,6 +797,12 @@ class Layer:
         _check(_lib.paro_layer_mask_stats(P(self.ptr), P(_ptr(kept)), ctypes.byref(tot)))
         return kept, tot.value
 
+    def debug_pdump(self, targets, scale: float = 0.0, pv_bits: int = 8):
+        """Final P codes of each (head, q-block) in `targets` after K3 (test hook):
+        codes [n][kb][64][64] and meta [n][kb][4] = (lo, pscale, key block, 1) per
+        quantized tile in kept order (paro_layer_debug_pdump)."""
+        return _pdump(self, targets, scale, pv_bits)
+
     def debug_qk(self, tiles: np.ndarray) -> np.ndarray:
         """int32 S_g of (h, qb, bj) tiles through K3's tcgen05 QK path -> [n, G, 64, 64]."""
         t = np.ascontiguousarray(tiles, np.uint32).reshape(-1, 3)
@@ -810,6 +814,16 @@ class Layer:
         out = ds.download((t.shape[0], G, 64, 64), np.int32)
         _close(dt, ds)
         return out
+
+
+def _pdump(layer, targets, scale, pv_bits):
+    t = np.ascontiguousarray(targets, np.uint32).reshape(-1, 2)
+    n = t.shape[0]
+    codes = np.zeros((n, layer.kb, 64, 64), np.uint8)
+    meta = np.zeros((n, layer.kb, 4), np.float32)
+    _check(_lib.paro_layer_debug_pdump(P(layer.ptr), None, ctypes.c_float(scale), ctypes.c_int(pv_bits), U32(n),
+                                       P(_ptr(t)), P(_ptr(codes)), P(_ptr(meta))))
+    return codes, meta
 
 
 def stream_sync(stream=None) -> None:

@@ -213,7 +213,21 @@ struct K3Params {
     uint32_t n_items;
     uint32_t* work_counter; // next index into `order` (zeroed before the launch; DYNAMIC)
     unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
+    K3Dump dump;               // P-code dump test hook (dump.slot == nullptr: off)
 };
+
+// P-code dump of one row's final codes for step t (cols [c0, c0 + 16*nch) of the
+// row's 64 key columns; 64B-swizzled P tile rows as written by quantize_store)
+__device__ __forceinline__ void dump_row(const K3Dump& dm, int32_t slot, uint32_t t, uint32_t r, const uint8_t* prow,
+                                         int c0chunk, int nch) {
+    uint8_t* dst = dm.codes + (((size_t)slot * dm.kb + t) * 64 + r) * 64;
+    for (int c = c0chunk; c < c0chunk + nch; ++c)
+        *reinterpret_cast<uint4*>(dst + 16 * c) = *reinterpret_cast<const uint4*>(prow + ((c ^ ((r >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void dump_meta(const K3Dump& dm, int32_t slot, uint32_t t, float lo, float pscale,
+                                          uint32_t bj) {
+    *reinterpret_cast<float4*>(dm.meta + ((size_t)slot * dm.kb + t) * 4) = make_float4(lo, pscale, (float)bj, 1.f);
+}
 
 struct Item {
     uint32_t h, qa, qb, na, nb, n; // qb = 0xffff when the pair has no B
@@ -1220,6 +1234,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 st.l = L.init_l[srow];
             }
             RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
+            const int32_t dslot = P.dump.slot && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
                 const bool live = t < nmine;
@@ -1247,6 +1262,11 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                 gamma, lo, pscale, 0u, nullptr,
                                 reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 2) * 512, bar(BR::RED),
                                 T & 1, prof);
+                if (dslot >= 0 && live) {
+                    dump_row(P.dump, dslot, t, r, prow, 0, 4);
+                    if (r == 0)
+                        dump_meta(P.dump, dslot, t, lo, pscale, bj);
+                }
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1462,6 +1482,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 for (int c = 0; c < DH / 2; ++c)
                     acc[c] = pk(a0[c].x, a0[c].y);
             }
+            const int32_t dslot = P.dump.slot && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             // acc = gamma * acc + (pscale * vscale) * ip + u_c over this warp's O columns,
             // for step U (its P side was published before this warp's own PFULL arrive)
             auto dequant = [&](uint32_t U) {
@@ -1533,6 +1554,11 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                       reinterpret_cast<float4*>(smem + C::OFF_XCH),
                                       reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512,
                                       bar(BR::RED), T & 1, prof);
+                if (dslot >= 0 && live) {
+                    dump_row(P.dump, dslot, t, r, prow, (int)half * 2, 2);
+                    if (r == 0 && half == 0)
+                        dump_meta(P.dump, dslot, t, lo, pscale, bj);
+                }
                 PROF_T(tw2);
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1698,7 +1724,7 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
-                      uint32_t head_begin, uint32_t head_count, bool chunked) {
+                      uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump) {
     if (head_count == 0)
         return cudaSuccess;
     K3Params p;
@@ -1711,6 +1737,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
     p.order = (chunked ? L.order_chunk : L.order) + (size_t)head_begin * L.np;
     p.n_items = head_count * L.np;
     p.stats = nullptr;
+    p.dump = dump ? *dump : K3Dump{nullptr, nullptr, nullptr, 0};
     p.work_counter = L.work_counter;
     if (PARO_DYNAMIC) {
         const cudaError_t e = cudaMemsetAsync(L.work_counter, 0, sizeof(uint32_t), st);

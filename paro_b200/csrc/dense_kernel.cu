@@ -125,7 +125,7 @@ __device__ __forceinline__ double k4_exact(double scale64, const double (&a)[G],
 }
 
 template <int D>
-__global__ void __launch_bounds__(128) k4_dense(LayerDev L, const float* __restrict__ v, double scale64,
+__global__ void __launch_bounds__(128) k4_dense(LayerDev L, double scale64,
                                                 float* __restrict__ out, uint8_t* __restrict__ zeroed,
                                                 uint32_t head_begin) {
     using C = K4Cfg<D>;
@@ -508,26 +508,34 @@ void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_
     cb = (kb + ch - 1) / ch;
 }
 
-cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
-                      uint32_t head_begin, uint32_t head_count, cudaStream_t st) {
+// K4a: the dense-prefix path's bf16 hi/lo V^T tiles, split from the fp32 V at
+// reorder_quantize time (so attention never reads the caller's fp32 V)
+cudaError_t launch_k4a(const LayerDev& L, const float* v, uint32_t head_begin, uint32_t head_count, cudaStream_t st) {
     if (L.dp == 0 || head_count == 0)
         return cudaSuccess;
-    const dim3 grid(L.nd * L.k4_cb + (L.kb - L.nd), head_count);
-    const dim3 cgrid(L.nd, head_count);
     const dim3 vgrid(L.kb, head_count);
     if (L.D == 64)
         k4_vsplit<64><<<vgrid, 256, 0, st>>>(L, v, head_begin);
     else
         k4_vsplit<128><<<vgrid, 256, 0, st>>>(L, v, head_begin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k4(const LayerDev& L, double scale, float* out, uint8_t* zeroed, uint32_t head_begin,
+                      uint32_t head_count, cudaStream_t st) {
+    if (L.dp == 0 || head_count == 0)
+        return cudaSuccess;
+    const dim3 grid(L.nd * L.k4_cb + (L.kb - L.nd), head_count);
+    const dim3 cgrid(L.nd, head_count);
     if (L.D == 64) {
         constexpr size_t smem = K4Cfg<64>::SMEM;
         cudaFuncSetAttribute(k4_dense<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k4_dense<64><<<grid, 128, smem, st>>>(L, v, scale, out, zeroed, head_begin);
+        k4_dense<64><<<grid, 128, smem, st>>>(L, scale, out, zeroed, head_begin);
         k4_combine<64><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
     } else {
         constexpr size_t smem = K4Cfg<128>::SMEM;
         cudaFuncSetAttribute(k4_dense<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k4_dense<128><<<grid, 128, smem, st>>>(L, v, scale, out, zeroed, head_begin);
+        k4_dense<128><<<grid, 128, smem, st>>>(L, scale, out, zeroed, head_begin);
         k4_combine<128><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
     }
     return cudaGetLastError();

@@ -40,14 +40,17 @@ cudaError_t launch_late_mean(const double* sums, uint32_t T, size_t total, doubl
 cudaError_t launch_block_terms(const double* sums, const float* maxs, const uint32_t* counts, uint32_t k, uint32_t n,
                                uint32_t block, float sigma, double* terms, uint32_t* sparse, cudaStream_t st);
 void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_t& ch);
-cudaError_t launch_k4(const LayerDev& L, const float* v, double scale, float* out, uint8_t* zeroed,
+cudaError_t launch_k4a(const LayerDev& L, const float* v, uint32_t head_begin, uint32_t head_count, cudaStream_t st);
+cudaError_t launch_k4(const LayerDev& L, double scale, float* out, uint8_t* zeroed,
                       uint32_t head_begin, uint32_t head_count, cudaStream_t st);
 cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
                                     float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
-                      uint32_t head_begin, uint32_t head_count, bool chunked);
+                      uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump = nullptr);
+cudaError_t launch_k1_quant_proof(uint32_t lo, uint32_t count, uint32_t nx, uint32_t seed, unsigned long long* bad,
+                                  uint32_t* first, int num_sms, cudaStream_t st);
 cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
                             const uint32_t* tiles, int32_t* S, cudaStream_t st);
 } // namespace paro
@@ -291,7 +294,6 @@ struct paro_layer {
     bool masks_set = false;
     int last_v_bits = 0;
     int last_launches = 0;
-    const float* last_v = nullptr; // fp32 V of the last reorder_quantize (K4 reads the dense tiles)
     CUtensorMap tm_q, tm_k, tm_v;
     // e2e staging
     float* rope = nullptr; // [2][N - dp][D]: cos, sin (paro_layer_set_rope)
@@ -423,7 +425,8 @@ void check_layer(const paro_layer* l) {
 }
 
 void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, float* out, uint8_t* zeroed,
-                   uint32_t head_begin = 0, uint32_t head_count = ~0u, bool chunked = false) {
+                   uint32_t head_begin = 0, uint32_t head_count = ~0u, bool chunked = false,
+                   const paro::K3Dump* dump = nullptr) {
     check_bits(pv_bits);
     if (!l->masks_set)
         fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before attention");
@@ -437,12 +440,10 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
     if (head_count == ~0u)
         head_count = l->L.H;
     if (l->L.dp) { // dense text-token prefix: dense rows done, the others' state for K3
-        if (!l->last_v)
-            fail(PARO_E_CONFIG, "dense prefix: reorder_quantize must run before attention");
-        cuda_check(paro::launch_k4(l->L, l->last_v, eff, out, zeroed, head_begin, head_count, st), "k4 launch");
+        cuda_check(paro::launch_k4(l->L, eff, out, zeroed, head_begin, head_count, st), "k4 launch");
     }
     cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
-                               head_begin, head_count, chunked),
+                               head_begin, head_count, chunked, dump),
                "k3_attention launch");
 }
 
@@ -550,10 +551,9 @@ int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_r
         for (uint32_t i = 0; i < nd; ++i) {
             if (size < off + 4)
                 fail(PARO_E_FORMAT, "truncated distinct entry (schedule parse position " + std::to_string(off) + ")");
-            const uint32_t ti = get_u32(data + off);
-            off += 4;
+            off += 4; // the stored timestep field: at(t) ignores it and takes distinct[t] by position
             const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
-            if (ti == t && t < T / 2) {
+            if (i == t) {
                 want = data + off;
                 want_size = used;
             }
@@ -783,85 +783,6 @@ int paro_quant_decode(const uint8_t* p, size_t size, paro_quant_header* hdr, int
         hdr->rows = rows;
         hdr->cols = cols;
         hdr->groups = ng;
-    });
-}
-
-int paro_gen_mask(const double* sums, uint32_t kr, uint32_t kc, double density, uint32_t block, uint32_t guard,
-                  uint8_t* bits, uint32_t* repaired_rows) {
-    return guarded([&] {
-        // gen_mask (mask.cpp:56-130)
-        if (!(density > 0.0 && density <= 1.0))
-            fail(PARO_E_CONFIG, "density must be in (0,1], got " + std::to_string(density));
-        const size_t total = (size_t)kr * kc;
-        const size_t target = (size_t)std::ceil(density * (double)total);
-        auto guarded_blk = [&](size_t i, size_t j) { return i < guard || j < guard; };
-        size_t guard_count = 0;
-        if (guard > 0) {
-            const size_t gr = std::min<size_t>(guard, kr), gc = std::min<size_t>(guard, kc);
-            guard_count = total - (kr - gr) * (kc - gc);
-        }
-        if (guard_count > target)
-            fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
-                                    " blocks but the dense prefix alone occupies " + std::to_string(guard_count));
-        if (guard == 0 && target < kr)
-            fail(PARO_E_CONFIG, "density " + std::to_string(density) + " keeps " + std::to_string(target) +
-                                    " blocks, fewer than the " + std::to_string(kr) + " rows that each need one");
-        struct Ref {
-            double sum;
-            uint32_t row, col;
-        };
-        std::vector<Ref> cand;
-        cand.reserve(total - guard_count);
-        for (uint32_t i = 0; i < kr; ++i)
-            for (uint32_t j = 0; j < kc; ++j)
-                if (!guarded_blk(i, j))
-                    cand.push_back({sums[(size_t)i * kc + j], i, j});
-        // keep-preference: larger sum, then smaller (row, col) -- a strict total order
-        std::sort(cand.begin(), cand.end(), [](const Ref& a, const Ref& b) {
-            if (a.sum != b.sum)
-                return a.sum > b.sum;
-            if (a.row != b.row)
-                return a.row < b.row;
-            return a.col < b.col;
-        });
-        std::memset(bits, 0, total);
-        for (size_t i = 0; i < kr; ++i)
-            for (size_t j = 0; j < kc; ++j)
-                if (guarded_blk(i, j))
-                    bits[i * kc + j] = 1;
-        for (size_t c = 0; c < target - guard_count; ++c)
-            bits[(size_t)cand[c].row * kc + cand[c].col] = 1;
-        std::vector<size_t> row_kept(kr, 0);
-        for (size_t i = 0; i < kr; ++i)
-            for (size_t j = 0; j < kc; ++j)
-                row_kept[i] += bits[i * kc + j];
-        uint32_t repaired = 0;
-        for (size_t i = 0; i < kr; ++i) {
-            if (row_kept[i] > 0)
-                continue;
-            size_t best = 0;
-            for (size_t j = 1; j < kc; ++j)
-                if (sums[i * kc + j] > sums[i * kc + best])
-                    best = j;
-            bits[i * kc + best] = 1;
-            ++row_kept[i];
-            ++repaired;
-            bool dropped = false;
-            for (size_t c = cand.size(); c-- > 0;) {
-                const Ref& cb = cand[c];
-                if (bits[(size_t)cb.row * kc + cb.col] && row_kept[cb.row] >= 2) {
-                    bits[(size_t)cb.row * kc + cb.col] = 0;
-                    --row_kept[cb.row];
-                    dropped = true;
-                    break;
-                }
-            }
-            if (!dropped)
-                fail(PARO_E_CONFIG, "cannot repair empty mask row " + std::to_string(i) + " at density " +
-                                        std::to_string(density));
-        }
-        if (repaired_rows)
-            *repaired_rows = repaired;
     });
 }
 
@@ -1377,7 +1298,7 @@ int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const f
             fail(PARO_E_CONFIG, "null Q/K/V");
         set_device(layer->ctx);
         cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, 0, layer->L.H, (cudaStream_t)stream), "k1 launch");
-        layer->last_v = v;
+        cuda_check(paro::launch_k4a(layer->L, v, 0, layer->L.H, (cudaStream_t)stream), "k4a launch");
         layer->last_v_bits = v_bits;
     });
 }
@@ -1401,8 +1322,8 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
         set_device(layer->ctx);
         cudaStream_t st = (cudaStream_t)stream;
         cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, 0, layer->L.H, st), "k1 launch");
+        cuda_check(paro::launch_k4a(layer->L, v, 0, layer->L.H, st), "k4a launch");
         layer->last_v_bits = pv_bits;
-        layer->last_v = v;
         run_attention(layer, st, scale, pv_bits, out, zeroed);
         layer->last_launches = 2;
     });
@@ -1459,13 +1380,14 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
             layer->ev.push_back(e);
         }
         cudaEvent_t* ev = layer->ev.data();
-        // uploads start at once: the staging buffers are idle (every forward_host
-        // returns synchronised) and nothing queued on the caller's stream (K2 of
-        // set_masks) feeds them; K1/K3 of each chunk still run on that stream after it
+        // stream order: the uploads (s_in) and downloads (s_out) start after the work
+        // already queued on the caller's stream -- it may still be writing the pinned
+        // host inputs (an async D2H into q/k/v) or reading the staging buffers; K1/K3
+        // of each chunk run on that stream
         cuda_check(cudaEventRecord(ev[0], st), "event record");
+        cuda_check(cudaStreamWaitEvent(layer->s_in, ev[0], 0), "stream wait");
         cuda_check(cudaStreamWaitEvent(layer->s_out, ev[0], 0), "stream wait");
         layer->last_v_bits = pv_bits;
-        layer->last_v = layer->dv;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t h0 = L.chunk_start[c], hn = L.chunk_start[c + 1] - h0;
             const size_t off = (size_t)h0 * head_elems, bytes = (size_t)hn * head_elems * 4;
@@ -1476,6 +1398,7 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
             cuda_check(cudaEventRecord(e_in, layer->s_in), "event record");
             cuda_check(cudaStreamWaitEvent(st, e_in, 0), "stream wait");
             cuda_check(paro::launch_k1(L, layer->dq, layer->dk, layer->dv, pv_bits, h0, hn, st), "k1 launch");
+            cuda_check(paro::launch_k4a(L, layer->dv, h0, hn, st), "k4a launch");
             run_attention(layer, st, scale, pv_bits, layer->dout, zeroed ? layer->dzero : nullptr, h0, hn, true);
             cuda_check(cudaEventRecord(e_k, st), "event record");
             cuda_check(cudaStreamWaitEvent(layer->s_out, e_k, 0), "stream wait");
@@ -1596,6 +1519,83 @@ int paro_layer_debug_qk(paro_layer* layer, paro_stream_t stream, uint32_t n_tile
         set_device(layer->ctx);
         cuda_check(paro::launch_debug_qk(layer->L, layer->tm_q, layer->tm_k, n_tiles, tiles, S, (cudaStream_t)stream),
                    "debug_qk launch");
+    });
+}
+
+int paro_debug_k1_quant_proof(paro_ctx* ctx, uint32_t bits_begin, uint64_t bits_count, uint32_t nx, uint32_t seed,
+                              uint64_t* mismatches, uint32_t* first) {
+    return guarded([&] {
+        if (!ctx || !mismatches)
+            fail(PARO_E_CONFIG, "null argument");
+        if ((uint64_t)bits_begin + bits_count > 0x7f800000ull)
+            fail(PARO_E_CONFIG, "amax bit patterns must be finite (< 0x7f800000)");
+        set_device(ctx);
+        unsigned long long* dbad = dalloc<unsigned long long>(1);
+        uint32_t* dfirst = dalloc<uint32_t>(5);
+        struct Free {
+            void* p[2];
+            ~Free() {
+                for (void* x : p)
+                    cudaFree(x);
+            }
+        } guard{{dbad, dfirst}};
+        cuda_check(cudaMemset(dbad, 0, 8), "memset");
+        cuda_check(cudaMemset(dfirst, 0, 20), "memset");
+        for (uint64_t off = 0; off < bits_count; off += 1ull << 30) {
+            const uint32_t n = (uint32_t)std::min<uint64_t>(1ull << 30, bits_count - off);
+            cuda_check(paro::launch_k1_quant_proof(bits_begin + (uint32_t)off, n, nx, seed, dbad, dfirst, ctx->num_sms,
+                                                   nullptr),
+                       "k1 quant proof");
+        }
+        cuda_check(cudaDeviceSynchronize(), "k1 quant proof sync");
+        unsigned long long h = 0;
+        cuda_check(cudaMemcpy(&h, dbad, 8, cudaMemcpyDeviceToHost), "D2H");
+        *mismatches = h;
+        if (first)
+            cuda_check(cudaMemcpy(first, dfirst, 20, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int paro_layer_debug_pdump(paro_layer* layer, paro_stream_t stream, float scale, int pv_bits, uint32_t n_targets,
+                           const uint32_t* targets, uint8_t* codes, float* meta) {
+    return guarded([&] {
+        check_layer(layer);
+        set_device(layer->ctx);
+        const LayerDev& L = layer->L;
+        if (n_targets == 0)
+            return;
+        if (!targets || !codes || !meta)
+            fail(PARO_E_CONFIG, "null pdump argument");
+        std::vector<int32_t> slot((size_t)L.H * L.kb2, -1);
+        for (uint32_t i = 0; i < n_targets; ++i) {
+            const uint32_t h = targets[2 * i], qb = targets[2 * i + 1];
+            if (h >= L.H || qb >= L.kb)
+                fail(PARO_E_INPUT, "pdump target (" + std::to_string(h) + ", " + std::to_string(qb) + ") out of range");
+            if (slot[(size_t)h * L.kb2 + qb] >= 0)
+                fail(PARO_E_INPUT, "pdump target listed twice");
+            slot[(size_t)h * L.kb2 + qb] = (int32_t)i;
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t ncodes = (size_t)n_targets * L.kb * 64 * 64, nmeta = (size_t)n_targets * L.kb * 4;
+        int32_t* dslot = dalloc<int32_t>(slot.size());
+        uint8_t* dcodes = dalloc<uint8_t>(ncodes);
+        float* dmeta = dalloc<float>(nmeta);
+        float* dout = dalloc<float>((size_t)L.H * L.N * L.D);
+        struct Free {
+            void* p[4];
+            ~Free() {
+                for (void* x : p)
+                    cudaFree(x);
+            }
+        } guard{{dslot, dcodes, dmeta, dout}};
+        cuda_check(cudaMemcpyAsync(dslot, slot.data(), slot.size() * 4, cudaMemcpyHostToDevice, st), "pdump H2D");
+        cuda_check(cudaMemsetAsync(dcodes, 0, ncodes, st), "pdump memset");
+        cuda_check(cudaMemsetAsync(dmeta, 0, nmeta * 4, st), "pdump memset");
+        const paro::K3Dump dm{dslot, dcodes, dmeta, L.kb};
+        run_attention(layer, st, scale, pv_bits, dout, nullptr, 0, ~0u, false, &dm);
+        cuda_check(cudaMemcpyAsync(codes, dcodes, ncodes, cudaMemcpyDeviceToHost, st), "pdump D2H");
+        cuda_check(cudaMemcpyAsync(meta, dmeta, nmeta * 4, cudaMemcpyDeviceToHost, st), "pdump D2H");
+        cuda_check(cudaStreamSynchronize(st), "pdump sync");
     });
 }
 

@@ -88,4 +88,14 @@ struct LayerDev {
 
 __host__ __device__ inline uint32_t meta_stride(uint32_t D) { return 4 + D; }
 
+// Test hook (paro_layer_debug_pdump): K3 copies the final P codes of every
+// quantized tile of the selected (head, q-block)s -- after the exact boundary
+// path -- with the tile group's (lo, pscale) and key block. slot == nullptr: off.
+struct K3Dump {
+    const int32_t* slot; // [H][kb2]: dump slot of (h, qb) or -1
+    uint8_t* codes;      // [nslot][kb][64][64] (row-major, key columns)
+    float* meta;         // [nslot][kb][4]: lo, pscale, key block, 1
+    uint32_t kb;
+};
+
 } // namespace paro

@@ -30,6 +30,8 @@ namespace paro {
 // round-down adds: floor(RD(|q| + 0.5)) == floor(|q| + 0.5), and
 // RD(t + 2^23) leaves floor(t) in the mantissa. No XU-pipe instruction.
 __device__ __forceinline__ int quant_sym(float x, float scale, float rs, float qmax) {
+    if (scale < 1.17549435e-38f) // subnormal scale: see quant_sym4
+        return (int)roundf(fminf(qmax, fmaxf(-qmax, __fdiv_rn(x, scale))));
     const float q0 = __fmul_rn(x, rs);
     const float e = __fmaf_rn(-q0, scale, x);
     float q = __fmaf_rn(e, rs, q0);
@@ -66,7 +68,23 @@ __device__ __forceinline__ int round_half_away(float q) {
     const int m = (int)(__float_as_uint(__fadd_rd(t, 8388608.0f)) & 0x7fffffu);
     return q < 0.0f ? -m : m;
 }
-__device__ __forceinline__ void quant_sym4(float4 v, float scale, float rs, int& c0, int& c1, int& c2, int& c3) {
+__device__ __forceinline__ int quant_ieee(float x, float scale, float qmax) {
+    return round_half_away(fminf(qmax, fmaxf(-qmax, __fdiv_rn(x, scale))));
+}
+__device__ __forceinline__ void quant_sym4(float4 v, float scale, float rs, float qmax, int& c0, int& c1, int& c2,
+                                           int& c3) {
+    if (scale < 1.17549435e-38f) {
+        // subnormal group scale (amax < qmax * 2^-126): RN(1/scale) overflows or is
+        // inexact enough that the residual step no longer gives RN(x/scale), so the
+        // group takes the IEEE quotient and the clamp as written (a group-uniform
+        // branch; found by the every-amax-bit-pattern proof in
+        // tests/test_gpu_fullshape_int.py)
+        c0 = quant_ieee(v.x, scale, qmax);
+        c1 = quant_ieee(v.y, scale, qmax);
+        c2 = quant_ieee(v.z, scale, qmax);
+        c3 = quant_ieee(v.w, scale, qmax);
+        return;
+    }
     const uint64_t s2 = f2pk(scale, scale), r2 = f2pk(rs, rs), ns2 = f2pk(-scale, -scale);
     float a, b, c, d;
     f2upk(quot2(f2pk(v.x, v.y), s2, r2, ns2), a, b);
@@ -223,9 +241,9 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(Laye
         const size_t off = head_codes + (size_t)(b * 64 + r0 + RPP * j) * D + c4 * 4;
         const float4 a = xq[j], c = xk[j], e = xv[j];
         int a0, a1, a2, a3, k0, k1, k2, k3, v0, v1, v2, v3;
-        quant_sym4(a, sq, rq, a0, a1, a2, a3);
-        quant_sym4(c, sk, rk, k0, k1, k2, k3);
-        quant_sym4(e, sv, rv, v0, v1, v2, v3);
+        quant_sym4(a, sq, rq, 127.0f, a0, a1, a2, a3);
+        quant_sym4(c, sk, rk, 127.0f, k0, k1, k2, k3);
+        quant_sym4(e, sv, rv, vq, v0, v1, v2, v3);
         *reinterpret_cast<uint32_t*>(L.q + off) = pack4(a0, a1, a2, a3);
         *reinterpret_cast<uint32_t*>(L.k + off) = pack4(k0, k1, k2, k3);
         *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
@@ -553,7 +571,13 @@ cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
-    k2_pair_qblocks<<<L.H, 256, (2 * L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    // dynamic smem above the 48 KB default once kb > ~6143 (N > ~393K tokens)
+    const int smem_pair = (int)((2 * L.kb + 1) * sizeof(uint32_t));
+    if (smem_pair > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(k2_pair_qblocks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair)) !=
+            cudaSuccess)
+        return e;
+    k2_pair_qblocks<<<L.H, 256, smem_pair, st>>>(L);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
@@ -561,7 +585,98 @@ cudaError_t launch_k2(const LayerDev& L, const uint8_t* bits, cudaStream_t st) {
 }
 
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st) {
-    k2_work_order<<<1 + L.nchunks, 1024, (L.kb + 1) * sizeof(uint32_t), st>>>(L);
+    const int smem = (int)((L.kb + 1) * sizeof(uint32_t));
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k2_work_order, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    k2_work_order<<<1 + L.nchunks, 1024, smem, st>>>(L);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Test hook (paro_debug_k1_quant_proof): K1's quantizer -- the reciprocal +
+// one-FMA-residual quotient and the dropped clamp of quant_sym4, and the
+// standalone quantize's quant_sym -- against the
+// reference arithmetic (kernels_scalar.cpp:78-85: IEEE x/scale, clamp to
+// [-qmax, qmax], round half away) for every amax bit pattern in [lo, lo + count):
+// scale = amax/qmax (0 -> 1) exactly as K1 forms it, x = +amax, -amax and nx
+// pseudo-random x with |x| <= amax (uniform over the bit patterns <= amax, random
+// sign), for qmax 127 (Q/K, V INT8) and 7 (V INT4). Counts mismatches; records
+// the first one (amax bits, x bits, qmax, K1 code, reference code).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ int ref_code(float x, float scale, float qmax) {
+    float q = __fdiv_rn(x, scale);
+    q = fminf(qmax, fmaxf(-qmax, q));
+    return (int)roundf(q);
+}
+__global__ void __launch_bounds__(256) k1_quant_proof(uint32_t lo, uint32_t count, uint32_t nx, uint32_t seed,
+                                                      unsigned long long* bad, uint32_t* first) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint32_t ab = lo + i;
+        const float amax = __uint_as_float(ab);
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const float qmax = v ? 7.0f : 127.0f;
+            float scale = __fdiv_rn(amax, qmax);
+            if (scale == 0.0f)
+                scale = 1.0f;
+            const float rs = __frcp_rn(scale);
+            for (uint32_t j = 0; j < nx + 2; j += 4) {
+                float xs[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t jj = j + e;
+                    if (jj == 0)
+                        xs[e] = amax;
+                    else if (jj == 1)
+                        xs[e] = -amax;
+                    else {
+                        const uint32_t h = mix32(ab * 0x9e3779b9u ^ mix32(jj * 0x85ebca6bu + seed + (uint32_t)v));
+                        const uint32_t xb = (uint32_t)(((unsigned long long)mix32(h) * ((unsigned long long)ab + 1)) >> 32);
+                        xs[e] = __uint_as_float(xb | (h & 0x80000000u));
+                    }
+                }
+                int c[4];
+                quant_sym4(make_float4(xs[0], xs[1], xs[2], xs[3]), scale, rs, qmax, c[0], c[1], c[2], c[3]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (j + e >= nx + 2)
+                        continue;
+                    const int r = ref_code(xs[e], scale, qmax);
+                    const int cs = quant_sym(xs[e], scale, rs, qmax); // the standalone quantize's element path
+                    if (c[e] != r || cs != r) {
+                        if (atomicAdd(bad, 1ull) == 0ull) {
+                            first[0] = ab;
+                            first[1] = __float_as_uint(xs[e]);
+                            first[2] = (uint32_t)qmax;
+                            first[3] = (uint32_t)(c[e] != r ? c[e] : cs);
+                            first[4] = (uint32_t)r;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_k1_quant_proof(uint32_t lo, uint32_t count, uint32_t nx, uint32_t seed, unsigned long long* bad,
+                                  uint32_t* first, int num_sms, cudaStream_t st) {
+    if (count == 0)
+        return cudaSuccess;
+    const uint32_t blocks = (count + 255) / 256;
+    const uint32_t cap = (uint32_t)num_sms * 8;
+    k1_quant_proof<<<blocks < cap ? blocks : cap, 256, 0, st>>>(lo, count, nx, seed, bad, first);
     return cudaGetLastError();
 }
 

@@ -11,8 +11,7 @@ ctx = paro.Context(0)
 g = paro.parse_grid(grid_text)
 N = g.token_count()
 heads = list(range(H))
-q, k, v, masks = bench.build_inputs(paro, heads, N, d, density, "random")
-orders = bench.head_orders(paro, g, H)
+orders, q, k, v, masks = bench.workload_ours(paro, ctx, heads, grid_text, N, d, density, "random")
 layer = paro.Layer(ctx, H, d, g, orders)
 dmask = torch.from_numpy(masks).cuda()
 hq, hk, hv = (paro.HostBuffer(q.shape, np.float32) for _ in range(3))

@@ -10,12 +10,11 @@ grid_text, H, d, density, pv, _ = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1
 ctx = paro.Context(0)
 g = paro.parse_grid(grid_text)
 N = g.token_count()
-orders_all = bench.head_orders(paro, g, H)
 s = torch.cuda.current_stream(); sp = s.cuda_stream
 for hn in [H, H // 2, H // 4, H // 8]:
     heads = list(range(hn))
-    q, k, v, masks = bench.build_inputs(paro, heads, N, d, density, "random")
-    layer = paro.Layer(ctx, hn, d, g, [orders_all[h] for h in heads])
+    orders, q, k, v, masks = bench.workload_ours(paro, ctx, heads, grid_text, N, d, density, "random")
+    layer = paro.Layer(ctx, hn, d, g, orders)
     dq, dk, dv = (torch.from_numpy(x).cuda() for x in (q, k, v))
     dm = torch.from_numpy(masks).cuda()
     out = torch.empty_like(dq); z = torch.empty((hn, N), dtype=torch.uint8, device="cuda")

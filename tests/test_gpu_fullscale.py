@@ -33,8 +33,7 @@ def test_full_size_sampled_rows(paro, ctx, oracle, grid, H, d, density, pv_bits,
     N = g.token_count()
     kb = (N + 63) // 64
     heads = list(range(H))
-    q, k, v, masks = bench.build_inputs(paro, heads, N, d, density, "random")
-    orders = bench.head_orders(paro, g, H)
+    orders, q, k, v, masks = bench.workload_ours(paro, ctx, heads, grid, N, d, density, "random")
     layer = paro.Layer(ctx, H, d, g, orders)
     layer.set_masks(masks)
     out, zeroed = layer.forward_host(q, k, v, 0.0, pv_bits)

@@ -51,6 +51,25 @@ def test_gen_mask_matches_reference(paro, ctx, reference, k, density, guard, tie
         assert reps[i] == rep
 
 
+def test_gen_mask_matches_golden(paro, ctx, kat):
+    """The committed reference fixture (tests/golden/make_golden.py: gen_mask(U, 0.4, 16))."""
+    m, rep = ctx.gen_mask(kat["gen_mask_sums"], 0.4, 16)
+    assert np.array_equal(m.bits, kat["gen_mask_bits"])
+
+
+@pytest.mark.parametrize("kb,density,seed", [(275, 0.3, 1), (275, 0.2, 2), (64, 0.3, 3), (2, 0.3, 4), (40, 0.05, 5)])
+def test_gen_mask_ties_vs_reference(paro, ctx, reference, kb, density, seed):
+    rng = np.random.default_rng(seed)
+    sums = rng.random((kb, kb))
+    sums[rng.random((kb, kb)) < 0.2] = 0.5  # ties exercise the (row, col) tie-break
+    if seed != 5:
+        sums += 2.0 * np.eye(kb)
+    m, rep = ctx.gen_mask(sums, density, 64)
+    rc, bits, rep2 = reference.gen_mask(sums, density, 64)
+    assert rc == 0 and np.array_equal(m.bits, bits) and rep == rep2
+    assert m.popcount() == int(np.ceil(density * kb * kb))
+
+
 def test_gen_mask_repairs_empty_rows(paro, ctx, reference):
     k = 24
     s = np.full((k, k), 1.0)

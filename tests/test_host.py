@@ -1,6 +1,6 @@
 """CPU tests of the product library (no GPU needed): the C-ABI .so loads and
 exports every symbol include/paro_b200.h declares; the host-side integer stages
-(grid, make_perm, enumerate, PMSK/PSCH, gen_mask, synthetic generator) are
+(grid, make_perm, enumerate, PMSK/PSCH, synthetic generator) are
 bit-exact with the reference (golden fixtures and, where built, the live
 reference library); errors map to the reference's exception classes."""
 import ctypes
@@ -149,31 +149,6 @@ def test_schedule_at_matches_golden(paro, kat):
         paro.schedule_at(img + b"xx", 0)
     with pytest.raises(paro.FormatError):
         paro.schedule_at(b"PSCHxxxx", 0)
-
-
-def test_gen_mask_matches_golden(paro, kat):
-    m, rep = paro.gen_mask(kat["gen_mask_sums"], 0.4, 16)
-    assert np.array_equal(m.bits, kat["gen_mask_bits"])
-
-
-@pytest.mark.parametrize("kb,density,seed", [(275, 0.3, 1), (275, 0.2, 2), (64, 0.3, 3), (2, 0.3, 4), (40, 0.05, 5)])
-def test_gen_mask_vs_reference(paro, reference, kb, density, seed):
-    rng = np.random.default_rng(seed)
-    sums = rng.random((kb, kb))
-    sums[rng.random((kb, kb)) < 0.2] = 0.5  # ties exercise the (row, col) tie-break
-    if seed != 5:
-        sums += 2.0 * np.eye(kb)
-    m, rep = paro.gen_mask(sums, density, 64)
-    rc, bits, rep2 = reference.gen_mask(sums, density, 64)
-    assert rc == 0 and np.array_equal(m.bits, bits) and rep == rep2
-    assert m.popcount() == int(np.ceil(density * kb * kb))
-
-
-def test_gen_mask_errors(paro):
-    with pytest.raises(paro.ConfigError):
-        paro.gen_mask(np.ones((4, 4)), 0.0, 64)
-    with pytest.raises(paro.ConfigError):
-        paro.gen_mask(np.ones((10, 10)), 0.05, 64)  # fewer kept blocks than rows
 
 
 # ------------------------------------------------------------------ synthetic inputs
