@@ -46,14 +46,12 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "k3_common.cuh"
 #include "layer.cuh"
 #include "ptx.cuh"
 
 namespace paro {
 
-#ifndef PARO_DYNAMIC
-#define PARO_DYNAMIC 1
-#endif
 template <int D>
 struct K3Cfg {
     static constexpr int G = D / 64;
@@ -130,51 +128,6 @@ __device__ __forceinline__ uint64_t desc_v(uint32_t saddr) {
     return ptx::smem_desc(saddr, K3Cfg<D>::ATOM * 8, K3Cfg<D>::ATOM, K3Cfg<D>::LAYOUT);
 }
 
-__device__ __forceinline__ float ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// ---- packed fp32x2 helpers (FFMA2 / FADD2 / FMUL2 on sm_100a)
-__device__ __forceinline__ uint64_t pk(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk(uint64_t v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t add2_rm(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-
 // QK issue for one q-block tile (M = 64): S_g in TMEM columns tm_s + 64*g at the
 // tile's lane offset; two K=32 steps per 64-column group.
 template <int D>
@@ -189,63 +142,6 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
         }
 }
 
-// Phase timers (PARO_K3_PROF builds only): clock64 deltas summed per warp role.
-//   [0..7]  softmax: wait, pass1, reduce, pass2, exact, post, steps, items
-//   [8..11] epilogue: wait, dequant, store, steps
-//   [12..15] mma: wait KV/S, wait P/O, issue, steps
-#ifdef PARO_K3_PROF
-static __device__ unsigned long long g_prof[24];
-#define PROF_T(v) const long long v = clock64()
-#define PROF_ADD(i, d) prof[i] += (unsigned long long)(d)
-#else
-#define PROF_T(v)
-#define PROF_ADD(i, d)
-#endif
-
-struct K3Params {
-    LayerDev L;
-    double scale64;   // effective scale (AttnInputs::effective_scale, fp64)
-    float scale_log2; // effective scale * log2(e)
-    float p_qmax;     // 255 or 15
-    float* out;       // [H][N][D] original token order
-    uint8_t* zeroed;  // [H][N] or null
-    const uint32_t* order; // LPT-sorted work items (h << 16 | p) of this launch
-    uint32_t n_items;
-    uint32_t* work_counter; // next index into `order` (zeroed before the launch; DYNAMIC)
-    unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
-    K3Dump dump;               // P-code dump test hook (dump.slot == nullptr: off)
-};
-
-// P-code dump of one row's final codes for step t (cols [c0, c0 + 16*nch) of the
-// row's 64 key columns; 64B-swizzled P tile rows as written by quantize_store)
-__device__ __forceinline__ void dump_row(const K3Dump& dm, int32_t slot, uint32_t t, uint32_t r, const uint8_t* prow,
-                                         int c0chunk, int nch) {
-    uint8_t* dst = dm.codes + (((size_t)slot * dm.kb + t) * 64 + r) * 64;
-    for (int c = c0chunk; c < c0chunk + nch; ++c)
-        *reinterpret_cast<uint4*>(dst + 16 * c) = *reinterpret_cast<const uint4*>(prow + ((c ^ ((r >> 1) & 3)) << 4));
-}
-__device__ __forceinline__ void dump_meta(const K3Dump& dm, int32_t slot, uint32_t t, float lo, float pscale,
-                                          uint32_t bj) {
-    *reinterpret_cast<float4*>(dm.meta + ((size_t)slot * dm.kb + t) * 4) = make_float4(lo, pscale, (float)bj, 1.f);
-}
-
-struct Item {
-    uint32_t h, qa, qb, na, nb, n; // qb = 0xffff when the pair has no B
-};
-
-__device__ __forceinline__ Item load_item(const LayerDev& L, uint32_t it) {
-    Item x;
-    x.h = it >> 16;
-    const uint32_t p = it & 0xffffu;
-    const uint32_t pr = L.pairs[(size_t)x.h * L.np + p];
-    x.qa = pr & 0xffffu;
-    x.qb = pr >> 16;
-    x.na = L.qb_count[(size_t)x.h * L.kb2 + x.qa];
-    x.nb = x.qb != 0xffffu ? L.qb_count[(size_t)x.h * L.kb2 + x.qb] : 0u;
-    x.n = x.na > x.nb ? x.na : x.nb;
-    return x;
-}
-
 // ---------------------------------------------------------------------------
 // Softmax, one step for this thread's row. Pass 1 reads S for the row extremes
 // (exact in the integer domain at d=64); the tile group's lo/hi then come from
@@ -255,116 +151,6 @@ __device__ __forceinline__ Item load_item(const LayerDev& L, uint32_t it) {
 // has no tile this step (`live` false) run the same instructions but change
 // no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
-
-// wait for several mbarrier phases, issuing the probes back to back so their
-// latencies overlap (each try_wait costs ~90 cycles even when already complete)
-__device__ __forceinline__ void mbar_wait2(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1) {
-    const bool r0 = ptx::mbar_try_wait(b0, p0);
-    const bool r1 = ptx::mbar_try_wait(b1, p1);
-    if (!r0)
-        ptx::mbar_wait(b0, p0);
-    if (!r1)
-        ptx::mbar_wait(b1, p1);
-}
-// Waits of roles with slack (producer: 3-stage ring; epilogue: double-buffered
-// O) back off with __nanosleep between probes so their spinning leaves the issue
-// slots to the softmax and MMA warps on the same sub-partition.
-#ifndef PARO_LAZY_NS
-#define PARO_LAZY_NS 512
-#endif
-__device__ __forceinline__ void mbar_wait_lazy(uint32_t b, uint32_t p) {
-    if (PARO_LAZY_NS == 0) {
-        ptx::mbar_wait(b, p);
-        return;
-    }
-    while (!ptx::mbar_try_wait(b, p))
-        __nanosleep(PARO_LAZY_NS);
-}
-// The MMA issuer has a step of slack too (S and P are double-buffered; a
-// softmax step is ~5k cycles). Measured at c2 (K3 ms): spin everywhere 4.87;
-// producer + epilogue 512 ns back-off 4.75; + MMA 500 ns 4.61 (1000: 4.61,
-// 2000: 4.65); c5 unchanged within noise. Only the softmax waits stay hot.
-#ifndef PARO_LAZY_MMA_NS
-#define PARO_LAZY_MMA_NS 500
-#endif
-__device__ __forceinline__ void mbar_wait_mma(uint32_t b, uint32_t p) {
-    if (PARO_LAZY_MMA_NS == 0) {
-        ptx::mbar_wait(b, p);
-        return;
-    }
-    while (!ptx::mbar_try_wait(b, p))
-        __nanosleep(PARO_LAZY_MMA_NS);
-}
-__device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
-                                           uint32_t p2) {
-    const bool r0 = ptx::mbar_try_wait(b0, p0);
-    const bool r1 = ptx::mbar_try_wait(b1, p1);
-    const bool r2 = ptx::mbar_try_wait(b2, p2);
-    if (!r0)
-        ptx::mbar_wait(b0, p0);
-    if (!r1)
-        ptx::mbar_wait(b1, p1);
-    if (!r2)
-        ptx::mbar_wait(b2, p2);
-}
-
-__device__ __forceinline__ uint64_t fma2_rm(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t r;
-    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
-// Per-row, per-step exact statistics published for the boundary path (d=64):
-// the exact (fp64, reference-order) min / max logit of the row's tile and the
-// running max after it.
-struct RowStat { // 40 bytes
-    double tmin, tmax, m;
-    float pmin, pmax; // the fast path's fp32 row extremes (candidate selection)
-    int valid, pad;
-};
-static_assert(sizeof(RowStat) == 40, "RowStat layout");
-
-constexpr double kLog2e = 1.4426950408889634;
-// Relative band of the fast-path quotient q = (p - lo) / pscale at d=64. The
-// fp32 path forms the exp2 argument as (S - smax) * c + d with d = exact
-// (tmax - m) * log2e, so its error is ~6e-8 * |arg| + the ex2.approx error
-// (~2.4e-7); with lo/hi from the same formula the quotient is within ~4-6e-7
-// of the reference's. A code is trusted only if q*(1-kappa) and q*(1+kappa)
-// round to the same integer, else it is recomputed exactly in fp64.
-// Measured on c2/c3 (8M sampled elements each): kappa 0 leaves code flips
-// (max|dO|/max|O| 5.8e-4 INT8, 6.4e-3 INT4); 4e-7 and 8e-7 are exact.
-#ifndef PARO_RED_MBAR
-#define PARO_RED_MBAR 1
-#endif
-#ifndef PARO_KAPPA
-#define PARO_KAPPA 6e-7f
-#endif
-constexpr float kKappa = PARO_KAPPA;
-
-// int32 S of (row r, key j) recomputed from the smem Q/K tiles (64-byte rows, 64B swizzle)
-__device__ __forceinline__ int32_t dot_row64(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t j) {
-    const uint8_t* qr = qtile + (r >> 3) * 512 + (r & 7) * 64;
-    const uint8_t* kr = ktile + (j >> 3) * 512 + (j & 7) * 64;
-    int32_t acc = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int4 a = *reinterpret_cast<const int4*>(qr + ((c ^ ((r >> 1) & 3)) << 4));
-        const int4 b = *reinterpret_cast<const int4*>(kr + ((c ^ ((j >> 1) & 3)) << 4));
-        acc = __dp4a(a.x, b.x, acc);
-        acc = __dp4a(a.y, b.y, acc);
-        acc = __dp4a(a.z, b.z, acc);
-        acc = __dp4a(a.w, b.w, acc);
-    }
-    return acc;
-}
-
-// round-half-away of q >= 0 exactly as std::round (kernels_scalar.cpp:84)
-__device__ __forceinline__ uint32_t round_half_away_pos(float q) {
-    float t = truncf(q);
-    if (__fsub_rn(q, t) >= 0.5f)
-        t = __fadd_rn(t, 1.0f);
-    return (uint32_t)t;
-}
 
 // d=128: the two int32 group sums S_0, S_1 of (row r, key j) from the smem Q/K
 // tiles (128-byte rows, 128B swizzle: 16-B chunk c of row r at c ^ (r & 7))
@@ -472,11 +258,6 @@ constexpr float kErrS = 5e-7f, kGapSlack = 2e-5f;
 // Lanes whose q-block has no tile this step (`live` false) run the same
 // instructions but change no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
-struct RowState {
-    float m32, l;
-    double m64;
-};
-
 template <int D, bool SPLIT>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
@@ -742,6 +523,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     // wait for the other compute warps (an mbarrier, so arriving never blocks;
     // c5 132.7 -> 129.0 ms). At d=64 holding 32 p values across the wait spills
     // (96 registers) and measured slower, so it keeps bar.sync.
+    // (Measured at d=64 with 12 warps and setmaxnreg giving the softmax 120 registers
+    // for the row's 64 p values: 5.32 vs 4.52 ms at c2, branch k3-multislot-experiment.)
     constexpr bool kOverlap = SPLIT && PARO_RED_MBAR;
     float pv0[32];
     if constexpr (kOverlap) {
@@ -973,7 +756,9 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     pscale_out = pscale;
 }
 
-template <int D>
+// DUMP: the P-code dump test hook is compiled in (a separate instantiation, so the
+// product kernel carries no extra registers for it)
+template <int D, bool DUMP>
 __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     k3_attention(const __grid_constant__ K3Params P, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
@@ -1234,7 +1019,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 st.l = L.init_l[srow];
             }
             RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
-            const int32_t dslot = P.dump.slot && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
+            const int32_t dslot = DUMP && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
                 const bool live = t < nmine;
@@ -1260,9 +1045,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
                                 gamma, lo, pscale, 0u, nullptr,
-                                reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 2) * 512, bar(BR::RED),
+                                reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + quad * 512, bar(BR::RED),
                                 T & 1, prof);
-                if (dslot >= 0 && live) {
+                if (DUMP && dslot >= 0 && live) {
                     dump_row(P.dump, dslot, t, r, prow, 0, 4);
                     if (r == 0)
                         dump_meta(P.dump, dslot, t, lo, pscale, bj);
@@ -1482,7 +1267,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 for (int c = 0; c < DH / 2; ++c)
                     acc[c] = pk(a0[c].x, a0[c].y);
             }
-            const int32_t dslot = P.dump.slot && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
+            const int32_t dslot = DUMP && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             // acc = gamma * acc + (pscale * vscale) * ip + u_c over this warp's O columns,
             // for step U (its P side was published before this warp's own PFULL arrive)
             auto dequant = [&](uint32_t U) {
@@ -1554,7 +1339,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                       reinterpret_cast<float4*>(smem + C::OFF_XCH),
                                       reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512,
                                       bar(BR::RED), T & 1, prof);
-                if (dslot >= 0 && live) {
+                if (DUMP && dslot >= 0 && live) {
                     dump_row(P.dump, dslot, t, r, prow, (int)half * 2, 2);
                     if (r == 0 && half == 0)
                         dump_meta(P.dump, dslot, t, lo, pscale, bj);
@@ -1715,10 +1500,11 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
                                const CUtensorMap& tv, int grid, cudaStream_t st) {
     init_watchdog();
     const uint32_t smem = K3Cfg<D>::SMEM_BYTES;
-    cudaError_t e = cudaFuncSetAttribute(k3_attention<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = p.dump.slot ? k3_attention<D, true> : k3_attention<D, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    k3_attention<D><<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv);
+    kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv);
     return cudaGetLastError();
 }
 

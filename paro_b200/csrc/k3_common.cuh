@@ -1,0 +1,240 @@
+// k3_common.cuh -- pieces of K3 (attention_kernel.cu) shared with its experimental
+// variants: packed fp32x2 / exp2 helpers, TMEM loads, launch parameters, work
+// items, mbarrier wait flavours, the exact-path row statistics and the P-code
+// dump hook.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layer.cuh"
+#include "ptx.cuh"
+
+namespace paro {
+
+#ifndef PARO_DYNAMIC
+#define PARO_DYNAMIC 1
+#endif
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---- packed fp32x2 helpers (FFMA2 / FADD2 / FMUL2 on sm_100a)
+__device__ __forceinline__ uint64_t pk(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2_rm(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+// Phase timers (PARO_K3_PROF builds only): clock64 deltas summed per warp role.
+//   [0..7]  softmax: wait, pass1, reduce, pass2, exact, post, steps, items
+//   [8..11] epilogue: wait, dequant, store, steps
+//   [12..15] mma: wait KV/S, wait P/O, issue, steps
+#ifdef PARO_K3_PROF
+static __device__ unsigned long long g_prof[24];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(i, d) prof[i] += (unsigned long long)(d)
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, d)
+#endif
+
+struct K3Params {
+    LayerDev L;
+    double scale64;   // effective scale (AttnInputs::effective_scale, fp64)
+    float scale_log2; // effective scale * log2(e)
+    float p_qmax;     // 255 or 15
+    float* out;       // [H][N][D] original token order
+    uint8_t* zeroed;  // [H][N] or null
+    const uint32_t* order; // LPT-sorted work items (h << 16 | p) of this launch
+    uint32_t n_items;
+    uint32_t* work_counter; // next index into `order` (zeroed before the launch; DYNAMIC)
+    unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
+    K3Dump dump;               // P-code dump test hook (dump.slot == nullptr: off)
+};
+
+// P-code dump of one row's final codes for step t (cols [c0, c0 + 16*nch) of the
+// row's 64 key columns; 64B-swizzled P tile rows as written by quantize_store)
+__device__ __forceinline__ void dump_row(const K3Dump& dm, int32_t slot, uint32_t t, uint32_t r, const uint8_t* prow,
+                                         int c0chunk, int nch) {
+    uint8_t* dst = dm.codes + (((size_t)slot * dm.kb + t) * 64 + r) * 64;
+    for (int c = c0chunk; c < c0chunk + nch; ++c)
+        *reinterpret_cast<uint4*>(dst + 16 * c) = *reinterpret_cast<const uint4*>(prow + ((c ^ ((r >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void dump_meta(const K3Dump& dm, int32_t slot, uint32_t t, float lo, float pscale,
+                                          uint32_t bj) {
+    *reinterpret_cast<float4*>(dm.meta + ((size_t)slot * dm.kb + t) * 4) = make_float4(lo, pscale, (float)bj, 1.f);
+}
+
+struct Item {
+    uint32_t h, qa, qb, na, nb, n; // qb = 0xffff when the pair has no B
+};
+
+__device__ __forceinline__ Item load_item(const LayerDev& L, uint32_t it) {
+    Item x;
+    x.h = it >> 16;
+    const uint32_t p = it & 0xffffu;
+    const uint32_t pr = L.pairs[(size_t)x.h * L.np + p];
+    x.qa = pr & 0xffffu;
+    x.qb = pr >> 16;
+    x.na = L.qb_count[(size_t)x.h * L.kb2 + x.qa];
+    x.nb = x.qb != 0xffffu ? L.qb_count[(size_t)x.h * L.kb2 + x.qb] : 0u;
+    x.n = x.na > x.nb ? x.na : x.nb;
+    return x;
+}
+
+// wait for several mbarrier phases, issuing the probes back to back so their
+// latencies overlap (each try_wait costs ~90 cycles even when already complete)
+__device__ __forceinline__ void mbar_wait2(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1) {
+    const bool r0 = ptx::mbar_try_wait(b0, p0);
+    const bool r1 = ptx::mbar_try_wait(b1, p1);
+    if (!r0)
+        ptx::mbar_wait(b0, p0);
+    if (!r1)
+        ptx::mbar_wait(b1, p1);
+}
+// Waits of roles with slack (producer: 3-stage ring; epilogue: double-buffered
+// O) back off with __nanosleep between probes so their spinning leaves the issue
+// slots to the softmax and MMA warps on the same sub-partition.
+#ifndef PARO_LAZY_NS
+#define PARO_LAZY_NS 512
+#endif
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t b, uint32_t p) {
+    if (PARO_LAZY_NS == 0) {
+        ptx::mbar_wait(b, p);
+        return;
+    }
+    // no watchdog here: these roles wait on barriers that the softmax warps also
+    // depend on, and their waits (ptx::mbar_wait) trap on a stalled pipeline
+    while (!ptx::mbar_try_wait(b, p))
+        __nanosleep(PARO_LAZY_NS);
+}
+// The MMA issuer has a step of slack too (S and P are double-buffered; a
+// softmax step is ~5k cycles). Measured at c2 (K3 ms): spin everywhere 4.87;
+// producer + epilogue 512 ns back-off 4.75; + MMA 500 ns 4.61 (1000: 4.61,
+// 2000: 4.65); c5 unchanged within noise. Only the softmax waits stay hot.
+#ifndef PARO_LAZY_MMA_NS
+#define PARO_LAZY_MMA_NS 500
+#endif
+__device__ __forceinline__ void mbar_wait_mma(uint32_t b, uint32_t p) {
+    if (PARO_LAZY_MMA_NS == 0) {
+        ptx::mbar_wait(b, p);
+        return;
+    }
+    while (!ptx::mbar_try_wait(b, p))
+        __nanosleep(PARO_LAZY_MMA_NS);
+}
+__device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                           uint32_t p2) {
+    const bool r0 = ptx::mbar_try_wait(b0, p0);
+    const bool r1 = ptx::mbar_try_wait(b1, p1);
+    const bool r2 = ptx::mbar_try_wait(b2, p2);
+    if (!r0)
+        ptx::mbar_wait(b0, p0);
+    if (!r1)
+        ptx::mbar_wait(b1, p1);
+    if (!r2)
+        ptx::mbar_wait(b2, p2);
+}
+
+__device__ __forceinline__ uint64_t fma2_rm(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Per-row, per-step exact statistics published for the boundary path (d=64):
+// the exact (fp64, reference-order) min / max logit of the row's tile and the
+// running max after it.
+struct RowStat { // 40 bytes
+    double tmin, tmax, m;
+    float pmin, pmax; // the fast path's fp32 row extremes (candidate selection)
+    int valid, pad;
+};
+static_assert(sizeof(RowStat) == 40, "RowStat layout");
+
+constexpr double kLog2e = 1.4426950408889634;
+// Relative band of the fast-path quotient q = (p - lo) / pscale at d=64. The
+// fp32 path forms the exp2 argument as (S - smax) * c + d with d = exact
+// (tmax - m) * log2e, so its error is ~6e-8 * |arg| + the ex2.approx error
+// (~2.4e-7); with lo/hi from the same formula the quotient is within ~4-6e-7
+// of the reference's. A code is trusted only if q*(1-kappa) and q*(1+kappa)
+// round to the same integer, else it is recomputed exactly in fp64.
+// Measured on c2/c3 (8M sampled elements each): kappa 0 leaves code flips
+// (max|dO|/max|O| 5.8e-4 INT8, 6.4e-3 INT4); 4e-7 and 8e-7 are exact.
+#ifndef PARO_RED_MBAR
+#define PARO_RED_MBAR 1
+#endif
+#ifndef PARO_KAPPA
+#define PARO_KAPPA 6e-7f
+#endif
+constexpr float kKappa = PARO_KAPPA;
+
+// int32 S of (row r, key j) recomputed from the smem Q/K tiles (64-byte rows, 64B swizzle)
+__device__ __forceinline__ int32_t dot_row64(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t j) {
+    const uint8_t* qr = qtile + (r >> 3) * 512 + (r & 7) * 64;
+    const uint8_t* kr = ktile + (j >> 3) * 512 + (j & 7) * 64;
+    int32_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int4 a = *reinterpret_cast<const int4*>(qr + ((c ^ ((r >> 1) & 3)) << 4));
+        const int4 b = *reinterpret_cast<const int4*>(kr + ((c ^ ((j >> 1) & 3)) << 4));
+        acc = __dp4a(a.x, b.x, acc);
+        acc = __dp4a(a.y, b.y, acc);
+        acc = __dp4a(a.z, b.z, acc);
+        acc = __dp4a(a.w, b.w, acc);
+    }
+    return acc;
+}
+
+// round-half-away of q >= 0 exactly as std::round (kernels_scalar.cpp:84)
+__device__ __forceinline__ uint32_t round_half_away_pos(float q) {
+    float t = truncf(q);
+    if (__fsub_rn(q, t) >= 0.5f)
+        t = __fadd_rn(t, 1.0f);
+    return (uint32_t)t;
+}
+
+struct RowState {
+    float m32, l;
+    double m64;
+};
+
+
+} // namespace paro

@@ -30,7 +30,7 @@ namespace paro {
 // round-down adds: floor(RD(|q| + 0.5)) == floor(|q| + 0.5), and
 // RD(t + 2^23) leaves floor(t) in the mantissa. No XU-pipe instruction.
 __device__ __forceinline__ int quant_sym(float x, float scale, float rs, float qmax) {
-    if (scale < 1.17549435e-38f) // subnormal scale: see quant_sym4
+    if (scale < 0x1p-100f) // tiny scale: see quant_sym4
         return (int)roundf(fminf(qmax, fmaxf(-qmax, __fdiv_rn(x, scale))));
     const float q0 = __fmul_rn(x, rs);
     const float e = __fmaf_rn(-q0, scale, x);
@@ -73,12 +73,12 @@ __device__ __forceinline__ int quant_ieee(float x, float scale, float qmax) {
 }
 __device__ __forceinline__ void quant_sym4(float4 v, float scale, float rs, float qmax, int& c0, int& c1, int& c2,
                                            int& c3) {
-    if (scale < 1.17549435e-38f) {
-        // subnormal group scale (amax < qmax * 2^-126): RN(1/scale) overflows or is
-        // inexact enough that the residual step no longer gives RN(x/scale), so the
-        // group takes the IEEE quotient and the clamp as written (a group-uniform
-        // branch; found by the every-amax-bit-pattern proof in
-        // tests/test_gpu_fullshape_int.py)
+    if (scale < 0x1p-100f) {
+        // tiny group scale: for x near a rounding boundary (|x| ~ (k + 1/2) scale) the
+        // residual x - q0*scale falls below 2^-126 (or RN(1/scale) overflows), so the
+        // residual step no longer gives RN(x/scale); such groups take the IEEE
+        // quotient and the clamp as written (group-uniform branch; found by the
+        // every-amax-bit-pattern proof in tests/test_gpu_fullshape_int.py)
         c0 = quant_ieee(v.x, scale, qmax);
         c1 = quant_ieee(v.y, scale, qmax);
         c2 = quant_ieee(v.z, scale, qmax);

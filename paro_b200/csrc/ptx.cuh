@@ -94,6 +94,13 @@ static __device__ unsigned long long g_watchdog_ns = 4000000000ull;
 // of the limit and a clock read between probes -- beats both a tighter spin (c2
 // +14%, c5 +7%) and a __nanosleep(32..400) back-off (+1..4%). Roles with slack
 // use a sleeping wait instead: attention_kernel.cu mbar_wait_lazy / _mma.)
+__device__ __forceinline__ void watchdog_trip() {
+    if (g_watchdog_ns)
+        __trap();
+}
+// The suspending try_wait also returns early when other barrier traffic in a busy
+// CTA wakes it; the probe loop (one L1 load of the limit and a clock read between
+// probes) measured faster than tighter loops in K3 (round 1).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity))
         return;
