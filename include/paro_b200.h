@@ -53,7 +53,7 @@ const char* paro_version(void);
  * ------------------------------------------------------------------------- */
 
 /* parse_grid("F:13,H:30,W:45") -- replaces paro::parse_grid + TokenGrid
- * validation (tensor.cpp:320-341, 389-408). labels/extents hold >= 3 slots. */
+ * validation (tensor.cpp:26-47, 95-114). labels/extents hold >= 3 slots. */
 int paro_parse_grid(const char* text, int* ndim, char* labels, uint32_t* extents);
 
 /* make_perm(grid, order) -- replaces paro::make_perm (reorder.hpp:32,
@@ -158,6 +158,9 @@ int paro_synth_randn(uint64_t seed, size_t count, float* out);
 int paro_ctx_create(int device, paro_ctx** out);
 int paro_ctx_destroy(paro_ctx* ctx);
 int paro_ctx_num_sms(const paro_ctx* ctx, int* out);
+/* visible CUDA devices (one paro_ctx per device, each driven from its own host
+ * thread: the multi-GPU head shard) */
+int paro_device_count(int* out);
 
 /* pinned host buffers for the e2e path (cudaHostAlloc / cudaFreeHost) */
 int paro_host_alloc(size_t bytes, void** out);

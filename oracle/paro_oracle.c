@@ -28,7 +28,7 @@
 #define ORACLE_FORMAT 3 /* FormatError/IoError, error.hpp:31-36 */
 
 /* ------------------------------------------------------------------------- */
-/* Token grid + permutation: tensor.cpp:364-387 (flat_index, grid_coords),     */
+/* Token grid + permutation: tensor.cpp:70-93 (flat_index, grid_coords),     */
 /* reorder.cpp:49-72 (make_perm).                                              */
 /* ------------------------------------------------------------------------- */
 int oracle_make_perm(int ndim, const char* labels, const uint32_t* extents, const char* order,
@@ -43,7 +43,7 @@ int oracle_make_perm(int ndim, const char* labels, const uint32_t* extents, cons
             if (labels[b] == order[a])
                 found = b;
         if (found < 0)
-            return ORACLE_CONFIG; /* axis_index throws InputError, tensor.cpp:350-355 */
+            return ORACLE_CONFIG; /* axis_index throws InputError, tensor.cpp:56-61 */
         src_axis[a] = found;
         pext[a] = extents[found];
     }
@@ -53,7 +53,7 @@ int oracle_make_perm(int ndim, const char* labels, const uint32_t* extents, cons
     for (size_t old = 0; old < n; ++old) {
         uint32_t coords[3];
         size_t idx = old;
-        for (int a = ndim; a-- > 0;) { /* grid_coords: tensor.cpp:378-387 */
+        for (int a = ndim; a-- > 0;) { /* grid_coords: tensor.cpp:84-93 */
             coords[a] = (uint32_t)(idx % extents[a]);
             idx /= extents[a];
         }

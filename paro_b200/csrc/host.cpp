@@ -106,11 +106,11 @@ struct Grid {
         for (int a = 0; a < ndim; ++a)
             if (labels[a] == c)
                 return a;
-        fail(PARO_E_INPUT, std::string("grid has no axis labeled '") + c + "'"); // tensor.cpp:350-355
+        fail(PARO_E_INPUT, std::string("grid has no axis labeled '") + c + "'"); // tensor.cpp:56-61
     }
 };
 
-// TokenGrid constructor rules (tensor.cpp:320-341)
+// TokenGrid constructor rules (tensor.cpp:26-47)
 void validate_grid(const Grid& g) {
     if (g.ndim != 2 && g.ndim != 3)
         fail(PARO_E_CONFIG, "token grid must have 2 or 3 axes, got " + std::to_string(g.ndim));
@@ -133,7 +133,7 @@ void validate_grid(const Grid& g) {
         fail(PARO_E_CONFIG, "2D grids use labels H and W only");
 }
 
-// parse_grid (tensor.cpp:389-408)
+// parse_grid (tensor.cpp:95-114)
 Grid parse_grid_text(const char* text) {
     if (!text)
         fail(PARO_E_CONFIG, "null grid text");
@@ -204,7 +204,7 @@ PermDesc perm_desc(const Grid& g, const std::string& order) {
         pd.ostride[off + a] = stride[src];
     }
     // a repeated label would make this a non-bijection; make_perm builds a
-    // TokenGrid from the re-listed axes, which rejects duplicates (tensor.cpp:333-334)
+    // TokenGrid from the re-listed axes, which rejects duplicates (tensor.cpp:39-40)
     unsigned seen = 0;
     for (int a = 0; a < g.ndim; ++a) {
         const unsigned bit = 1u << g.axis_index(order[a]);
@@ -1071,6 +1071,14 @@ int paro_ctx_destroy(paro_ctx* ctx) {
 
 int paro_ctx_num_sms(const paro_ctx* ctx, int* out) {
     return guarded([&] { *out = ctx->num_sms; });
+}
+
+int paro_device_count(int* out) {
+    return guarded([&] {
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        *out = n;
+    });
 }
 
 int paro_host_alloc(size_t bytes, void** out) {
