@@ -64,6 +64,11 @@ def parse_args():
     ap.add_argument("--mask-family", default="random", choices=["random", "banded"])
     ap.add_argument("--dense-prefix", type=int, default=0,
                     help="diagnostic: text tokens in front of the grid (K4 + K3); BASELINE configs use 0")
+    ap.add_argument("--schedule", type=int, default=0, metavar="T",
+                    help="per-timestep mask schedule of T steps (PSCH per head, paro_layer_set_schedule): step i "
+                         "runs timestep i %% T with its kept lists resident, no K2 in the step")
+    ap.add_argument("--schedule-prefetch", action="store_true",
+                    help="with --schedule: two list buffers, K2 of t+1 on a side stream during step t")
     ap.add_argument("--rope", action="store_true",
                     help="diagnostic: rotary embedding fused into K1 (paro_layer_set_rope); BASELINE configs do not rotate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -541,10 +546,25 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    step_no = [0]
+    if args.schedule:  # one PSCH schedule per head from the GPU build_schedule over per-timestep sums
+        blobs = []
+        for i, h in enumerate(my_heads):
+            rng = np.random.default_rng(104729 * (h + 1))
+            sums_t = np.stack([head_sums(h, kb, density, args.mask_family) + 0.1 * rng.random((kb, kb))
+                               for _ in range(args.schedule)])
+            ms, _ = ctx.build_schedule(sums_t, density, 64)
+            blobs.append(paro.serialize_schedule(args.schedule, ms))
+        layer.set_schedule(blobs, 2 if args.schedule_prefetch else 0, sp)
+
     def step(events=None):
         if events:
             events[0].record(stream)
-        layer.set_masks_device(dmask.data_ptr(), sp)
+        if args.schedule:  # timestep i % T: the lists are resident (or prefetched), no K2 here
+            layer.select_timestep(step_no[0] % args.schedule, sp)
+            step_no[0] += 1
+        else:
+            layer.set_masks_device(dmask.data_ptr(), sp)
         if events:
             events[1].record(stream)
         layer.reorder_quantize(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), pv_bits, sp)
@@ -641,7 +661,10 @@ def main():
         "dtype": "int8",
         "dtype_detail": "QK s8*s8->s32 and PV u8(u4 codes)*s8->s32 on tcgen05; fp32 softmax / dequant, fp64 row extremes",
         "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), K5 gen_mask masks (GPU)",
-        "config": bench_config(args.config, args.mask_family, all_masks, world, args.dense_prefix, args.rope),
+        "config": {**bench_config(args.config, args.mask_family, all_masks, world, args.dense_prefix, args.rope),
+                   **({"schedule": f"{args.schedule} timesteps, PSCH per head, kept lists "
+                                   + ("double-buffered, K2 of t+1 prefetched on a side stream" if args.schedule_prefetch
+                                      else "of every entry resident (no K2 in the step)")} if args.schedule else {})},
         "ms_per_layer": ms_step,
         "kernels_ms": {"k2_mask_lists": k2_ms, "k1_reorder_quantize": k1_ms, "k3_attention": k3_ms},
         "roofline": {
@@ -658,7 +681,8 @@ def main():
                         "unit": "GB/s", "frac": k1_gbs / hbm_peak, "algorithmic_bytes_per_launch": k1_bytes,
                         "traffic": _scaled(ncu_traffic(args.config, "k1_reorder_quantize"), hpr / H)},
         # per step: K2 (3 kernels) + K1 + K3, plus K4a + K4 + combine with a dense prefix
-        "gpu_launches": (5 + (3 if args.dense_prefix else 0)) * args.steps,
+        "gpu_launches": ((2 if args.schedule and not args.schedule_prefetch else 5) + (3 if args.dense_prefix else 0))
+                        * args.steps,
         "clocks": clk,
         "e2e": e2e,
     }

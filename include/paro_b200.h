@@ -220,6 +220,21 @@ int paro_layer_set_masks(paro_layer* layer, paro_stream_t stream, const uint8_t*
 int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const uint8_t* device_bits);
 /* The same from one serialized PMSK blob per head (deserialize_mask, mask.cpp:217-244): block 64,
  * a ceil(N/64)^2 grid; errors name the head. */
+/* Per-timestep mask schedule (MaskSchedule, mask.hpp; load_schedule / at(t),
+ * mask.cpp:132-140, 267-305): one PSCH image per head, all covering the same T
+ * timesteps. The T/2 distinct masks and the shared late mask of every head are
+ * uploaded once. resident_lists = 0: K2 builds every entry's kept lists now, and
+ * paro_layer_select_timestep is a pointer switch (no K2 in the step);
+ * resident_lists = 2: two list buffers -- select_timestep(t) makes t's lists
+ * current and builds t+1's on a side stream while step t runs (the paper's
+ * double-buffered prefetch). A later set_masks* ends the
+ * schedule. select_timestep: at(t) semantics and errors (t >= T: InputError). */
+int paro_layer_set_schedule(paro_layer* layer, paro_stream_t stream, const uint8_t* const* psch, const size_t* sizes,
+                            uint32_t resident_lists);
+int paro_layer_select_timestep(paro_layer* layer, paro_stream_t stream, uint32_t t);
+/* timesteps T, entries T/2 + 1, the entry whose lists are current (-1: none) */
+int paro_layer_schedule_info(const paro_layer* layer, uint32_t* timesteps, uint32_t* entries, int* current_entry);
+
 int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uint8_t* const* blobs,
                               const size_t* sizes);
 

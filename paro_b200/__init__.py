@@ -258,6 +258,20 @@ def schedule_at(data: bytes, t: int) -> BlockMask:
     return BlockMask(kr.value, kc.value, b.value, bits)
 
 
+def serialize_schedule(timesteps: int, masks: Sequence["BlockMask"]) -> bytes:
+    """PSCH image of a schedule (save_schedule, mask.cpp:246-263): `masks` holds the
+    timesteps//2 distinct masks (timestep i = position i) and then the shared late mask."""
+    half = timesteps // 2
+    if len(masks) != half + 1:
+        raise ShapeError(f"a {timesteps}-step schedule has {half} distinct masks + 1 shared, got {len(masks)}")
+    out = bytearray(b"PSCH")
+    out += int(timesteps).to_bytes(4, "little") + int(half).to_bytes(4, "little")
+    for i in range(half):
+        out += int(i).to_bytes(4, "little") + serialize_mask(masks[i])
+    out += serialize_mask(masks[half])
+    return bytes(out)
+
+
 def synth_randn(seed: int, count: int) -> np.ndarray:
     out = np.empty(count, np.float32)
     _check(_lib.paro_synth_randn(ctypes.c_uint64(seed), SZ(count), P(_ptr(out))))
@@ -711,6 +725,25 @@ class Layer:
         ptrs = (ctypes.c_void_p * self.heads)(*[_ptr(x) for x in bufs])
         sizes = (ctypes.c_size_t * self.heads)(*[len(b) for b in blobs])
         _check(_lib.paro_layer_set_masks_pmsk(P(self.ptr), P(stream), ptrs, sizes))
+
+    def set_schedule(self, blobs: Sequence[bytes], resident_lists: int = 0, stream=None) -> None:
+        """One PSCH image per head (paro_layer_set_schedule): resident_lists 0 builds every
+        entry's kept lists now; 2 double-buffers them with a prefetch of t+1."""
+        if len(blobs) != self.heads:
+            raise ShapeError(f"{len(blobs)} schedules for {self.heads} heads")
+        bufs = [np.frombuffer(b, np.uint8).copy() if len(b) else np.zeros(1, np.uint8) for b in blobs]
+        ptrs = (P * len(bufs))(*[P(_ptr(b)) for b in bufs])
+        sizes = (SZ * len(bufs))(*[len(b) for b in blobs])
+        _check(_lib.paro_layer_set_schedule(P(self.ptr), P(stream), ptrs, sizes, U32(resident_lists)))
+
+    def select_timestep(self, t: int, stream=None) -> None:
+        """Make timestep t's masks current (MaskSchedule::at(t), mask.cpp:132-140)."""
+        _check(_lib.paro_layer_select_timestep(P(self.ptr), P(stream), U32(t)))
+
+    def schedule_info(self):
+        T, E, cur = U32(), U32(), ctypes.c_int()
+        _check(_lib.paro_layer_schedule_info(P(self.ptr), ctypes.byref(T), ctypes.byref(E), ctypes.byref(cur)))
+        return T.value, E.value, cur.value
 
     def set_rope(self, cos: Optional[np.ndarray], sin: Optional[np.ndarray], stream=None) -> None:
         """Rotary embedding fused into K1 (paro_layer_set_rope): cos / sin [N - dense_prefix, d]

@@ -301,6 +301,20 @@ struct paro_layer {
     uint8_t* dzero = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr; // H2D / D2H copy streams
     std::vector<cudaEvent_t> ev;                  // [0] start, then per chunk: in, computed, out
+    // per-timestep mask schedule (paro_layer_set_schedule)
+    struct Lists { // K2 outputs of one schedule entry, all heads
+        uint16_t* items = nullptr;
+        uint32_t *pairs = nullptr, *pair_count = nullptr, *qb_count = nullptr, *order = nullptr, *order_chunk = nullptr;
+        int entry = -1;
+        cudaEvent_t ready = nullptr;
+    };
+    uint32_t sched_T = 0, sched_entries = 0, sched_resident = 0;
+    uint8_t* sched_masks = nullptr; // [entries][H][kb][kb] (block bytes, uploaded once)
+    std::vector<Lists> sched_lists; // entries (resident) or 2 (double-buffered prefetch)
+    int sched_cur = -1;             // index into sched_lists of the current timestep's lists
+    cudaStream_t s_k2 = nullptr;    // prefetch stream
+    cudaEvent_t ev_prefetch = nullptr;
+    Lists base;                     // the layer's own K2 buffers (set_masks)
 };
 
 namespace {
@@ -375,7 +389,80 @@ void encode_codes_map(paro_ctx* ctx, CUtensorMap* m, int8_t* base, uint32_t D, u
         fail(PARO_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+// ---------------------------------------------------------------- mask schedules
+static void use_lists(paro_layer* l, const paro_layer::Lists& x) {
+    l->L.items = x.items;
+    l->L.pairs = x.pairs;
+    l->L.pair_count = x.pair_count;
+    l->L.qb_count = x.qb_count;
+    l->L.order = x.order;
+    l->L.order_chunk = x.order_chunk;
+}
+static paro_layer::Lists current_lists(const paro_layer* l) {
+    paro_layer::Lists x;
+    x.items = l->L.items;
+    x.pairs = l->L.pairs;
+    x.pair_count = l->L.pair_count;
+    x.qb_count = l->L.qb_count;
+    x.order = l->L.order;
+    x.order_chunk = l->L.order_chunk;
+    return x;
+}
+static paro_layer::Lists alloc_lists(const LayerDev& L) {
+    paro_layer::Lists x;
+    x.items = dalloc<uint16_t>((size_t)L.H * L.kb * L.kb);
+    x.pairs = dalloc<uint32_t>((size_t)L.H * L.np);
+    x.pair_count = dalloc<uint32_t>((size_t)L.H * L.np);
+    x.qb_count = dalloc<uint32_t>((size_t)L.H * L.kb2);
+    x.order = dalloc<uint32_t>((size_t)L.H * L.np);
+    x.order_chunk = dalloc<uint32_t>((size_t)L.H * L.np);
+    cuda_check(cudaMemset(x.qb_count, 0, (size_t)L.H * L.kb2 * 4), "cudaMemset");
+    cuda_check(cudaEventCreateWithFlags(&x.ready, cudaEventDisableTiming), "event create");
+    return x;
+}
+void clear_schedule(paro_layer* l) {
+    if (!l->sched_T)
+        return;
+    for (auto& x : l->sched_lists) {
+        cudaFree(x.items);
+        cudaFree(x.pairs);
+        cudaFree(x.pair_count);
+        cudaFree(x.qb_count);
+        cudaFree(x.order);
+        cudaFree(x.order_chunk);
+        cudaEventDestroy(x.ready);
+    }
+    l->sched_lists.clear();
+    cudaFree(l->sched_masks);
+    l->sched_masks = nullptr;
+    if (l->s_k2)
+        cudaStreamDestroy(l->s_k2);
+    if (l->ev_prefetch)
+        cudaEventDestroy(l->ev_prefetch);
+    l->s_k2 = nullptr;
+    l->ev_prefetch = nullptr;
+    l->sched_T = l->sched_entries = 0;
+    l->sched_cur = -1;
+    use_lists(l, l->base);
+    l->masks_set = false;
+}
+// K2 of schedule entry e into list buffer x, on stream st
+static void build_entry(paro_layer* l, paro_layer::Lists& x, uint32_t e, cudaStream_t st) {
+    LayerDev tmp = l->L;
+    tmp.items = x.items;
+    tmp.pairs = x.pairs;
+    tmp.pair_count = x.pair_count;
+    tmp.qb_count = x.qb_count;
+    tmp.order = x.order;
+    tmp.order_chunk = x.order_chunk;
+    const size_t per = (size_t)l->L.H * l->L.kb * l->L.kb;
+    cuda_check(paro::launch_k2(tmp, l->sched_masks + (size_t)e * per, st), "k2 launch (schedule)");
+    cuda_check(cudaEventRecord(x.ready, st), "event record");
+    x.entry = (int)e;
+}
+
 void free_layer(paro_layer* l) {
+    clear_schedule(l); // restores the layer's own K2 buffers into l->L
     cudaFree(l->L.perm);
     cudaFree(l->L.q);
     cudaFree(l->L.k);
@@ -532,47 +619,51 @@ int paro_serialize_mask(const uint8_t* bits, uint32_t k_rows, uint32_t k_cols, u
     });
 }
 
+// PSCH (mask.cpp:246-305): magic, u32 timesteps, u32 distinct (= T/2), (u32 t,
+// PMSK) x distinct, shared PMSK. Validates like load_schedule and returns the
+// T/2 + 1 PMSK blobs in at() order: distinct[i] by POSITION (at(t) ignores the
+// stored timestep field, mask.cpp:132-140), then the shared late mask.
+static uint32_t parse_psch(const uint8_t* data, size_t size, std::vector<std::pair<const uint8_t*, size_t>>& ent) {
+    if (size < 12)
+        fail(PARO_E_FORMAT, "truncated schedule header (at byte offset " + std::to_string(size) + ")");
+    if (std::memcmp(data, "PSCH", 4) != 0)
+        fail(PARO_E_FORMAT, "bad magic, expected \"PSCH\" (at byte offset 0)");
+    const uint32_t T = get_u32(data + 4), nd = get_u32(data + 8);
+    if (nd != T / 2)
+        fail(PARO_E_FORMAT, "schedule declares " + std::to_string(nd) + " distinct masks, expected " +
+                                std::to_string(T / 2));
+    ent.clear();
+    size_t off = 12;
+    for (uint32_t i = 0; i < nd; ++i) {
+        if (size < off + 4)
+            fail(PARO_E_FORMAT, "truncated distinct entry (schedule parse position " + std::to_string(off) + ")");
+        off += 4;
+        const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
+        ent.emplace_back(data + off, used);
+        off += used;
+    }
+    const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
+    ent.emplace_back(data + off, used);
+    off += used;
+    if (off != size)
+        fail(PARO_E_FORMAT, std::to_string(size - off) + " trailing bytes (at byte offset " + std::to_string(off) + ")");
+    return T;
+}
+
+// MaskSchedule::at(t) as an entry index into parse_psch's list (mask.cpp:132-140)
+static uint32_t schedule_entry(uint32_t T, uint32_t t) {
+    if (t >= T)
+        fail(PARO_E_INPUT, "timestep " + std::to_string(t) + " out of range, schedule covers " + std::to_string(T));
+    return t < T / 2 ? t : T / 2;
+}
+
 int paro_schedule_at(const uint8_t* data, size_t size, uint32_t t, uint32_t* k_rows, uint32_t* k_cols,
                      uint32_t* block, uint8_t* bits) {
     return guarded([&] {
-        // PSCH (mask.cpp:267-305): magic, u32 timesteps, u32 distinct (= T/2),
-        // (u32 t, PMSK) x distinct, shared PMSK; at(t) (mask.cpp:132-140)
-        if (size < 12)
-            fail(PARO_E_FORMAT, "truncated schedule header (at byte offset " + std::to_string(size) + ")");
-        if (std::memcmp(data, "PSCH", 4) != 0)
-            fail(PARO_E_FORMAT, "bad magic, expected \"PSCH\" (at byte offset 0)");
-        const uint32_t T = get_u32(data + 4), nd = get_u32(data + 8);
-        if (nd != T / 2)
-            fail(PARO_E_FORMAT, "schedule declares " + std::to_string(nd) + " distinct masks, expected " +
-                                    std::to_string(T / 2));
-        size_t off = 12;
-        const uint8_t* want = nullptr;
-        size_t want_size = 0;
-        for (uint32_t i = 0; i < nd; ++i) {
-            if (size < off + 4)
-                fail(PARO_E_FORMAT, "truncated distinct entry (schedule parse position " + std::to_string(off) + ")");
-            off += 4; // the stored timestep field: at(t) ignores it and takes distinct[t] by position
-            const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
-            if (i == t) {
-                want = data + off;
-                want_size = used;
-            }
-            off += used;
-        }
-        const size_t used = decode_pmsk(data + off, size - off, nullptr, nullptr, nullptr, nullptr);
-        const uint8_t* shared = data + off;
-        off += used;
-        if (off != size)
-            fail(PARO_E_FORMAT, std::to_string(size - off) + " trailing bytes (at byte offset " + std::to_string(off) + ")");
-        if (t >= T)
-            fail(PARO_E_INPUT, "timestep " + std::to_string(t) + " out of range, schedule covers " + std::to_string(T));
-        if (t >= T / 2) {
-            want = shared;
-            want_size = used;
-        } else if (!want) {
-            fail(PARO_E_FORMAT, "schedule has no distinct mask for timestep " + std::to_string(t));
-        }
-        decode_pmsk(want, want_size, k_rows, k_cols, block, bits);
+        std::vector<std::pair<const uint8_t*, size_t>> ent;
+        const uint32_t T = parse_psch(data, size, ent);
+        const auto& e = ent[schedule_entry(T, t)];
+        decode_pmsk(e.first, e.second, k_rows, k_cols, block, bits);
     });
 }
 
@@ -1226,6 +1317,7 @@ int paro_layer_destroy(paro_layer* layer) {
 static void set_masks_impl(paro_layer* l, cudaStream_t st, const uint8_t* bits, bool host) {
     check_layer(l);
     set_device(l->ctx);
+    clear_schedule(l); // a plain mask set ends any schedule
     const uint8_t* dbits = nullptr;
     const size_t bytes = (size_t)l->L.H * l->L.kb * l->L.kb;
     if (bits) {
@@ -1297,6 +1389,123 @@ int paro_layer_set_masks_device(paro_layer* layer, paro_stream_t stream, const u
     return guarded([&] { set_masks_impl(layer, (cudaStream_t)stream, device_bits, false); });
 }
 
+int paro_layer_set_schedule(paro_layer* layer, paro_stream_t stream, const uint8_t* const* psch, const size_t* sizes,
+                            uint32_t resident_lists) {
+    return guarded([&] {
+        check_layer(layer);
+        set_device(layer->ctx);
+        const LayerDev& L = layer->L;
+        if (!psch || !sizes)
+            fail(PARO_E_CONFIG, "null PSCH blob list");
+        if (resident_lists != 0 && resident_lists != 2)
+            fail(PARO_E_CONFIG, "resident_lists must be 0 (every entry) or 2 (double-buffered prefetch)");
+        const size_t kk = (size_t)L.kb * L.kb;
+        uint32_t T = 0;
+        std::vector<uint8_t> bits; // [entries][H][kb][kb]
+        std::vector<std::pair<const uint8_t*, size_t>> ent;
+        for (uint32_t h = 0; h < L.H; ++h) {
+            const uint32_t Th = parse_psch(psch[h], sizes[h], ent);
+            if (h == 0) {
+                if (Th == 0)
+                    fail(PARO_E_CONFIG, "schedule covers no timestep");
+                T = Th;
+                bits.assign((size_t)(T / 2 + 1) * L.H * kk, 0);
+            } else if (Th != T) {
+                fail(PARO_E_SHAPE, "head " + std::to_string(h) + ": schedule covers " + std::to_string(Th) +
+                                       " timesteps, head 0 covers " + std::to_string(T));
+            }
+            for (size_t e = 0; e < ent.size(); ++e) {
+                uint32_t kr = 0, kc = 0, block = 0;
+                decode_pmsk(ent[e].first, ent[e].second, &kr, &kc, &block, nullptr);
+                if (block != 64)
+                    fail(PARO_E_CONFIG, "head " + std::to_string(h) + ": mask block " + std::to_string(block) +
+                                            ", the B200 path runs block 64");
+                if (kr != L.kb || kc != L.kb)
+                    fail(PARO_E_SHAPE, "head " + std::to_string(h) + ": mask grid " + std::to_string(kr) + "x" +
+                                           std::to_string(kc) + " does not cover " + std::to_string(L.kb) + "x" +
+                                           std::to_string(L.kb) + " blocks");
+                decode_pmsk(ent[e].first, ent[e].second, &kr, &kc, &block, bits.data() + (e * L.H + h) * kk);
+            }
+        }
+        clear_schedule(layer);
+        layer->base = current_lists(layer);
+        cudaStream_t st = (cudaStream_t)stream;
+        const uint32_t E = T / 2 + 1;
+        layer->sched_masks = dalloc<uint8_t>(bits.size());
+        cuda_check(cudaMemcpyAsync(layer->sched_masks, bits.data(), bits.size(), cudaMemcpyHostToDevice, st),
+                   "schedule upload");
+        cuda_check(cudaStreamSynchronize(st), "schedule upload"); // `bits` is a local host buffer
+        layer->sched_T = T;
+        layer->sched_entries = E;
+        layer->sched_resident = resident_lists;
+        if (resident_lists == 0) { // every entry's kept lists built once
+            for (uint32_t e = 0; e < E; ++e) {
+                layer->sched_lists.push_back(alloc_lists(L));
+                build_entry(layer, layer->sched_lists.back(), e, st);
+            }
+        } else {
+            for (int i = 0; i < 2; ++i)
+                layer->sched_lists.push_back(alloc_lists(L));
+            cuda_check(cudaStreamCreateWithFlags(&layer->s_k2, cudaStreamNonBlocking), "stream create");
+            cuda_check(cudaEventCreateWithFlags(&layer->ev_prefetch, cudaEventDisableTiming), "event create");
+        }
+        layer->sched_cur = -1;
+        layer->masks_set = false; // until a timestep is selected
+    });
+}
+
+int paro_layer_select_timestep(paro_layer* layer, paro_stream_t stream, uint32_t t) {
+    return guarded([&] {
+        check_layer(layer);
+        if (!layer->sched_T)
+            fail(PARO_E_CONFIG, "paro_layer_set_schedule must be called before selecting a timestep");
+        set_device(layer->ctx);
+        cudaStream_t st = (cudaStream_t)stream;
+        const uint32_t e = schedule_entry(layer->sched_T, t);
+        auto& lists = layer->sched_lists;
+        int cur = -1;
+        if (layer->sched_resident == 0) {
+            cur = (int)e;
+        } else {
+            for (int i = 0; i < 2; ++i)
+                if (lists[i].entry == (int)e)
+                    cur = i;
+            if (cur >= 0) { // prefetched (or current): order this stream after its K2
+                cuda_check(cudaStreamWaitEvent(st, lists[cur].ready, 0), "stream wait");
+            } else { // not prefetched (first call, or a jump): build it now on the caller's stream
+                cur = layer->sched_cur == 0 ? 1 : 0;
+                build_entry(layer, lists[cur], e, st);
+            }
+            // prefetch t+1's lists into the other buffer on the side stream, after the
+            // work already queued here (the previous step still reads that buffer)
+            if (t + 1 < layer->sched_T) {
+                const uint32_t e1 = schedule_entry(layer->sched_T, t + 1);
+                auto& other = lists[1 - cur];
+                if (e1 != e && other.entry != (int)e1) {
+                    cuda_check(cudaEventRecord(layer->ev_prefetch, st), "event record");
+                    cuda_check(cudaStreamWaitEvent(layer->s_k2, layer->ev_prefetch, 0), "stream wait");
+                    build_entry(layer, other, e1, layer->s_k2);
+                }
+            }
+        }
+        layer->sched_cur = cur;
+        use_lists(layer, lists[cur]);
+        layer->masks_set = true;
+    });
+}
+
+int paro_layer_schedule_info(const paro_layer* layer, uint32_t* timesteps, uint32_t* entries, int* current_entry) {
+    return guarded([&] {
+        check_layer(layer);
+        if (timesteps)
+            *timesteps = layer->sched_T;
+        if (entries)
+            *entries = layer->sched_entries;
+        if (current_entry)
+            *current_entry = layer->sched_cur >= 0 ? layer->sched_lists[layer->sched_cur].entry : -1;
+    });
+}
+
 int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,
                                 const float* v, int v_bits) {
     return guarded([&] {
@@ -1346,8 +1555,23 @@ int paro_layer_set_pipeline_chunks(paro_layer* layer, paro_stream_t stream, uint
         LayerDev& L = layer->L;
         const uint32_t c = std::min(std::min(chunks, L.H), paro::kMaxChunks);
         set_chunks(L, (L.H + c - 1) / c, false);
-        if (layer->masks_set) // re-sort the per-chunk work lists for the new split
+        if (layer->sched_T) { // re-sort every built schedule entry's per-chunk lists
+            for (auto& x : layer->sched_lists) {
+                if (x.entry < 0)
+                    continue;
+                LayerDev tmp = L;
+                tmp.pairs = x.pairs;
+                tmp.pair_count = x.pair_count;
+                tmp.qb_count = x.qb_count;
+                tmp.order = x.order;
+                tmp.order_chunk = x.order_chunk;
+                cuda_check(cudaStreamWaitEvent((cudaStream_t)stream, x.ready, 0), "stream wait");
+                cuda_check(paro::launch_k2_order(tmp, (cudaStream_t)stream), "k2 order launch");
+                cuda_check(cudaEventRecord(x.ready, (cudaStream_t)stream), "event record");
+            }
+        } else if (layer->masks_set) { // re-sort the per-chunk work lists for the new split
             cuda_check(paro::launch_k2_order(L, (cudaStream_t)stream), "k2 order launch");
+        }
     });
 }
 
