@@ -66,6 +66,19 @@ int paro_make_perm(int ndim, const char* labels, const uint32_t* extents, const 
  * count*ndim chars (no terminators); count = ndim! (<= 6). */
 int paro_enumerate_orders(int ndim, const char* labels, char* orders, int* count);
 
+/* load_plan_file (reorder.cpp:193-216) on an in-memory plan text ("head_id,order"
+ * lines; `name` prefixes FormatError messages like the file path does). Query
+ * with heads/orders NULL: *count entries, *orders_size bytes for the orders
+ * (each NUL-terminated, in file order). */
+int paro_parse_plan(const char* text, size_t len, const char* name, uint32_t* count, uint32_t* heads, char* orders,
+                    size_t* orders_size);
+/* plan_for_head (tools/main.cpp:118-126) for n heads: text NULL -> identity
+ * order; else the first entry naming each head (InputError "<name>: no plan
+ * entry for head h" when none), validated as make_perm does. orders_out: n*ndim
+ * chars, ready for paro_layer_create. */
+int paro_plan_for_heads(const char* text, size_t len, const char* name, const char* grid_text, uint32_t n,
+                        const uint32_t* head_ids, char* orders_out);
+
 /* PMSK blob decode -- replaces paro::deserialize_mask (mask.hpp:74,
  * mask.cpp:217-244). bits (k_rows*k_cols bytes, row-major) may be NULL to
  * query the header; consumed may be NULL. */

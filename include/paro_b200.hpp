@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <fstream>
+#include <iterator>
 #include <memory>
 #include <string>
 #include <vector>
@@ -76,6 +78,45 @@ inline paro::PermPlan make_perm(const paro::TokenGrid& grid, const std::string& 
     p.inverse.resize(grid.token_count());
     check(paro_make_perm((int)grid.ndim(), labels, ext, order.c_str(), p.forward.data(), p.inverse.data()));
     return p;
+}
+
+// load_plan_file (reorder.hpp:74, reorder.cpp:193-216)
+inline std::vector<std::pair<std::uint32_t, std::string>> load_plan_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f)
+        throw paro::IoError("cannot open '" + path + "' for reading");
+    const std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    uint32_t n = 0;
+    size_t bytes = 0;
+    check(paro_parse_plan(text.data(), text.size(), path.c_str(), &n, nullptr, nullptr, &bytes));
+    std::vector<uint32_t> heads(n ? n : 1);
+    std::vector<char> orders(bytes ? bytes : 1);
+    check(paro_parse_plan(text.data(), text.size(), path.c_str(), &n, heads.data(), orders.data(), &bytes));
+    std::vector<std::pair<std::uint32_t, std::string>> out;
+    for (size_t i = 0, o = 0; i < n; ++i) {
+        out.emplace_back(heads[i], std::string(orders.data() + o));
+        o += out.back().second.size() + 1;
+    }
+    return out;
+}
+
+// plan_for_head (tools/main.cpp:118-126): identity without a plan file, the head's
+// entry otherwise (InputError when the plan does not name the head)
+inline paro::PermPlan plan_for_head(const std::string& plan_path, const paro::TokenGrid& grid, std::uint32_t head) {
+    std::string text;
+    if (!plan_path.empty()) {
+        std::ifstream f(plan_path, std::ios::binary);
+        if (!f)
+            throw paro::IoError("cannot open '" + plan_path + "' for reading");
+        text.assign((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    }
+    std::string gt;
+    for (const auto& a : grid.axes)
+        gt += (gt.empty() ? "" : ",") + std::string(1, a.label) + ":" + std::to_string(a.extent);
+    std::string order(grid.ndim(), '\0');
+    check(paro_plan_for_heads(plan_path.empty() ? nullptr : text.data(), text.size(), plan_path.c_str(), gt.c_str(), 1,
+                              &head, order.data()));
+    return paro_b200::make_perm(grid, order);
 }
 
 // deserialize_mask (mask.hpp:74, mask.cpp:217-244)

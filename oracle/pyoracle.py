@@ -434,6 +434,23 @@ class Reference:
                                    _ptr(out))
         return out
 
+    def load_plan_file(self, path):
+        """(rc, [(head, order)], error message) of the reference's load_plan_file."""
+        cnt = U32()
+        rc = self.lib.ref_load_plan_file(path.encode(), ctypes.byref(cnt), None, None)
+        if rc:
+            return rc, None, self.lib.ref_last_error().decode()
+        heads = np.empty(max(1, cnt.value), np.uint32)
+        orders = ctypes.create_string_buffer(8 * max(1, cnt.value))
+        self.lib.ref_load_plan_file(path.encode(), ctypes.byref(cnt), _ptr(heads), orders)
+        return 0, [(int(heads[i]), orders.raw[8 * i:8 * i + 8].rstrip(b"\0").decode()) for i in range(cnt.value)], ""
+
+    def plan_for_head(self, path, grid_text, head, n):
+        """(rc, inverse permutation, error message) of tools/main.cpp plan_for_head."""
+        inv = np.empty(n, np.uint32)
+        rc = self.lib.ref_plan_for_head(path.encode() if path else None, grid_text.encode(), U32(head), _ptr(inv))
+        return rc, (inv if rc == 0 else None), (self.lib.ref_last_error().decode() if rc else "")
+
     def synth_randn_streams(self, seed0, stride, nstreams, count, threads=0):
         """[nstreams, count] N(0,1) values, stream s seeded seed0 + stride*s (synth.cpp:20-22, 173-182)."""
         out = np.empty((nstreams, count), np.float32)

@@ -305,6 +305,47 @@ void ref_test_values(uint64_t state, size_t count, float* out) {
         out[i] = oracle::test_value(state);
 }
 
+// load_plan_file (reorder.cpp:193-216) -> count entries; heads[] and orders
+// (count * 8 chars, NUL-padded) may be NULL to query the count
+int ref_load_plan_file(const char* path, uint32_t* count, uint32_t* heads, char* orders) {
+    return guarded([&] {
+        auto e = paro::load_plan_file(path);
+        *count = (uint32_t)e.size();
+        for (size_t i = 0; i < e.size(); ++i) {
+            if (heads)
+                heads[i] = e[i].first;
+            if (orders) {
+                std::memset(orders + 8 * i, 0, 8);
+                std::memcpy(orders + 8 * i, e[i].second.data(), std::min<size_t>(7, e[i].second.size()));
+            }
+        }
+    });
+}
+
+// plan_for_head of tools/main.cpp:118-126 (the CLI helper is not in the library;
+// its five lines are restated here over the library's load_plan_file / make_perm)
+int ref_plan_for_head(const char* path, const char* grid_text, uint32_t head, uint32_t* inverse) {
+    return guarded([&] {
+        const paro::TokenGrid grid = paro::parse_grid(grid_text);
+        paro::PermPlan plan;
+        const std::string p = path ? path : "";
+        if (p.empty()) {
+            plan = paro::make_perm(grid, grid.label_string());
+        } else {
+            bool found = false;
+            for (const auto& [h, order] : paro::load_plan_file(p))
+                if (h == head) {
+                    plan = paro::make_perm(grid, order);
+                    found = true;
+                    break;
+                }
+            if (!found)
+                throw paro::InputError(p + ": no plan entry for head " + std::to_string(head));
+        }
+        std::memcpy(inverse, plan.inverse.data(), plan.inverse.size() * 4);
+    });
+}
+
 // N(0,1) stream of the reference's synthetic generator: std::mt19937_64 seeded
 // with `seed`, the documented uniform (rng() >> 11) * 2^-53 (synth.cpp:20-22) and
 // Box-Muller on (1 - u1, u2), one value per pair (synth.cpp:173-182; that

@@ -258,6 +258,49 @@ def schedule_at(data: bytes, t: int) -> BlockMask:
     return BlockMask(kr.value, kc.value, b.value, bits)
 
 
+def parse_plan(text: bytes, name: str = "plan"):
+    """load_plan_file (reorder.cpp:193-216) on plan text: [(head, order)] in file order."""
+    cnt, size = U32(), SZ()
+    _check(_lib.paro_parse_plan(text, SZ(len(text)), name.encode(), ctypes.byref(cnt), None, None, ctypes.byref(size)))
+    heads = np.empty(max(1, cnt.value), np.uint32)
+    buf = ctypes.create_string_buffer(max(1, size.value))
+    _check(_lib.paro_parse_plan(text, SZ(len(text)), name.encode(), ctypes.byref(cnt), P(_ptr(heads)), buf,
+                                ctypes.byref(size)))
+    orders = buf.raw[:size.value].split(b"\0")[:cnt.value]
+    return [(int(heads[i]), orders[i].decode()) for i in range(cnt.value)]
+
+
+def load_plan_file(path: str):
+    """[(head, order)] of a plan file (IoError when it cannot be read, like the reference)."""
+    try:
+        with open(path, "rb") as f:
+            text = f.read()
+    except OSError:
+        raise IoError(f"cannot open '{path}' for reading") from None
+    return parse_plan(text, path)
+
+
+def plan_orders(plan_path: Optional[str], grid: "TokenGrid | str", heads: Sequence[int]) -> list:
+    """plan_for_head (tools/main.cpp:118-126) for each head: no plan file -> the identity
+    order; else the head's entry (InputError when missing). Orders for Layer()."""
+    text = None
+    name = plan_path or "plan"
+    if plan_path:
+        try:
+            with open(plan_path, "rb") as f:
+                text = f.read()
+        except OSError:
+            raise IoError(f"cannot open '{plan_path}' for reading") from None
+    gtext = grid if isinstance(grid, str) else grid.text()
+    ids = np.ascontiguousarray(list(heads), np.uint32)
+    nd = len(parse_grid(gtext).labels)
+    out = ctypes.create_string_buffer(max(1, len(ids) * nd))
+    _check(_lib.paro_plan_for_heads(text, SZ(len(text) if text is not None else 0), name.encode(), gtext.encode(),
+                                    U32(len(ids)), P(_ptr(ids)) if len(ids) else None, out))
+    raw = out.raw[:len(ids) * nd].decode()
+    return [raw[i * nd:(i + 1) * nd] for i in range(len(ids))]
+
+
 def serialize_schedule(timesteps: int, masks: Sequence["BlockMask"]) -> bytes:
     """PSCH image of a schedule (save_schedule, mask.cpp:246-263): `masks` holds the
     timesteps//2 distinct masks (timestep i = position i) and then the shared late mask."""

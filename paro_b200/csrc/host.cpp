@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cerrno>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -565,6 +567,99 @@ int paro_make_perm(int ndim, const char* labels, const uint32_t* extents, const 
             const uint32_t old = paro::perm_src(pd, (uint32_t)i);
             inverse[i] = old;
             forward[old] = (uint32_t)i;
+        }
+    });
+}
+
+// ---------------------------------------------------------------- per-head plan text
+// load_plan_file (reorder.cpp:193-216) on an in-memory image: one "head_id,order"
+// per line, empty lines skipped; the head id parses like std::stoul (leading
+// blanks, sign, trailing text allowed; no digits or out of range -> "bad head id");
+// the order is the text after the first comma (validated when a plan is made).
+namespace {
+struct PlanEntry {
+    uint32_t head;
+    std::string order;
+};
+std::vector<PlanEntry> parse_plan(const char* text, size_t len, const std::string& name) {
+    std::vector<PlanEntry> out;
+    size_t pos = 0, lineno = 0;
+    while (pos < len) {
+        size_t end = pos;
+        while (end < len && text[end] != '\n')
+            ++end;
+        const std::string line(text + pos, end - pos);
+        pos = end + 1;
+        ++lineno;
+        if (line.empty())
+            continue;
+        const size_t comma = line.find(',');
+        if (comma == std::string::npos)
+            fail(PARO_E_FORMAT, name + ":" + std::to_string(lineno) + ": expected head_id,order");
+        const std::string id = line.substr(0, comma);
+        errno = 0;
+        char* stop = nullptr;
+        const unsigned long v = std::strtoul(id.c_str(), &stop, 10);
+        if (stop == id.c_str() || errno == ERANGE)
+            fail(PARO_E_FORMAT, name + ":" + std::to_string(lineno) + ": bad head id");
+        out.push_back({static_cast<uint32_t>(v), line.substr(comma + 1)});
+    }
+    return out;
+}
+} // namespace
+
+int paro_parse_plan(const char* text, size_t len, const char* name, uint32_t* count, uint32_t* heads, char* orders,
+                    size_t* orders_size) {
+    return guarded([&] {
+        const auto e = parse_plan(text ? text : "", text ? len : 0, name ? name : "plan");
+        size_t need = 0;
+        for (const auto& x : e)
+            need += x.order.size() + 1;
+        *count = (uint32_t)e.size();
+        if (orders_size) {
+            if (orders && *orders_size < need)
+                fail(PARO_E_CONFIG, "plan orders buffer too small");
+            *orders_size = need;
+        }
+        if (heads)
+            for (size_t i = 0; i < e.size(); ++i)
+                heads[i] = e[i].head;
+        if (orders) {
+            size_t o = 0;
+            for (const auto& x : e) {
+                std::memcpy(orders + o, x.order.c_str(), x.order.size() + 1);
+                o += x.order.size() + 1;
+            }
+        }
+    });
+}
+
+int paro_plan_for_heads(const char* text, size_t len, const char* name, const char* grid_text, uint32_t n,
+                        const uint32_t* head_ids, char* orders_out) {
+    return guarded([&] {
+        // plan_for_head (tools/main.cpp:118-126): no plan -> identity (the grid's own
+        // label order); otherwise the first entry naming the head, else InputError
+        Grid g = parse_grid_text(grid_text);
+        const std::string ident(g.labels, g.labels + g.ndim);
+        std::vector<PlanEntry> e;
+        const std::string nm = name ? name : "plan";
+        if (text)
+            e = parse_plan(text, len, nm);
+        for (uint32_t i = 0; i < n; ++i) {
+            std::string order = ident;
+            if (text) {
+                const PlanEntry* hit = nullptr;
+                for (const auto& x : e)
+                    if (x.head == head_ids[i]) {
+                        hit = &x;
+                        break;
+                    }
+                if (!hit)
+                    fail(PARO_E_INPUT, nm + ": no plan entry for head " + std::to_string(head_ids[i]));
+                order = hit->order;
+            }
+            perm_desc(g, order); // make_perm's validation of the order (ConfigError / InputError)
+            std::memcpy(orders_out + (size_t)i * ident.size(), order.data(), ident.size());
         }
     });
 }

@@ -71,6 +71,17 @@ static void host_tests() {
     paro::TokenGrid cube({{'F', 4}, {'H', 4}, {'W', 4}});
     CHECK_THROWS_AS(paro_b200::make_perm(cube, "FH"), paro::ConfigError);
     CHECK_THROWS_AS(paro_b200::make_perm(cube, "FHX"), paro::InputError);
+    // per-head plan files: the reference's writer, our reader and plan_for_head (a3)
+    {
+        const std::string path = "/tmp/paro_adapter_test.plan";
+        paro::save_plan_file({{0, "WHF"}, {2, "HFW"}, {2, "FHW"}}, path);
+        CHECK(paro_b200::load_plan_file(path) == paro::load_plan_file(path));
+        CHECK(paro_b200::plan_for_head(path, cube, 2).inverse == paro::make_perm(cube, "HFW").inverse);
+        CHECK(paro_b200::plan_for_head("", cube, 9).inverse == paro::make_perm(cube, "FHW").inverse);
+        CHECK_THROWS_AS(paro_b200::plan_for_head(path, cube, 1), paro::InputError);
+        CHECK_THROWS_AS(paro_b200::load_plan_file("/nonexistent/x.plan"), paro::IoError);
+        std::remove(path.c_str());
+    }
     // PMSK decode (mask.cpp:217-244)
     std::mt19937 g(3);
     for (auto [kr, kc] : {std::pair<size_t, size_t>{33, 17}, {275, 275}, {1, 1}}) {
