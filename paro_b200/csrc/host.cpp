@@ -265,6 +265,7 @@ size_t decode_pmsk(const uint8_t* data, size_t size, uint32_t* kr, uint32_t* kc,
 struct paro_ctx {
     int device = 0;
     int num_sms = 0;
+    size_t l2_bytes = 0;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     char* pinned = nullptr; // host staging of select_permutation, grown on demand
     size_t pinned_bytes = 0;
@@ -1239,6 +1240,7 @@ int paro_ctx_create(int device, paro_ctx** out) {
         auto* c = new paro_ctx;
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
+        c->l2_bytes = (size_t)prop.l2CacheSize;
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
         cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
@@ -1376,6 +1378,16 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
             L.order = dalloc<uint32_t>((size_t)heads * L.np);
             L.order_chunk = dalloc<uint32_t>((size_t)heads * L.np);
             set_chunks(L, default_heads_per_chunk(heads, N, head_dim), true);
+            // L2 groups of the whole-layer work order: as many heads as keep their
+            // K + V codes within half of L2 (c2: 27 of 48 heads, c5: 3 of 40);
+            // PARO_L2_GROUP_HEADS overrides (0 = one global LPT order)
+            {
+                const size_t kv = (size_t)L.kb2 * 64 * head_dim * 2;
+                size_t g = std::max<size_t>(1, (ctx->l2_bytes / 2) / std::max<size_t>(kv, 1));
+                if (const char* e = getenv("PARO_L2_GROUP_HEADS"))
+                    g = (size_t)atoi(e);
+                L.l2_group = (uint32_t)std::min<size_t>(g, heads);
+            }
             L.work_counter = dalloc<uint32_t>(1);
             l->fwd = dalloc<uint32_t>((size_t)heads * N);
             l->inv = dalloc<uint32_t>((size_t)heads * N);

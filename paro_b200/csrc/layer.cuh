@@ -63,6 +63,7 @@ struct LayerDev {
     uint32_t nchunks;      // host-buffer pipeline chunks (<= kMaxChunks)
     uint32_t chunk_start[65];
     uint32_t* work_counter;
+    uint32_t l2_group;     // heads per L2 group of the whole-layer LPT order (0: one group)
     // dense text-token prefix (AttnInputs::dense_prefix): dp rows / tokens, nd =
     // ceil(dp/64) dense key tiles; K4 hands K3 each non-dense row's running
     // state after the dense tiles: m (fp64), l, acc [H][kb2*64][(D)]

@@ -457,15 +457,26 @@ __global__ void __launch_bounds__(256) k2_pair_qblocks(LayerDev L) {
 // into L.order; block c >= 1 sorts the items of chunk c-1's heads into
 // the same span of L.order_chunk (the chunked host-buffer pipeline runs K3
 // once per chunk).
+// Block 0's whole-layer order is LPT inside consecutive groups of L.l2_group heads
+// (all heads when 0): the persistent K3 CTAs then work on about one group at a
+// time, whose K/V codes the host sized to half of L2, so the K/V tiles re-read by
+// every q-block pair of a head stay L2-resident instead of streaming from HBM.
+__device__ void k2_lpt_range(const LayerDev& L, uint32_t h0, uint32_t h1, uint32_t* out, uint32_t* s_hist);
+
 __global__ void __launch_bounds__(1024) k2_work_order(LayerDev L) {
     extern __shared__ uint32_t s_hist[]; // kb + 1 buckets
-    uint32_t h0 = 0, h1 = L.H;
-    uint32_t* out = L.order;
     if (blockIdx.x > 0) {
-        h0 = L.chunk_start[blockIdx.x - 1];
-        h1 = L.chunk_start[blockIdx.x];
-        out = L.order_chunk;
+        k2_lpt_range(L, L.chunk_start[blockIdx.x - 1], L.chunk_start[blockIdx.x], L.order_chunk, s_hist);
+        return;
     }
+    const uint32_t g = L.l2_group ? L.l2_group : L.H;
+    for (uint32_t h0 = 0; h0 < L.H; h0 += g) {
+        k2_lpt_range(L, h0, h0 + g < L.H ? h0 + g : L.H, L.order, s_hist);
+        __syncthreads();
+    }
+}
+
+__device__ void k2_lpt_range(const LayerDev& L, uint32_t h0, uint32_t h1, uint32_t* out, uint32_t* s_hist) {
     const uint32_t first = h0 * L.np, total = (h1 - h0) * L.np;
     const uint32_t* key_of = L.pair_count + first;
     out += first;
