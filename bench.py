@@ -69,6 +69,8 @@ def parse_args():
                          "runs timestep i %% T with its kept lists resident, no K2 in the step")
     ap.add_argument("--schedule-prefetch", action="store_true",
                     help="with --schedule: two list buffers, K2 of t+1 on a side stream during step t")
+    ap.add_argument("--v-packed", action="store_true",
+                    help="INT4 V nibble-packed in HBM, unpacked to i8 in shared memory by K3 (paro_layer_set_v_packing)")
     ap.add_argument("--rope", action="store_true",
                     help="diagnostic: rotary embedding fused into K1 (paro_layer_set_rope); BASELINE configs do not rotate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -531,6 +533,8 @@ def main():
     total_ops = sum(kept_ops(all_masks[h], N, d) for h in range(H))
 
     layer = paro.Layer(ctx, hpr, d, g, my_orders, dense_prefix=args.dense_prefix)
+    if args.v_packed:
+        layer.set_v_packing(True)
     if args.rope:  # diffusers-style real tables, one row per grid token (L2-resident across heads)
         ang = np.repeat(np.arange(g.token_count(), dtype=np.float64)[:, None]
                         * (10000.0 ** (-np.arange(d // 2) / (d // 2)))[None, :], 2, axis=1)
@@ -662,6 +666,8 @@ def main():
         "dtype_detail": "QK s8*s8->s32 and PV u8(u4 codes)*s8->s32 on tcgen05; fp32 softmax / dequant, fp64 row extremes",
         "data": "synthetic N(0,1) Q/K/V (MT19937-64 Box-Muller), K5 gen_mask masks (GPU)",
         "config": {**bench_config(args.config, args.mask_family, all_masks, world, args.dense_prefix, args.rope),
+                   **({"v_storage": "INT4 nibble-packed in HBM, unpacked in smem"} if args.v_packed and pv_bits == 4
+                      else {}),
                    **({"schedule": f"{args.schedule} timesteps, PSCH per head, kept lists "
                                    + ("double-buffered, K2 of t+1 prefetched on a side stream" if args.schedule_prefetch
                                       else "of every entry resident (no K2 in the step)")} if args.schedule else {})},

@@ -289,6 +289,15 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
 int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float* q, const float* k, const float* v,
                             float scale, int pv_bits, float* out, uint8_t* zeroed);
 
+/* INT4 V storage: packed = 1 stores 4-bit V codes two per
+ * byte in HBM (low nibble first, two's complement -- the PARQ payload layout) and K3
+ * unpacks each tile to i8 in shared memory for the kind::i8 P.V MMA (Blackwell has
+ * no INT4 MMA); 0 (default; PARO_V_PACKED=1 flips it) keeps one code per byte, which
+ * K3 feeds to the MMA directly. Measured (round 2): packing halves V's footprint
+ * (c5: 387 -> 194 MB) and costs K3 14-19% (the unpack competes with the softmax
+ * for issue slots; K3 is not HBM-bound). Applies from the next reorder_quantize. */
+int paro_layer_set_v_packing(paro_layer* layer, int packed);
+
 /* Number of head chunks forward_host pipelines (clamped to [1, heads]).
  * Re-sorts the per-chunk work lists on `stream` if masks are already set. */
 int paro_layer_set_pipeline_chunks(paro_layer* layer, paro_stream_t stream, uint32_t chunks);
@@ -301,12 +310,16 @@ typedef struct {
     uint32_t groups;   /* head_dim/64 column groups of Q/K */
     int8_t* q_codes;   /* [H, kb2*64, d] int8 */
     int8_t* k_codes;   /* [H, kb2*64, d] int8 */
-    int8_t* v_codes;   /* [H, kb2*64, d] int8 (within +-qmax of the v_bits used) */
+    int8_t* v_codes;   /* [H, kb2*64, d] int8 codes; with v_packed: [H, kb2*64, d/2] bytes, two
+                          two's-complement INT4 codes per byte, low nibble = even column
+                          (the PARQ payload layout, quant.cpp:237-243) */
     float* q_scales;   /* [H, kb2, groups] */
     float* tile_meta;  /* [H, kb2, 4+d]: k_scale[g0], k_scale[g1] (0 if d=64), v_scale, 0,
                           v_colsum[d] (exact integers in fp32) */
     uint32_t* inverse; /* [H, N] device perm tables (filled at create) */
     uint32_t* forward; /* [H, N] */
+    uint32_t v_bits;   /* V code width of the last reorder_quantize (0: none yet) */
+    uint32_t v_packed; /* 1: v_codes hold nibble-packed INT4 (paro_layer_set_v_packing) */
 } paro_layer_buffers;
 int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out);
 

@@ -301,6 +301,19 @@ def plan_orders(plan_path: Optional[str], grid: "TokenGrid | str", heads: Sequen
     return [raw[i * nd:(i + 1) * nd] for i in range(len(ids))]
 
 
+def unpack_nibbles(packed: np.ndarray) -> np.ndarray:
+    """Two's-complement INT4 pairs, low nibble first (quant.cpp:237-243, 313-318) -> int8."""
+    p = np.asarray(packed, np.uint8)
+    lo = (p & 0x0F).astype(np.int8)
+    hi = (p >> 4).astype(np.int8)
+    lo = np.where(lo > 7, lo - 16, lo).astype(np.int8)
+    hi = np.where(hi > 7, hi - 16, hi).astype(np.int8)
+    out = np.empty(p.shape[:-1] + (2 * p.shape[-1],), np.int8)
+    out[..., 0::2] = lo
+    out[..., 1::2] = hi
+    return out
+
+
 def serialize_schedule(timesteps: int, masks: Sequence["BlockMask"]) -> bytes:
     """PSCH image of a schedule (save_schedule, mask.cpp:246-263): `masks` holds the
     timesteps//2 distinct masks (timestep i = position i) and then the shared late mask."""
@@ -547,7 +560,7 @@ class _Buffers(ctypes.Structure):
     _fields_ = [
         ("heads", U32), ("tokens", U32), ("head_dim", U32), ("kblocks", U32), ("kblocks_padded", U32),
         ("groups", U32), ("q_codes", P), ("k_codes", P), ("v_codes", P), ("q_scales", P), ("tile_meta", P),
-        ("inverse", P), ("forward", P),
+        ("inverse", P), ("forward", P), ("v_bits", U32), ("v_packed", U32),
     ]
 
 
@@ -779,6 +792,11 @@ class Layer:
         sizes = (SZ * len(bufs))(*[len(b) for b in blobs])
         _check(_lib.paro_layer_set_schedule(P(self.ptr), P(stream), ptrs, sizes, U32(resident_lists)))
 
+    def set_v_packing(self, packed: bool) -> None:
+        """INT4 V nibble-packed in HBM and unpacked to i8 in shared memory by K3
+        (paro_layer_set_v_packing); from the next reorder_quantize."""
+        _check(_lib.paro_layer_set_v_packing(P(self.ptr), ctypes.c_int(1 if packed else 0)))
+
     def select_timestep(self, t: int, stream=None) -> None:
         """Make timestep t's masks current (MaskSchedule::at(t), mask.cpp:132-140)."""
         _check(_lib.paro_layer_select_timestep(P(self.ptr), P(stream), U32(t)))
@@ -847,7 +865,9 @@ class Layer:
         return {
             "q": download_ptr(b.q_codes, (H, rows, D), np.int8),
             "k": download_ptr(b.k_codes, (H, rows, D), np.int8),
-            "v": download_ptr(b.v_codes, (H, rows, D), np.int8),
+            "v": (unpack_nibbles(download_ptr(b.v_codes, (H, rows, D // 2), np.uint8)) if b.v_packed
+                  else download_ptr(b.v_codes, (H, rows, D), np.int8)),
+            "v_packed": download_ptr(b.v_codes, (H, rows, D // 2), np.uint8) if b.v_packed else None,
             "q_scales": download_ptr(b.q_scales, (H, kb2, b.groups), np.float32),
             "meta": download_ptr(b.tile_meta, (H, kb2, 4 + D), np.float32),
             "inverse": download_ptr(b.inverse, (H, b.tokens), np.uint32),

@@ -90,9 +90,16 @@ struct K3Cfg {
     static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
     static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 16) : 0); // + int4 S pairs
     // exact path: per compute warp, its risky (owner lane, group) list (<= 32 x 16 entries)
-    static constexpr uint32_t OFF_BAR = OFF_XLIST + NCW * 512 * 2;
-    static constexpr uint32_t NBAR = 2 + 2 * NS + 21; // == Bars<NS>::COUNT (static_assert below)
-    static constexpr uint32_t NCONS = 9; // warps reading the item queue: MMA + 8 (softmax + epilogue | compute)
+    // INT4 V arrives nibble-packed (D/2 bytes per key row); d = 64 unpacks it in place
+    // (the packed tile lands in the upper half of its V tile), d = 128 from this staging
+    static constexpr uint32_t VPK_BYTES = 64 * D / 2;
+    static constexpr uint32_t OFF_VPK = OFF_XLIST + NCW * 512 * 2; // d = 128: [NS][2 side] packed V tiles
+    static constexpr uint32_t OFF_BAR = OFF_VPK + (SPLIT ? NS * 2 * VPK_BYTES : 0);
+    static constexpr uint32_t NBAR = 2 + 3 * NS + 21; // == Bars<NS>::COUNT (static_assert below)
+    // warps reading the item queue: MMA + 8 (softmax + epilogue | compute) + at d = 128
+    // the two warpgroup-0 warps that unpack INT4 V (one side each)
+    static constexpr uint32_t NCONS = SPLIT ? 11 : 9;
+    static constexpr uint32_t NVFULL = SPLIT ? 2 : 1; // arrivals per VFULL phase
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
     static constexpr uint32_t SMEM_BYTES = OFF_TMEMPTR + 16;
     // swizzle: rows of D int8 -> 64B (D=64) or 128B (D=128) swizzle atoms of 8 rows
@@ -110,7 +117,8 @@ struct Bars {
                               PFULL = SEMPTY + 2, PEMPTY = PFULL + 2, OFULL = PEMPTY + 2, OEMPTY = OFULL + 2,
                               LFULL = OEMPTY + 2, LEMPTY = LFULL + 1, RED = LEMPTY + 1,
                               QFULL1 = RED + 1, QEMPTY1 = RED + 2, ITEMFULL = QEMPTY1 + 1, ITEMEMPTY = ITEMFULL + 2,
-                              COUNT = ITEMEMPTY + 2;
+                              VFULL = ITEMEMPTY + 2, // packed INT4 V of a stage unpacked (producer)
+                              COUNT = VFULL + NS;
 };
 static_assert(Bars<K3Cfg<64>::NS>::COUNT == K3Cfg<64>::NBAR && Bars<K3Cfg<128>::NS>::COUNT == K3Cfg<128>::NBAR,
               "mbarrier block must hold every barrier (the TMEM pointer slot follows it)");
@@ -756,12 +764,76 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     pscale_out = pscale;
 }
 
+// INT4 V: one 64-key tile from its nibble-packed form (row r: D/2 bytes, byte b =
+// columns 2b (low nibble) and 2b+1, two's complement) into the i8 tile of the P.V
+// MMA's B operand (rows of D bytes, 64B / 128B swizzle), by the 32 lanes of a warp.
+// d = 64 unpacks in place (the packed tile sits in the upper half of the output
+// tile: every lane reads its two rows before any lane writes).
+// nibble n -> byte sext(n) in every byte lane without cross-byte carries:
+// ((n ^ 8) + 0x78) ^ 0x80 = (n ^ 8) - 8 (the sum stays within 0x78..0x87)
+__device__ __forceinline__ uint32_t sext_nibbles(uint32_t n4) {
+    return ((n4 ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+}
+__device__ __forceinline__ void nib8(uint32_t w, uint32_t& o0, uint32_t& o1) {
+    const uint32_t lo = sext_nibbles(w & 0x0F0F0F0Fu), hi = sext_nibbles((w >> 4) & 0x0F0F0F0Fu);
+    o0 = __byte_perm(lo, hi, 0x5140); // columns 0..3 of the word's 8
+    o1 = __byte_perm(lo, hi, 0x7362); // columns 4..7
+}
+template <int D>
+__device__ __forceinline__ void unpack_v_tile(const uint8_t* pk, uint8_t* vt, uint32_t lane) {
+    if (D == 64) {
+        uint4 w[4]; // rows 2 lane, 2 lane + 1: 32 packed bytes each
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            w[i] = *reinterpret_cast<const uint4*>(pk + lane * 64 + i * 16);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t r = 2 * lane + k;
+            uint8_t* row = vt + (r >> 3) * 512 + (r & 7) * 64;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { // 16-column chunk c <- packed words 2c, 2c+1 of the row
+                const uint4& src = w[2 * k + (c >> 1)];
+                const uint32_t wa = (c & 1) ? src.z : src.x, wb = (c & 1) ? src.w : src.y;
+                uint4 o;
+                nib8(wa, o.x, o.y);
+                nib8(wb, o.z, o.w);
+                *reinterpret_cast<uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4)) = o;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) { // rows lane, lane + 32: 64 packed bytes each
+            const uint32_t r = lane + 32 * k;
+            uint8_t* row = vt + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 src = *reinterpret_cast<const uint4*>(pk + r * 64 + q * 16);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = 2 * q + h;
+                    uint4 o;
+                    nib8(h ? src.z : src.x, o.x, o.y);
+                    nib8(h ? src.w : src.y, o.z, o.w);
+                    *reinterpret_cast<uint4*>(row + ((c ^ (r & 7)) << 4)) = o;
+                }
+            }
+        }
+    }
+}
+
 // DUMP: the P-code dump test hook is compiled in (a separate instantiation, so the
 // product kernel carries no extra registers for it)
-template <int D, bool DUMP>
+#ifndef PARO_DIAG_NOUNPACK
+#define PARO_DIAG_NOUNPACK 0 // diagnostic builds only: skip the INT4 unpack (wrong results)
+#endif
+// PACKED: INT4 V arrives nibble-packed and is unpacked in shared memory (a separate
+// instantiation: the INT8 kernels carry none of that code)
+template <int D, bool DUMP, bool PACKED>
 __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     k3_attention(const __grid_constant__ K3Params P, const __grid_constant__ CUtensorMap tm_q,
-                 const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+                 const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                 const __grid_constant__ CUtensorMap tm_vp) {
     using C = K3Cfg<D>;
     using BR = Bars<C::NS>;
     constexpr int G = C::G;
@@ -801,6 +873,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_init(bar(BR::ITEMFULL + i), 1);
             ptx::mbar_init(bar(BR::ITEMEMPTY + i), C::NCONS);
         }
+        for (int s = 0; s < NS; ++s)
+            ptx::mbar_init(bar(BR::VFULL + s), C::NVFULL);
         ptx::mbar_init(bar(BR::LFULL), 4); // !SPLIT: softmax -> epilogue row sums
         ptx::mbar_init(bar(BR::LEMPTY), 4);
         ptx::fence_barrier_init();
@@ -845,46 +919,84 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
+        // Lane 0 issues the TMA; with INT4 V (P.v_packed) the whole warp also unpacks
+        // each stage's nibble-packed V tiles into the i8 swizzled layout the P.V MMA
+        // reads (Blackwell has no INT4 MMA), one step behind the loads, and releases
+        // them with VFULL -- QK waits only for K.
         if (C::SPLIT)
             ptx::setmaxnreg_dec<C::REG_LOW>();
+        constexpr bool packed = PACKED;
         if (lane == 0) {
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_k);
-            ptx::prefetch_tmap(&tm_v);
-            uint32_t T = 0, I = 0;
-            for (uint32_t r = 0;; ++r) {
-                int it;
-                if (PARO_DYNAMIC) {
+            ptx::prefetch_tmap(packed ? &tm_vp : &tm_v);
+        }
+        uint32_t T = 0, I = 0;
+        uint32_t pend = 0; // bit 0: a step's packed V waits for its unpack; bits 1-2: sides A / B
+        auto unpack_pending = [&]() {
+            if (!(pend & 1u))
+                return;
+            const uint32_t U = T - 1, s = U % NS;
+            ptx::mbar_wait(bar(BR::KVFULL + s), (U / NS) & 1);
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                if (!((pend >> (1 + side)) & 1u) || PARO_DIAG_NOUNPACK)
+                    continue;
+                uint8_t* vt = smem + C::OFF_STAGE + s * C::STAGE_BYTES + (2 + side) * C::KV_BYTES;
+                const uint8_t* pk8 = C::SPLIT ? smem + C::OFF_VPK + (s * 2 + side) * C::VPK_BYTES : vt + C::KV_BYTES / 2;
+                unpack_v_tile<D>(pk8, vt, lane);
+            }
+            ptx::fence_proxy_async_smem(); // the unpacked codes -> the tensor core's view
+            __syncwarp();
+            if (lane == 0)
+                ptx::mbar_arrive(bar(BR::VFULL + s));
+            pend = 0;
+        };
+        // only d = 64 with INT4 V needs the whole warp in the loop (it unpacks); else lane 0 alone
+        const bool all_lanes = packed && !C::SPLIT;
+        const uint32_t wmask = all_lanes ? 0xffffffffu : 1u;
+        for (uint32_t r = 0; all_lanes || lane == 0; ++r) {
+            int it = 0;
+            if (PARO_DYNAMIC) {
+                if (lane == 0) {
                     const uint32_t idx = atomicAdd(P.work_counter, 1u);
                     it = idx < P.n_items ? (int)P.order[idx] : -1;
-                    const uint32_t slot = r & 1;
-                    mbar_wait_lazy(bar(BR::ITEMEMPTY + slot), ((r >> 1) & 1) ^ 1);
+                }
+                it = __shfl_sync(wmask, it, 0);
+                const uint32_t slot = r & 1;
+                mbar_wait_lazy(bar(BR::ITEMEMPTY + slot), ((r >> 1) & 1) ^ 1);
+                if (lane == 0) {
                     ring[slot] = it;
                     ptx::mbar_arrive(bar(BR::ITEMFULL + slot));
-                    if (it < 0)
-                        break;
-                } else {
-                    if (r >= rounds)
-                        break;
-                    it = item_at(r);
-                    if (it < 0)
-                        continue;
                 }
-                const Item x = load_item(L, (uint32_t)it);
-                const uint16_t* la = L.items + ((size_t)x.h * L.kb + x.qa) * L.kb;
-                const uint16_t* lb = L.items + ((size_t)x.h * L.kb + (x.qb != 0xffffu ? x.qb : 0)) * L.kb;
-                const int32_t row0 = (int32_t)(x.h * L.kb2 * 64);
-                ptx::mbar_wait(qempty(I), ((I >> 1) & 1) ^ 1);
+                __syncwarp(wmask);
+                if (it < 0)
+                    break;
+            } else {
+                if (r >= rounds)
+                    break;
+                it = item_at(r);
+                if (it < 0)
+                    continue;
+            }
+            const Item x = load_item(L, (uint32_t)it);
+            const uint16_t* la = L.items + ((size_t)x.h * L.kb + x.qa) * L.kb;
+            const uint16_t* lb = L.items + ((size_t)x.h * L.kb + (x.qb != 0xffffu ? x.qb : 0)) * L.kb;
+            const int32_t row0 = (int32_t)(x.h * L.kb2 * 64);
+            ptx::mbar_wait(qempty(I), ((I >> 1) & 1) ^ 1);
+            if (lane == 0) {
                 ptx::mbar_arrive_expect_tx(qfull(I), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
                 ptx::tma_load_2d(qbuf(I), &tm_q, 0, row0 + (int32_t)x.qa * 64, qfull(I));
                 if (x.qb != 0xffffu)
                     ptx::tma_load_2d(qbuf(I) + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
-                for (uint32_t t = 0; t < x.n; ++t, ++T) {
-                    const uint32_t s = T % NS;
-                    mbar_wait_lazy(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
-                    const bool ha = t < x.na, hb = t < x.nb;
-                    ptx::mbar_arrive_expect_tx(bar(BR::KVFULL + s),
-                                               (ha + hb) * (2 * C::KV_BYTES + C::META_BYTES));
+            }
+            for (uint32_t t = 0; t < x.n; ++t) {
+                const uint32_t s = T % NS;
+                mbar_wait_lazy(bar(BR::KVEMPTY + s), ((T / NS) & 1) ^ 1);
+                const bool ha = t < x.na, hb = t < x.nb;
+                if (lane == 0) {
+                    const uint32_t vbytes = packed ? C::VPK_BYTES : C::KV_BYTES;
+                    ptx::mbar_arrive_expect_tx(bar(BR::KVFULL + s), (ha + hb) * (C::KV_BYTES + vbytes + C::META_BYTES));
                     const uint32_t st = stage(s);
 #pragma unroll
                     for (int side = 0; side < 2; ++side) {
@@ -892,17 +1004,29 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                             const uint32_t bj = side ? lb[t] : la[t];
                             ptx::tma_load_2d(st + side * C::KV_BYTES, &tm_k, 0, row0 + (int32_t)bj * 64,
                                              bar(BR::KVFULL + s));
-                            ptx::tma_load_2d(st + (2 + side) * C::KV_BYTES, &tm_v, 0, row0 + (int32_t)bj * 64,
-                                             bar(BR::KVFULL + s));
+                            if (packed)
+                                ptx::tma_load_2d(C::SPLIT ? sbase + C::OFF_VPK + (s * 2 + side) * C::VPK_BYTES
+                                                          : st + (2 + side) * C::KV_BYTES + C::KV_BYTES / 2,
+                                                 &tm_vp, 0, row0 + (int32_t)bj * 64, bar(BR::KVFULL + s));
+                            else
+                                ptx::tma_load_2d(st + (2 + side) * C::KV_BYTES, &tm_v, 0, row0 + (int32_t)bj * 64,
+                                                 bar(BR::KVFULL + s));
                             ptx::bulk_load(st + 4 * C::KV_BYTES + side * C::META_BYTES,
                                            L.meta + ((size_t)x.h * L.kb2 + bj) * meta_stride(D), C::META_BYTES,
                                            bar(BR::KVFULL + s));
                         }
                     }
                 }
-                ++I;
+                if (packed && !C::SPLIT) { // unpack the previous step while this one's loads are in flight
+                    if (all_lanes)
+            unpack_pending();
+                    pend = 1u | (ha ? 2u : 0u) | (hb ? 4u : 0u);
+                }
+                ++T;
             }
+            ++I;
         }
+        unpack_pending();
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (C::SPLIT)
@@ -915,6 +1039,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 PROF_T(tm0);
                 mbar_wait_mma(bar(BR::PFULL + b), ph);
                 mbar_wait_mma(bar(BR::OEMPTY + b), ph ^ 1);
+                if (PACKED) // the unpacked V is usually ready: wait without a sleep back-off
+                    ptx::mbar_wait(bar(BR::VFULL + s), (U / NS) & 1);
                 ptx::tc_fence_after();
                 PROF_T(tm1);
                 PROF_ADD(1, tm1 - tm0);
@@ -1412,7 +1538,45 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         }
 #endif
     } else {
-        ptx::setmaxnreg_dec<C::REG_LOW>(); // warps 2-3: idle members of warpgroup 0
+        // warps 2-3 (d = 128): with INT4 V, warp 2 unpacks side A's and warp 3 side B's
+        // nibble-packed V tile of every step from the staging buffer (their SMSPs,
+        // not the producer's, carry the work); both arrive on VFULL every step
+        ptx::setmaxnreg_dec<C::REG_LOW>();
+        const uint32_t side = (uint32_t)warp - 2;
+        uint32_t T = 0;
+        for (uint32_t rr = 0;; ++rr) {
+            if (!PARO_DYNAMIC && rr >= rounds)
+                break;
+            const int it = next_item(rr, true);
+            __syncwarp();
+            if (lane == 0)
+                release_item(rr);
+            if (it < 0) {
+                if (PARO_DYNAMIC)
+                    break;
+                continue;
+            }
+            const Item x = load_item(L, (uint32_t)it);
+            if (!PACKED) {
+                T += x.n;
+                continue;
+            }
+            const uint32_t nmine = side ? x.nb : x.na;
+            for (uint32_t t = 0; t < x.n; ++t, ++T) {
+                const uint32_t s = T % NS;
+                // every step waits for its stage, even with no tile on this side: a warp
+                // must not arrive on VFULL(s) for step T + NS while step T's phase is open
+                ptx::mbar_wait(bar(BR::KVFULL + s), (T / NS) & 1);
+                if (t < nmine && !PARO_DIAG_NOUNPACK) {
+                    unpack_v_tile<D>(smem + C::OFF_VPK + (s * 2 + side) * C::VPK_BYTES,
+                                     smem + C::OFF_STAGE + s * C::STAGE_BYTES + (2 + side) * C::KV_BYTES, lane);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                }
+                if (lane == 0)
+                    ptx::mbar_arrive(bar(BR::VFULL + s));
+            }
+        }
     }
 
     ptx::tc_fence_before();
@@ -1497,19 +1661,20 @@ static void init_watchdog() {
 
 template <int D>
 static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                               const CUtensorMap& tv, int grid, cudaStream_t st) {
+                               const CUtensorMap& tv, const CUtensorMap& tvp, int grid, cudaStream_t st) {
     init_watchdog();
     const uint32_t smem = K3Cfg<D>::SMEM_BYTES;
-    auto kern = p.dump.slot ? k3_attention<D, true> : k3_attention<D, false>;
+    auto kern = p.L.v_packed ? (p.dump.slot ? k3_attention<D, true, true> : k3_attention<D, false, true>)
+                             : (p.dump.slot ? k3_attention<D, true, false> : k3_attention<D, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv);
+    kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv, tvp);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
                       uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump) {
     if (head_count == 0)
         return cudaSuccess;
@@ -1566,7 +1731,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
 #endif
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);
     const int grid = (int)(p.n_items < slots ? p.n_items : slots);
-    return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, grid, st) : launch_k3_t<128>(p, tq, tk, tv, grid, st);
+    return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, grid, st) : launch_k3_t<128>(p, tq, tk, tv, tvp, grid, st);
 }
 
 cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,

@@ -49,7 +49,7 @@ cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, con
                                     float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
                       uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump = nullptr);
 cudaError_t launch_k1_quant_proof(uint32_t lo, uint32_t count, uint32_t nx, uint32_t seed, unsigned long long* bad,
                                   uint32_t* first, int num_sms, cudaStream_t st);
@@ -297,7 +297,7 @@ struct paro_layer {
     bool masks_set = false;
     int last_v_bits = 0;
     int last_launches = 0;
-    CUtensorMap tm_q, tm_k, tm_v;
+    CUtensorMap tm_q, tm_k, tm_v, tm_vp; // tm_vp: nibble-packed INT4 V (D/2 bytes per row)
     // e2e staging
     float* rope = nullptr; // [2][N - dp][D]: cos, sin (paro_layer_set_rope)
     float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
@@ -311,6 +311,7 @@ struct paro_layer {
         int entry = -1;
         cudaEvent_t ready = nullptr;
     };
+    bool v_pack = false; // INT4 V nibble-packed in HBM (paro_layer_set_v_packing)
     uint32_t sched_T = 0, sched_entries = 0, sched_resident = 0;
     uint8_t* sched_masks = nullptr; // [entries][H][kb][kb] (block bytes, uploaded once)
     std::vector<Lists> sched_lists; // entries (resident) or 2 (double-buffered prefetch)
@@ -377,6 +378,19 @@ T* dalloc(size_t count) {
     void* p = nullptr;
     cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
     return static_cast<T*>(p);
+}
+
+// nibble-packed INT4 V: rows of D/2 bytes, no swizzle (K3 unpacks into the swizzled tile)
+void encode_packed_map(paro_ctx* ctx, CUtensorMap* m, int8_t* base, uint32_t D, uint64_t rows, uint32_t box_rows) {
+    cuuint64_t dims[2] = {D / 2, rows};
+    cuuint64_t strides[1] = {D / 2};
+    cuuint32_t box[2] = {D / 2, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = ctx->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(PARO_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
 void encode_codes_map(paro_ctx* ctx, CUtensorMap* m, int8_t* base, uint32_t D, uint64_t rows, uint32_t box_rows) {
@@ -532,7 +546,7 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
     if (l->L.dp) { // dense text-token prefix: dense rows done, the others' state for K3
         cuda_check(paro::launch_k4(l->L, eff, out, zeroed, head_begin, head_count, st), "k4 launch");
     }
-    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
+    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, l->tm_vp, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
                                head_begin, head_count, chunked, dump),
                "k3_attention launch");
 }
@@ -1389,6 +1403,7 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
                 L.l2_group = (uint32_t)std::min<size_t>(g, heads);
             }
             L.work_counter = dalloc<uint32_t>(1);
+            l->v_pack = getenv("PARO_V_PACKED") && atoi(getenv("PARO_V_PACKED")) != 0;
             l->fwd = dalloc<uint32_t>((size_t)heads * N);
             l->inv = dalloc<uint32_t>((size_t)heads * N);
             cuda_check(cudaMemset(L.q, 0, rows * head_dim), "cudaMemset");
@@ -1401,6 +1416,7 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
             encode_codes_map(ctx, &l->tm_q, L.q, head_dim, rows, 64);
             encode_codes_map(ctx, &l->tm_k, L.k, head_dim, rows, 64);
             encode_codes_map(ctx, &l->tm_v, L.v, head_dim, rows, 64);
+            encode_packed_map(ctx, &l->tm_vp, L.v, head_dim, rows, 64);
             cuda_check(cudaDeviceSynchronize(), "layer init");
         } catch (...) {
             free_layer(l);
@@ -1621,6 +1637,7 @@ int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const f
         if (!q || !k || !v)
             fail(PARO_E_CONFIG, "null Q/K/V");
         set_device(layer->ctx);
+        layer->L.v_packed = v_bits == 4 && layer->v_pack;
         cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, 0, layer->L.H, (cudaStream_t)stream), "k1 launch");
         cuda_check(paro::launch_k4a(layer->L, v, 0, layer->L.H, (cudaStream_t)stream), "k4a launch");
         layer->last_v_bits = v_bits;
@@ -1645,11 +1662,19 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
             fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
         set_device(layer->ctx);
         cudaStream_t st = (cudaStream_t)stream;
+        layer->L.v_packed = pv_bits == 4 && layer->v_pack;
         cuda_check(paro::launch_k1(layer->L, q, k, v, pv_bits, 0, layer->L.H, st), "k1 launch");
         cuda_check(paro::launch_k4a(layer->L, v, 0, layer->L.H, st), "k4a launch");
         layer->last_v_bits = pv_bits;
         run_attention(layer, st, scale, pv_bits, out, zeroed);
         layer->last_launches = 2;
+    });
+}
+
+int paro_layer_set_v_packing(paro_layer* layer, int packed) {
+    return guarded([&] {
+        check_layer(layer);
+        layer->v_pack = packed != 0;
     });
 }
 
@@ -1727,6 +1752,7 @@ int paro_layer_forward_host(paro_layer* layer, paro_stream_t stream, const float
         cuda_check(cudaStreamWaitEvent(layer->s_in, ev[0], 0), "stream wait");
         cuda_check(cudaStreamWaitEvent(layer->s_out, ev[0], 0), "stream wait");
         layer->last_v_bits = pv_bits;
+        layer->L.v_packed = pv_bits == 4 && layer->v_pack;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t h0 = L.chunk_start[c], hn = L.chunk_start[c + 1] - h0;
             const size_t off = (size_t)h0 * head_elems, bytes = (size_t)hn * head_elems * 4;
@@ -1782,6 +1808,8 @@ int paro_layer_get_buffers(const paro_layer* layer, paro_layer_buffers* out) {
         out->tile_meta = L.meta;
         out->inverse = layer->inv;
         out->forward = layer->fwd;
+        out->v_bits = (uint32_t)layer->last_v_bits;
+        out->v_packed = L.v_packed;
     });
 }
 
@@ -1803,8 +1831,10 @@ int paro_layer_export_parq(paro_layer* layer, paro_stream_t stream, uint32_t hea
         const cudaStream_t st = (cudaStream_t)stream;
         const size_t rows = L.N, d = L.D;
         std::vector<int8_t> c8(rows * d);
-        const int8_t* src = (which == 0 ? L.q : which == 1 ? L.k : L.v) + (size_t)head * L.kb2 * 64 * d;
-        cuda_check(cudaMemcpyAsync(c8.data(), src, rows * d, cudaMemcpyDeviceToHost, st), "export codes");
+        const bool nib = which == 2 && L.v_packed;
+        const int8_t* src = (which == 0 ? L.q : which == 1 ? L.k : L.v) + (size_t)head * L.kb2 * 64 * (nib ? d / 2 : d);
+        cuda_check(cudaMemcpyAsync(c8.data(), src, nib ? rows * d / 2 : rows * d, cudaMemcpyDeviceToHost, st),
+                   "export codes");
         std::vector<float> meta((size_t)L.kb * paro::meta_stride(L.D)), qs((size_t)L.kb * L.G);
         cuda_check(cudaMemcpyAsync(meta.data(), L.meta + (size_t)head * L.kb2 * paro::meta_stride(L.D),
                                    meta.size() * 4, cudaMemcpyDeviceToHost, st),
@@ -1813,6 +1843,12 @@ int paro_layer_export_parq(paro_layer* layer, paro_stream_t stream, uint32_t hea
                                    cudaMemcpyDeviceToHost, st),
                    "export scales");
         cuda_check(cudaStreamSynchronize(st), "export");
+        if (nib) // two's-complement nibbles, low first (the K1 layout) -> one code per element
+            for (size_t i = rows * d; i-- > 0;) {
+                const uint8_t byte = (uint8_t)c8[i / 2];
+                const int v = (i & 1) ? (byte >> 4) : (byte & 15);
+                c8[i] = (int8_t)(v > 7 ? v - 16 : v);
+            }
         std::vector<int32_t> codes(c8.begin(), c8.end());
         // group order: row blocks x column blocks, row-major (quant.cpp:45-56)
         std::vector<float> scales;

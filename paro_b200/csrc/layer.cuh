@@ -51,7 +51,8 @@ __host__ __device__ inline uint32_t perm_src(const PermDesc& pd, uint32_t i) {
 struct LayerDev {
     uint32_t H, N, D, G, kb, kb2, np;
     PermDesc* perm;
-    int8_t *q, *k, *v;
+    int8_t *q, *k, *v;      // v: int8 rows of D, or (v_packed) D/2 bytes of INT4 pairs, low nibble first
+    uint32_t v_packed;      // the last reorder_quantize wrote 4-bit V codes packed
     float* qsc;
     float* meta;
     uint16_t* items;

@@ -246,7 +246,11 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(Laye
         quant_sym4(e, sv, rv, vq, v0, v1, v2, v3);
         *reinterpret_cast<uint32_t*>(L.q + off) = pack4(a0, a1, a2, a3);
         *reinterpret_cast<uint32_t*>(L.k + off) = pack4(k0, k1, k2, k3);
-        *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
+        if (L.v_packed) // INT4, two codes per byte, low nibble first (PARQ payload, quant.cpp:237-243)
+            *reinterpret_cast<uint16_t*>(L.v + off / 2) =
+                (uint16_t)((v0 & 15) | ((v1 & 15) << 4) | ((v2 & 15) << 8) | ((v3 & 15) << 12));
+        else
+            *reinterpret_cast<uint32_t*>(L.v + off) = pack4(v0, v1, v2, v3);
         cs0 += v0;
         cs1 += v1;
         cs2 += v2;

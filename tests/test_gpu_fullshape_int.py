@@ -61,13 +61,16 @@ def chunks(H, n):
     return [list(range(h, min(H, h + n))) for h in range(0, H, n)]
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
-def test_k1_every_head_bit_exact(paro, ctx, oracle, cfg):
+@pytest.mark.parametrize("cfg,packed", [("c2", False), ("c3", False), ("c4", False), ("c5", False), ("c3", True),
+                                        ("c5", True)])
+def test_k1_every_head_bit_exact(paro, ctx, oracle, cfg, packed):
+    """packed: INT4 V nibble-packed in HBM (paro_layer_set_v_packing), compared after unpacking"""
     grid, H, d, _, vb = FULL[cfg]
     G = d // 64
     checked = 0
     for heads in chunks(H, 8 if d == 64 else 4):
         g, N, d, vb, ords, q, k, v, layer, _ = layer_for(paro, ctx, cfg, heads)
+        layer.set_v_packing(packed)
         kb = (N + 63) // 64
         bufs = [paro.DeviceBuffer.from_array(x) for x in (q, k, v)]
         layer.reorder_quantize(bufs[0].ptr, bufs[1].ptr, bufs[2].ptr, vb)
