@@ -1673,6 +1673,9 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
     return cudaGetLastError();
 }
 
+cudaError_t launch_k3_64(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                         int num_sms, cudaStream_t st);
+
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
                       uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump) {
@@ -1729,6 +1732,10 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
         cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }
 #endif
+    // d = 64 multi-slot kernel (attention64_kernel.cu), opt-in while it is measured (PARO_K3_SLOTS=1)
+    static const bool slots64 = getenv("PARO_K3_SLOTS") && atoi(getenv("PARO_K3_SLOTS")) != 0;
+    if (L.D == 64 && slots64 && !L.v_packed)
+        return launch_k3_64(p, tq, tk, tv, num_sms, st);
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);
     const int grid = (int)(p.n_items < slots ? p.n_items : slots);
     return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, grid, st) : launch_k3_t<128>(p, tq, tk, tv, tvp, grid, st);
