@@ -27,11 +27,14 @@
 //   (x = hi + lo, 16 significant bits; hi.hi + hi.lo + lo.hi). V is split once
 //   per layer by K4a into transposed bf16 hi / lo tiles in HBM (permuted order),
 //   which each CTA stages with cp.async and reads with ldmatrix.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "layer.cuh"
+#include "ptx.cuh"
 
 namespace paro {
 
@@ -427,6 +430,368 @@ __global__ void __launch_bounds__(128) k4_dense(LayerDev L, double scale64,
     }
 }
 
+// ---------------------------------------------------------------------------
+// K4 on the 5th-generation tensor cores (default; PARO_K4_LEGACY=1 keeps the
+// mma.sync kernel above). Same work units, semantics and outputs; per key tile:
+//   S = Q.K^T       tcgen05.mma kind::i8, M = 64 (TMEM lanes 0-15 of each
+//                   quadrant), N = 64 per column group, exact int32
+//   row max / p     one thread per row (lanes 0-15 of warp w own rows 16w..):
+//                   exact fp64 max as in k4_dense, p = exp2 of integer
+//                   differences, split into bf16 hi + lo and written as the
+//                   K-major SW128 A operand
+//   O_tile = P.V    tcgen05.mma kind::f16 (bf16 x bf16 -> fp32), 3-term split
+//                   Phi.Vhi + Phi.Vlo + Plo.Vhi accumulated in TMEM
+//   acc = gamma acc + O_tile in registers
+// K, V^T hi / lo tiles arrive by TMA, double-buffered one tile ahead.
+// ---------------------------------------------------------------------------
+template <int D>
+struct K4T {
+    static constexpr int G = D / 64;
+    static constexpr uint32_t QT = 64 * D;             // Q / K code tile
+    static constexpr uint32_t VT = D * 128;            // V^T bf16 tile (D rows of 64 keys)
+    static constexpr uint32_t PT = 64 * 128;           // P bf16 tile (64 rows of 64 keys)
+    static constexpr uint32_t STAGE = QT + 2 * VT;     // K, Vhi, Vlo (all 1024-aligned)
+    static constexpr uint32_t OFF_Q = 0, OFF_ST = QT, OFF_P = OFF_ST + 2 * STAGE, OFF_BAR = OFF_P + 2 * PT;
+    static constexpr uint32_t SMEM = OFF_BAR + 64;
+    static constexpr uint32_t TMEM_COLS = G * 64 + D <= 128 ? 128 : 256; // S groups, then O
+    static constexpr uint32_t LAYOUT = D == 64 ? ptx::kSwizzle64B : ptx::kSwizzle128B;
+    static constexpr uint32_t IDESC_QK = ptx::idesc_i8(true, true, false, false, 64, 64);
+    static constexpr uint32_t IDESC_PV = ptx::idesc_bf16(64, D);
+};
+
+// 16 TMEM lanes x 256 bits, 8 repetitions: the mma.sync accumulator fragment
+// layout -- thread t gets rows t/4 and t/4 + 8 of its quadrant's 16 lanes,
+// columns 8k + 2(t%4) + {0,1} for k = 0..7 (registers 4k..4k+3 = (r, c), (r, c+1),
+// (r+8, c), (r+8, c+1)); M = 64 keeps a q-block's rows in lanes 0-15 of each quadrant
+__device__ __forceinline__ void k4_ld_frag(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k4_dense_tc(const __grid_constant__ LayerDev L, double scale64,
+                                                   const __grid_constant__ CUtensorMap tm_q,
+                                                   const __grid_constant__ CUtensorMap tm_k,
+                                                   const __grid_constant__ CUtensorMap tm_vh,
+                                                   const __grid_constant__ CUtensorMap tm_vl, uint32_t head_begin) {
+    using C = K4T<D>;
+    constexpr int G = C::G;
+    constexpr int NT = D / 8; // 8-column blocks of the output
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sb = ptx::smem_u32(smem);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const uint32_t h = head_begin + blockIdx.y, u = blockIdx.x;
+    const uint32_t ndense_units = L.nd * L.k4_cb;
+    uint32_t qb, t0, t1, chunk = 0;
+    if (u < ndense_units) { // q-block with dense rows, key chunk `chunk`
+        qb = u / L.k4_cb;
+        chunk = u % L.k4_cb;
+        t0 = chunk * L.k4_ch;
+        t1 = min(L.kb, t0 + L.k4_ch);
+    } else { // q-block without dense rows: its dense tiles only
+        qb = L.nd + (u - ndense_units);
+        t0 = 0;
+        t1 = L.nd;
+    }
+    const int32_t row0 = (int32_t)(h * L.kb2 * 64);
+    const uint32_t rl[2] = {warp * 16 + gq, warp * 16 + gq + 8}; // rows within the q-block
+    const uint32_t rows[2] = {qb * 64 + rl[0], qb * 64 + rl[1]};
+    const uint32_t b_full = sb + C::OFF_BAR, b_q = b_full + 16, b_s = b_full + 24, b_o = b_full + 32;
+    if (tid == 0) {
+        ptx::mbar_init(b_full, 1);
+        ptx::mbar_init(b_full + 8, 1);
+        ptx::mbar_init(b_q, 1);
+        ptx::mbar_init(b_s, 1);
+        ptx::mbar_init(b_o, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0)
+        ptx::tmem_alloc<C::TMEM_COLS>(sb + C::OFF_BAR + 48);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::OFF_BAR + 48);
+    auto load_tile = [&](uint32_t bj, uint32_t st) {
+        const uint32_t dst = sb + C::OFF_ST + st * C::STAGE, bar = b_full + 8 * st;
+        ptx::mbar_arrive_expect_tx(bar, C::QT + 2 * C::VT);
+        ptx::tma_load_2d(dst, &tm_k, 0, row0 + (int32_t)bj * 64, bar);
+        const int32_t vrow = (int32_t)((h * L.kb2 + bj) * D);
+        ptx::tma_load_2d(dst + C::QT, &tm_vh, 0, vrow, bar);
+        ptx::tma_load_2d(dst + C::QT + C::VT, &tm_vl, 0, vrow, bar);
+    };
+    if (tid == 0) {
+        ptx::mbar_arrive_expect_tx(b_q, C::QT);
+        ptx::tma_load_2d(sb + C::OFF_Q, &tm_q, 0, row0 + (int32_t)qb * 64, b_q);
+        if (t0 < t1)
+            load_tile(t0, 0);
+    }
+    float sq[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        sq[g] = L.qsc[((size_t)h * L.kb2 + qb) * G + g];
+    double m64[2] = {-INFINITY, -INFINITY};
+    float lp[2] = {0.f, 0.f}; // this lane's share of l per row
+    float acc[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+    const uint32_t tl = tmem + ((warp * 32) << 16); // this warp's TMEM lane quadrant (rows in lanes 0-15)
+    ptx::mbar_wait(b_q, 0);
+    for (uint32_t bj = t0; bj < t1; ++bj) {
+        const uint32_t it = bj - t0, st = it & 1;
+        if (tid == 0 && bj + 1 < t1)
+            load_tile(bj + 1, st ^ 1); // that stage's previous tile finished (the loop ends in __syncthreads)
+        ptx::mbar_wait(b_full + 8 * st, (it >> 1) & 1);
+        const uint32_t kst = sb + C::OFF_ST + st * C::STAGE;
+        if (tid == 0) { // S = Q.K^T, exact int32 per 64-column group
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const uint32_t off = g * 64 + kk * 32;
+                    ptx::mma_i8(tmem + g * 64, ptx::smem_desc(sb + C::OFF_Q + off, 16, 8 * D, C::LAYOUT),
+                                ptx::smem_desc(kst + off, 16, 8 * D, C::LAYOUT), C::IDESC_QK, kk);
+                }
+            ptx::mma_commit(b_s);
+        }
+        bool act[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+            act[x] = rows[x] < L.N && (rows[x] < L.dp || bj < L.nd);
+        const uint32_t kn = min(64u, L.N - bj * 64);
+        double a[G];
+        float af[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            a[g] = __dmul_rn((double)sq[g], (double)L.meta[((size_t)h * L.kb2 + bj) * meta_stride(D) + g]);
+            af[g] = (float)a[g];
+        }
+        ptx::mbar_wait(b_s, it & 1);
+        ptx::tc_fence_after();
+        int32_t S[G][8][4];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            uint32_t f[32];
+            k4_ld_frag(tl + g * 64, f);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    S[g][n][e] = (int32_t)f[4 * n + e];
+        }
+        // ---- exact row max of the tile (k4_dense): fp32 screen, fp64 on the candidates
+        double best[2] = {-INFINITY, -INFINITY};
+        int32_t bs[2][G];
+        if constexpr (G == 1) {
+            int32_t im[2] = {INT32_MIN, INT32_MIN};
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (n * 8 + 2 * tq + (e & 1) < kn)
+                        im[e >> 1] = max(im[e >> 1], S[0][n][e]);
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                im[x] = max(im[x], __shfl_xor_sync(0xffffffffu, im[x], 1));
+                im[x] = max(im[x], __shfl_xor_sync(0xffffffffu, im[x], 2));
+                bs[x][0] = im[x];
+                const int32_t sv[1] = {im[x]};
+                best[x] = k4_exact<G>(scale64, a, sv);
+            }
+        } else {
+            float mx[2] = {-INFINITY, -INFINITY}, mag[2] = {0.f, 0.f};
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                    float xv = 0.f, mg = 0.f;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float tv = af[g] * (float)S[g][n][e];
+                        xv += tv;
+                        mg += fabsf(tv);
+                    }
+                    if (key < kn) {
+                        mx[e >> 1] = fmaxf(mx[e >> 1], xv);
+                        mag[e >> 1] = fmaxf(mag[e >> 1], mg);
+                    }
+                }
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int o = 1; o <= 2; o <<= 1) {
+                    mx[x] = fmaxf(mx[x], __shfl_xor_sync(0xffffffffu, mx[x], o));
+                    mag[x] = fmaxf(mag[x], __shfl_xor_sync(0xffffffffu, mag[x], o));
+                }
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    bs[x][g] = 0;
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int x = e >> 1;
+                    const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                    float xv = 0.f;
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        xv += af[g] * (float)S[g][n][e];
+                    if (key < kn && xv >= mx[x] - 1e-6f * mag[x]) {
+                        int32_t sv[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            sv[g] = S[g][n][e];
+                        const double lg = k4_exact<G>(scale64, a, sv);
+                        if (lg > best[x]) {
+                            best[x] = lg;
+#pragma unroll
+                            for (int g = 0; g < G; ++g)
+                                bs[x][g] = sv[g];
+                        }
+                    }
+                }
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int o = 1; o <= 2; o <<= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best[x], o);
+                    int32_t os[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        os[g] = __shfl_xor_sync(0xffffffffu, bs[x][g], o);
+                    if (ob > best[x]) {
+                        best[x] = ob;
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            bs[x][g] = os[g];
+                    }
+                }
+        }
+        // ---- running max, p -> bf16 hi / lo P rows (K-major, 128B swizzle: 16-B chunk n of row r at n ^ (r & 7))
+        float base[2], gam[2] = {1.f, 1.f}, cg[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            cg[g] = (float)(scale64 * a[g] * kLog2eD);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            if (!act[x]) {
+                base[x] = -INFINITY;
+                continue;
+            }
+            const double mn = fmax(m64[x], best[x]);
+            if (mn != m64[x]) { // (attention.cpp:170-178); m = -inf -> gamma 0 on zero state
+                gam[x] = ex2f((float)((m64[x] - mn) * kLog2eD));
+                lp[x] *= gam[x];
+                m64[x] = mn;
+            }
+            base[x] = (float)((best[x] - mn) * kLog2eD);
+        }
+        uint8_t* prow[2] = {smem + C::OFF_P + (rl[0] >> 3) * 1024 + (rl[0] & 7) * 128,
+                            smem + C::OFF_P + (rl[1] >> 3) * 1024 + (rl[1] & 7) * 128};
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            float P[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int x = e >> 1;
+                const uint32_t key = n * 8 + 2 * tq + (e & 1);
+                float arg = base[x];
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    arg = fmaf(cg[g], (float)(S[g][n][e] - bs[x][g]), arg);
+                P[e] = key < kn ? ex2f(arg) : 0.f; // base -inf (inactive row) -> 0
+                lp[x] += P[e];
+            }
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                uint32_t wh, wl;
+                bf16_split2(P[2 * x], P[2 * x + 1], wh, wl);
+                const uint32_t off = ((n ^ (rl[x] & 7)) << 4) + tq * 4;
+                *reinterpret_cast<uint32_t*>(prow[x] + off) = wh;
+                *reinterpret_cast<uint32_t*>(prow[x] + C::PT + off) = wl;
+            }
+        }
+        ptx::fence_proxy_async_smem(); // P rows -> the tensor core's view
+        ptx::tc_fence_before();        // S reads done before the next QK overwrites S
+        __syncthreads();
+        if (tid == 0) { // O_tile = Phi.Vhi + Phi.Vlo + Plo.Vhi (fp32 in TMEM)
+            ptx::tc_fence_after();
+            const uint32_t pa[3] = {sb + C::OFF_P, sb + C::OFF_P, sb + C::OFF_P + C::PT};
+            const uint32_t vb[3] = {kst + C::QT, kst + C::QT + C::VT, kst + C::QT};
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    ptx::mma_f16(tmem + G * 64, ptx::smem_desc(pa[t] + ks * 32, 16, 1024, ptx::kSwizzle128B),
+                                 ptx::smem_desc(vb[t] + ks * 32, 16, 1024, ptx::kSwizzle128B), C::IDESC_PV,
+                                 (t | ks) != 0);
+            ptx::mma_commit(b_o);
+        }
+        ptx::mbar_wait(b_o, it & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c64 = 0; c64 < D / 64; ++c64) {
+            uint32_t f[32];
+            k4_ld_frag(tl + G * 64 + c64 * 64, f);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    acc[c64 * 8 + n][e] = fmaf(acc[c64 * 8 + n][e], gam[e >> 1], __uint_as_float(f[4 * n + e]));
+        }
+        ptx::tc_fence_before();
+        __syncthreads(); // P, S, O and this tile's stage are free again
+    }
+    // ---- per-row results (as k4_dense): l = quad sum; lane holds columns n*8 + 2tq, +1
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+        lp[x] += __shfl_xor_sync(0xffffffffu, lp[x], 1);
+        lp[x] += __shfl_xor_sync(0xffffffffu, lp[x], 2);
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+        const uint32_t i = rows[x];
+        if (i >= L.N)
+            continue;
+        float* dst;
+        if (u < ndense_units) { // partial of (row, chunk)
+            const size_t pp = ((size_t)h * L.nd * 64 + i) * L.k4_cb + chunk;
+            if (tq == 0) {
+                L.part_m[pp] = m64[x];
+                L.part_l[pp] = lp[x];
+            }
+            dst = L.part_acc + pp * D;
+        } else { // K3's initial state (no dense rows in this q-block)
+            const size_t sr = (size_t)row0 + i;
+            if (tq == 0) {
+                L.init_m[sr] = m64[x];
+                L.init_l[sr] = lp[x];
+            }
+            dst = L.init_acc + sr * D;
+        }
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+            *reinterpret_cast<float2*>(dst + n * 8 + 2 * tq) = make_float2(acc[n][2 * x], acc[n][2 * x + 1]);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // final dense row (original token order, attention.cpp:242-251) or K3's initial state
 template <int D>
 __device__ __forceinline__ void k4_finish(const LayerDev& L, uint32_t h, uint32_t i, double m64, float l,
@@ -522,11 +887,30 @@ cudaError_t launch_k4a(const LayerDev& L, const float* v, uint32_t head_begin, u
 }
 
 cudaError_t launch_k4(const LayerDev& L, double scale, float* out, uint8_t* zeroed, uint32_t head_begin,
-                      uint32_t head_count, cudaStream_t st) {
+                      uint32_t head_count, cudaStream_t st, const CUtensorMap* tq, const CUtensorMap* tk,
+                      const CUtensorMap* tvh, const CUtensorMap* tvl) {
     if (L.dp == 0 || head_count == 0)
         return cudaSuccess;
     const dim3 grid(L.nd * L.k4_cb + (L.kb - L.nd), head_count);
     const dim3 cgrid(L.nd, head_count);
+    static const bool legacy = getenv("PARO_K4_LEGACY") && atoi(getenv("PARO_K4_LEGACY")) != 0;
+    if (!legacy && tvh) { // tcgen05 K4 (the combine kernel is shared)
+        cudaError_t e;
+        if (L.D == 64) {
+            if ((e = cudaFuncSetAttribute(k4_dense_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)K4T<64>::SMEM)) != cudaSuccess)
+                return e;
+            k4_dense_tc<64><<<grid, 128, K4T<64>::SMEM, st>>>(L, scale, *tq, *tk, *tvh, *tvl, head_begin);
+            k4_combine<64><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
+        } else {
+            if ((e = cudaFuncSetAttribute(k4_dense_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)K4T<128>::SMEM)) != cudaSuccess)
+                return e;
+            k4_dense_tc<128><<<grid, 128, K4T<128>::SMEM, st>>>(L, scale, *tq, *tk, *tvh, *tvl, head_begin);
+            k4_combine<128><<<cgrid, 128, 0, st>>>(L, out, zeroed, head_begin);
+        }
+        return cudaGetLastError();
+    }
     if (L.D == 64) {
         constexpr size_t smem = K4Cfg<64>::SMEM;
         cudaFuncSetAttribute(k4_dense<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

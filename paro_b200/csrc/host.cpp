@@ -44,7 +44,8 @@ cudaError_t launch_block_terms(const double* sums, const float* maxs, const uint
 void k4_chunking(uint32_t kb, uint32_t nd, uint32_t heads, uint32_t& cb, uint32_t& ch);
 cudaError_t launch_k4a(const LayerDev& L, const float* v, uint32_t head_begin, uint32_t head_count, cudaStream_t st);
 cudaError_t launch_k4(const LayerDev& L, double scale, float* out, uint8_t* zeroed,
-                      uint32_t head_begin, uint32_t head_count, cudaStream_t st);
+                      uint32_t head_begin, uint32_t head_count, cudaStream_t st, const CUtensorMap* tq,
+                      const CUtensorMap* tk, const CUtensorMap* tvh, const CUtensorMap* tvl);
 cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, const uint32_t* inv, uint32_t block,
                                     float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
@@ -298,6 +299,7 @@ struct paro_layer {
     int last_v_bits = 0;
     int last_launches = 0;
     CUtensorMap tm_q, tm_k, tm_v, tm_vp; // tm_vp: nibble-packed INT4 V (D/2 bytes per row)
+    CUtensorMap tm_vh, tm_vl;            // dense prefix: K4a's bf16 V^T hi / lo tiles (K4 on tcgen05)
     // e2e staging
     float* rope = nullptr; // [2][N - dp][D]: cos, sin (paro_layer_set_rope)
     float *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
@@ -378,6 +380,20 @@ T* dalloc(size_t count) {
     void* p = nullptr;
     cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
     return static_cast<T*>(p);
+}
+
+// K4a's V^T tiles: [H*kb2*D rows][64 bf16], 128B swizzle, one tile = D rows (the
+// K-major B operand of K4's bf16 P.V MMA)
+void encode_vt_map(paro_ctx* ctx, CUtensorMap* m, uint16_t* base, uint32_t D, uint64_t rows) {
+    cuuint64_t dims[2] = {64, rows};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, D};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = ctx->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(PARO_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
 // nibble-packed INT4 V: rows of D/2 bytes, no swizzle (K3 unpacks into the swizzled tile)
@@ -544,7 +560,9 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
     if (head_count == ~0u)
         head_count = l->L.H;
     if (l->L.dp) { // dense text-token prefix: dense rows done, the others' state for K3
-        cuda_check(paro::launch_k4(l->L, eff, out, zeroed, head_begin, head_count, st), "k4 launch");
+        cuda_check(paro::launch_k4(l->L, eff, out, zeroed, head_begin, head_count, st, &l->tm_q, &l->tm_k, &l->tm_vh,
+                                   &l->tm_vl),
+                   "k4 launch");
     }
     cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, l->tm_vp, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
                                head_begin, head_count, chunked, dump),
@@ -1378,6 +1396,8 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
                 L.part_acc = dalloc<float>(parts * head_dim);
                 L.vsplit_hi = dalloc<uint16_t>(rows * head_dim);
                 L.vsplit_lo = dalloc<uint16_t>(rows * head_dim);
+                encode_vt_map(ctx, &l->tm_vh, L.vsplit_hi, head_dim, rows / 64 * head_dim);
+                encode_vt_map(ctx, &l->tm_vl, L.vsplit_lo, head_dim, rows / 64 * head_dim);
             }
             L.perm = dalloc<PermDesc>(heads);
             L.q = dalloc<int8_t>(rows * head_dim);
