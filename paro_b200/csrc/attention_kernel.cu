@@ -483,7 +483,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
     uint64_t sum2 = pk(0.f, 0.f);
     const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
-    auto compute_p = [&](int h2, float (&pv)[32]) { // p of the row's 32 columns of half h2, + row sum
+    auto compute_p = [&](int h2, float (&pv)[32], bool mask_tail) { // p of the row's 32 columns of half h2, + row sum
         if (G == 1) {
             uint32_t x[32];
             ptx::tmem_ld32(s_addr + h2 * 32, x);
@@ -516,7 +516,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 pv[2 * k + 1] = ex2(yb);
             }
         }
-        if (tail_any) { // tail tile: the padded key columns (copies of column 0) leave the row sum
+        if (mask_tail && tail_any) { // tail tile: the padded key columns (copies of column 0) leave the row sum
 #pragma unroll
             for (int j = 0; j < 32; ++j)
                 if ((uint32_t)(h2 * 32 + j) >= ncol)
@@ -534,12 +534,30 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     // (Measured at d=64 with 12 warps and setmaxnreg giving the softmax 120 registers
     // for the row's 64 p values: 5.32 vs 4.52 ms at c2, branch k3-multislot-experiment.)
     constexpr bool kOverlap = SPLIT && PARO_RED_MBAR;
+    // d=64 (PARO_P_STASH): the same overlap without holding p in registers -- the
+    // row's 64 p values are computed before the wait and parked in TMEM over the
+    // row's S columns (S is dead once p exists; the exact path re-derives S from
+    // the smem Q/K tiles), then read back for the codes once lo/hi are known. The
+    // compute warps no longer meet at a barrier every step, so a warp that took
+    // the exact path delays the others only when it falls a whole pass behind.
+    constexpr bool kStash = !SPLIT && PARO_P_STASH;
     float pv0[32];
     if constexpr (kOverlap) {
         __syncwarp();
         if (lane == 0)
             ptx::mbar_arrive(red_bar);
-        compute_p((int)half, pv0);
+        compute_p((int)half, pv0, true);
+        ptx::mbar_wait(red_bar, red_par);
+    } else if constexpr (kStash) {
+        __syncwarp();
+        if (lane == 0)
+            ptx::mbar_arrive(red_bar);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            float pv[32];
+            compute_p(h2, pv, true);
+            ptx::tmem_st32(s_addr + h2 * 32, reinterpret_cast<const uint32_t(&)[32]>(pv));
+        }
         ptx::mbar_wait(red_bar, red_par);
     } else {
         ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
@@ -595,13 +613,32 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     };
     if constexpr (kOverlap) {
         quantize_store((int)half, pv0);
+    } else if constexpr (kStash) {
+        ptx::tmem_st_wait();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t x[32];
+            ptx::tmem_ld32(s_addr + h2 * 32, x);
+            ptx::tmem_ld_wait();
+            quantize_store(h2, reinterpret_cast<const float(&)[32]>(x));
+        }
     } else {
 #pragma unroll
         for (int hh = 0; hh < (SPLIT ? 1 : 2); ++hh) { // the warp's key-column half (SPLIT) or both
             const int h2 = SPLIT ? (int)half : hh;
             float pv[32];
-            compute_p(h2, pv);
+            // the tail mask is applied below, not here: a warp-uniform branch between
+            // the exponentials and the quantizer keeps ptxas from overlapping them
+            compute_p(h2, pv, SPLIT);
             quantize_store(h2, pv);
+        }
+        if (!SPLIT && tail_any) { // rare (the last key block): the row sum again without the padded columns
+            sum2 = pk(0.f, 0.f);
+#pragma unroll 1
+            for (int h2 = 0; h2 < 2; ++h2) {
+                float pv[32];
+                compute_p(h2, pv, true);
+            }
         }
     }
     if (!valid)
@@ -824,6 +861,9 @@ __device__ __forceinline__ void unpack_v_tile(const uint8_t* pk, uint8_t* vt, ui
 
 // DUMP: the P-code dump test hook is compiled in (a separate instantiation, so the
 // product kernel carries no extra registers for it)
+#ifndef PARO_DIAG_NOI2F
+#define PARO_DIAG_NOI2F 0 // diagnostic builds only: epilogue reads int32 P.V as fp32 bits (wrong results)
+#endif
 #ifndef PARO_DIAG_NOUNPACK
 #define PARO_DIAG_NOUNPACK 0 // diagnostic builds only: skip the INT4 unpack (wrong results)
 #endif
@@ -1282,7 +1322,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                         for (int hh = 0; hh < 2; ++hh) {
                             const int j = q4 * 4 + hh * 2;
                             const uint64_t x2 =
-                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
                             const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
                             acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
                         }
@@ -1422,7 +1462,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                         for (int hh = 0; hh < 2; ++hh) {
                             const int j = q4 * 4 + hh * 2;
                             const uint64_t x2 =
-                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
                             const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
                             acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
                         }

@@ -201,6 +201,10 @@ constexpr double kLog2e = 1.4426950408889634;
 #ifndef PARO_RED_MBAR
 #define PARO_RED_MBAR 1
 #endif
+// d=64: p parked in TMEM across the P-group reduction (mbarrier, no bar.sync)
+#ifndef PARO_P_STASH
+#define PARO_P_STASH 0
+#endif
 #ifndef PARO_KAPPA
 #define PARO_KAPPA 6e-7f
 #endif
