@@ -266,6 +266,13 @@ constexpr float kErrS = 5e-7f, kGapSlack = 2e-5f;
 // Lanes whose q-block has no tile this step (`live` false) run the same
 // instructions but change no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
+#ifdef PARO_K3_PROF
+// [0..1][4]: the four softmax warps' barrier arrivals, [2..3][4]: their step starts (by step parity)
+__device__ __forceinline__ long long (*prof_smem())[4] {
+    __shared__ long long a[4][4];
+    return a;
+}
+#endif
 template <int D, bool SPLIT>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
@@ -274,7 +281,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
                                              uint32_t half, float4* xch, uint16_t* xlist, uint32_t red_bar,
-                                             uint32_t red_par, unsigned long long (&prof)[14]) {
+                                             uint32_t red_par, unsigned long long (&prof)[18]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -542,6 +549,9 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     // the exact path delays the others only when it falls a whole pass behind.
     constexpr bool kStash = !SPLIT && PARO_P_STASH;
     float pv0[32];
+#ifdef PARO_K3_PROF
+    long long tbar = 0;
+#endif
     if constexpr (kOverlap) {
         __syncwarp();
         if (lane == 0)
@@ -560,7 +570,45 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         }
         ptx::mbar_wait(red_bar, red_par);
     } else {
+        PROF_T(tb0);
+#ifdef PARO_K3_PROF
+        long long(*prof_arrive)[4] = prof_smem();
+        if (G == 1 && lane == 0)
+            prof_arrive[red_par][(threadIdx.x >> 5) & 3] = tb0;
+#endif
         ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
+        PROF_T(tb1);
+#ifdef PARO_K3_PROF
+        tbar = tb1;
+        if (G == 1) {
+            PROF_ADD(11, tb0 - tp1);
+            PROF_ADD(12, tb1 - tb0);
+            if (((threadIdx.x >> 5) & 3) == 0) { // spread of the four arrivals, once per CTA step
+                long long a0 = prof_arrive[red_par][0], mn = a0, mx = a0;
+                for (int w = 1; w < 4; ++w) {
+                    mn = min(mn, prof_arrive[red_par][w]);
+                    mx = max(mx, prof_arrive[red_par][w]);
+                }
+                PROF_ADD(14, mx - mn);
+                PROF_ADD(15, 1);
+                a0 = prof_arrive[2 + red_par][0], mn = a0, mx = a0;
+                for (int w = 1; w < 4; ++w) {
+                    mn = min(mn, prof_arrive[2 + red_par][w]);
+                    mx = max(mx, prof_arrive[2 + red_par][w]);
+                }
+                PROF_ADD(16, mx - mn); // spread of the four step starts
+                if (lane == 0) {
+                    long long amn = prof_arrive[red_par][0];
+                    for (int w = 1; w < 4; ++w)
+                        amn = min(amn, prof_arrive[red_par][w]);
+                    for (int w = 0; w < 4; ++w) {
+                        atomicAdd(&g_profq[w], (unsigned long long)(prof_arrive[2 + red_par][w] - mn));
+                        atomicAdd(&g_profq[4 + w], (unsigned long long)(prof_arrive[red_par][w] - amn));
+                    }
+                }
+            }
+        }
+#endif
     }
     float lo = red_r[0].x, hi = red_r[0].y;
 #pragma unroll
@@ -574,6 +622,10 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const float inv = __frcp_rn(pscale);
     PROF_T(tp2);
     PROF_ADD(2, tp2 - tp1);
+#ifdef PARO_K3_PROF
+    if (G == 1 && !kOverlap && !kStash)
+        PROF_ADD(13, tp2 - tbar);
+#endif
     const float kap = kKappa;
     const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
     const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
@@ -1156,7 +1208,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         float* lsm = reinterpret_cast<float*>(smem + C::OFF_L);
         const uint32_t tail = L.N & 63;
         uint32_t T = 0, I = 0;
-        unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long prof[18] = {};
         for (uint32_t rr = 0;; ++rr) {
             if (!PARO_DYNAMIC && rr >= rounds)
                 break;
@@ -1195,6 +1247,10 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 ptx::tc_fence_after();
                 PROF_T(tw1);
                 PROF_ADD(0, tw1 - tw0);
+#ifdef PARO_K3_PROF
+                if (lane == 0)
+                    prof_smem()[2 + (T & 1)][quad] = tw1;
+#endif
                 const float* meta =
                     reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES + 4 * C::KV_BYTES +
                                                    side * C::META_BYTES);
@@ -1256,8 +1312,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         if (lane == 0) {
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
-            for (int i = 8; i < 11; ++i)
-                atomicAdd(&g_prof[8 + i], prof[i]);
+            for (int i = 8; i < 18; ++i)
+                if (i < 11 || i > 13 || G == 1)
+                    atomicAdd(&g_prof[8 + i], prof[i]);
         }
 #endif
         } else {
@@ -1394,7 +1451,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         const uint32_t tail = L.N & 63;
         constexpr int DH = D / 2; // O columns per warp
         uint32_t T = 0, I = 0;
-        unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long prof[18] = {};
         for (uint32_t rr = 0;; ++rr) {
             if (!PARO_DYNAMIC && rr >= rounds)
                 break;
@@ -1573,7 +1630,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         if (lane == 0) {
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
-            for (int i = 8; i < 14; ++i)
+            for (int i = 8; i < 18; ++i)
                 atomicAdd(&g_prof[8 + i], prof[i]);
         }
 #endif
@@ -1715,6 +1772,8 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
 
 cudaError_t launch_k3_64(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          int num_sms, cudaStream_t st);
+cudaError_t launch_k3_dec(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                          int num_sms, cudaStream_t st);
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
@@ -1754,7 +1813,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
 #endif
 #ifdef PARO_K3_PROF
     if (getenv("PARO_K3_PROF_PRINT")) {
-        unsigned long long h[24];
+        unsigned long long h[32];
         cudaDeviceSynchronize();
         cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
         const double n = (double)(h[7] ? h[7] : 1);
@@ -1768,6 +1827,17 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
                 (double)h[16] / (h[18] ? h[18] : 1), (double)h[17] / (h[18] ? h[18] : 1));
         fprintf(stderr, "[k3 prof] d=128 pass1: scan %.0f exchange %.0f dp4a %.0f rescan %.0f tail %.0f (rescans %.4f)\n",
                 h[16] / n, h[17] / n, h[18] / n, h[19] / n, h[20] / n, h[21] / n);
+        {
+            unsigned long long q[8];
+            cudaMemcpyFromSymbol(q, g_profq, sizeof(q));
+            const double ns = (double)(h[23] ? h[23] : 1);
+            fprintf(stderr, "[k3 prof] per quad lateness: start %.0f %.0f %.0f %.0f arrival %.0f %.0f %.0f %.0f\n", q[0] / ns,
+                    q[1] / ns, q[2] / ns, q[3] / ns, q[4] / ns, q[5] / ns, q[6] / ns, q[7] / ns);
+            memset(q, 0, sizeof(q));
+            cudaMemcpyToSymbol(g_profq, q, sizeof(q));
+        }
+        fprintf(stderr, "[k3 prof] d=64 reduce: to-barrier %.0f barrier %.0f after %.0f; arrival spread %.0f start spread %.0f per CTA step\n",
+                h[19] / n, h[20] / n, h[21] / n, (double)h[22] / (h[23] ? h[23] : 1), (double)h[24] / (h[23] ? h[23] : 1));
         memset(h, 0, sizeof(h));
         cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }
@@ -1776,6 +1846,10 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
     static const bool slots64 = getenv("PARO_K3_SLOTS") && atoi(getenv("PARO_K3_SLOTS")) != 0;
     if (L.D == 64 && slots64 && !L.v_packed)
         return launch_k3_64(p, tq, tk, tv, num_sms, st);
+    // d = 64 decoupled softmax / quantizer layout (attention_dec_kernel.cu); packed INT4 V stays here
+    static const bool dec64 = getenv("PARO_K3_DEC") && atoi(getenv("PARO_K3_DEC")) != 0;
+    if (L.D == 64 && dec64 && !L.v_packed && PARO_DYNAMIC)
+        return launch_k3_dec(p, tq, tk, tv, num_sms, st);
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);
     const int grid = (int)(p.n_items < slots ? p.n_items : slots);
     return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, grid, st) : launch_k3_t<128>(p, tq, tk, tv, tvp, grid, st);

@@ -67,7 +67,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 //   [8..11] epilogue: wait, dequant, store, steps
 //   [12..15] mma: wait KV/S, wait P/O, issue, steps
 #ifdef PARO_K3_PROF
-static __device__ unsigned long long g_prof[24];
+static __device__ unsigned long long g_prof[32];
+static __device__ unsigned long long g_profq[8];
 #define PROF_T(v) const long long v = clock64()
 #define PROF_ADD(i, d) prof[i] += (unsigned long long)(d)
 #else
