@@ -52,23 +52,35 @@
 
 namespace paro {
 
+// The four roles' hot loops share each sub-partition's instruction cache: the
+// per-half / per-chunk loops stay rolled (ncu: no_instruction stalls otherwise)
+#ifndef PARO_DEC_UNROLL
+#define PARO_DEC_UNROLL 1
+#endif
+constexpr int kDecUnroll = PARO_DEC_UNROLL;
+
 struct KDec {
     static constexpr int D = 64;
     static constexpr int NS = 3;  // K/V stages
-    static constexpr int NB = 4;  // TMEM buffers (S -> p -> P.V), 64 columns each
-    static constexpr int THREADS = 384;
+    static constexpr int NB = 3;  // TMEM buffers (S -> p -> P.V), 64 columns each; columns 192-255: the accumulators
+    static constexpr uint32_t TM_ACC = 192;
+    static constexpr int THREADS = 512;
     static constexpr int MINB = 2;
-    static constexpr uint32_t REG_LAUNCH = (65536 / (THREADS * MINB)) / 8 * 8; // 80
+    static constexpr uint32_t REG_LAUNCH = (65536 / (THREADS * MINB)) / 8 * 8; // 64
     static constexpr uint32_t REG_CTRL = 24;
 #ifndef PARO_DEC_MMA_NS
 #define PARO_DEC_MMA_NS 64
 #endif
 #ifndef PARO_DEC_REG_SOFT
-#define PARO_DEC_REG_SOFT 88
+#define PARO_DEC_REG_SOFT 96
 #endif
-    // warpgroup 0's release goes to the softmax and quantizer warpgroups: 128 x (24 + 88 + 128) = 384 x 80
+#ifndef PARO_DEC_REG_QUANT
+#define PARO_DEC_REG_QUANT 80
+#endif
+    // warpgroup 0's release goes to the others: 128 x (24 + 96 + 80 + 56) = 512 x 64
     static constexpr uint32_t REG_SOFT = PARO_DEC_REG_SOFT;
-    static constexpr uint32_t REG_QUANT = 3 * REG_LAUNCH - REG_CTRL - REG_SOFT;
+    static constexpr uint32_t REG_QUANT = PARO_DEC_REG_QUANT;
+    static constexpr uint32_t REG_EPI = 4 * REG_LAUNCH - REG_CTRL - REG_SOFT - REG_QUANT;
     static constexpr uint32_t QT_BYTES = 64 * 64, KV_BYTES = 64 * 64;
     static constexpr uint32_t META_BYTES = (4 + 64) * 4;
     static constexpr uint32_t STAGE_BYTES = (4 * KV_BYTES + 2 * META_BYTES + 1023) / 1024 * 1024;
@@ -77,7 +89,8 @@ struct KDec {
     static constexpr uint32_t OFF_STAGE = 4 * QT_BYTES;                    // K_A, K_B, V_A, V_B, meta_A, meta_B
     static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES;        // [2 parity][2 side] P codes
     static constexpr uint32_t OFF_U = OFF_P + 4 * P_BYTES;                 // [NB][2 side][64] column offsets
-    static constexpr uint32_t OFF_RED = OFF_U + NB * 2 * 64 * 4;           // [2 parity][4 quad][2 side] float2
+    static constexpr uint32_t OFF_RM = OFF_U + NB * 2 * 64 * 4;            // [NB][2 side][64] float4 row meta
+    static constexpr uint32_t OFF_RED = OFF_RM + NB * 2 * 64 * 16;         // [2 parity][4 quad][2 side] float2
     static constexpr uint32_t OFF_ROWSTAT = OFF_RED + 2 * 4 * 2 * 8;       // [2 parity][2 side][64] RowStatD
     static constexpr uint32_t OFF_XLIST = OFF_ROWSTAT + 2 * 2 * 64 * 48;   // [4 quantizer warps][512] u16
     static constexpr uint32_t OFF_BAR = OFF_XLIST + 4 * 512 * 2;
@@ -89,6 +102,7 @@ struct KDec {
     static constexpr uint32_t LANE16 = 16u << 16;
 };
 static_assert(KDec::SMEM * 2 <= 227 * 1024, "two CTAs per SM");
+static_assert(KDec::REG_EPI >= 56, "epilogue registers");
 
 // barrier indices
 enum : uint32_t {
@@ -97,16 +111,18 @@ enum : uint32_t {
     DB_KVFULL = 4,    // [NS]
     DB_KVEMPTY = 7,   // [NS] MMA commit after the step's P.V
     DB_SFULL = 10,    // [NB] QK of the step landed in its buffer
-    DB_RED = 14,      // [2] 4 softmax warps: row stats, P extremes and p of the step published
-    DB_QDONE = 16,    // [2] 4 quantizer warps: done with the step's row stats / extremes
-    DB_PFULL = 18,    // [2] 4 quantizer warps: P codes + column offsets of the step written
-    DB_PEMPTY = 20,   // [2] MMA commit after the step's P.V (P tile free)
-    DB_OFULL = 22,    // [NB] P.V of the step landed in its buffer
-    DB_BEMPTY = 26,   // [NB] 4 quantizer warps: the step's P.V read (buffer free for QK of step + 4)
-    DB_ITEMFULL = 30, // [2]
-    DB_ITEMEMPTY = 32 // [2]
+    DB_RED = 13,      // [2] 4 softmax warps: row stats, P extremes and p of the step published
+    DB_QDONE = 15,    // [2] 4 quantizer warps: done with the step's row stats / extremes
+    DB_PFULL = 17,    // [4] 4 quantizer warps: P codes, column offsets and row meta of the step written.
+                      //     Four deep: the epilogue tests it after the quantizers may have run two steps
+                      //     further (a two-deep ring would have wrapped its phase parity)
+    DB_PEMPTY = 21,   // [2] MMA commit after the step's P.V (P tile free)
+    DB_OFULL = 23,    // [NB] P.V of the step landed in its buffer
+    DB_BEMPTY = 26,   // [NB] 4 epilogue warps: the step's P.V read (buffer free for QK of step + NB)
+    DB_ITEMFULL = 29, // [2]
+    DB_ITEMEMPTY = 31 // [2]
 };
-static_assert(DB_ITEMEMPTY + 2 == KDec::NBAR, "barrier block");
+static_assert(DB_ITEMEMPTY + 2 <= KDec::NBAR, "barrier block");
 
 // per row and step, written by the softmax warp, read by the quantizers
 struct RowStatD { // 48 bytes
@@ -150,15 +166,16 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
             ptx::mbar_init(bar(DB_QEMPTY + i), 1 + 4);
             ptx::mbar_init(bar(DB_RED + i), 4);
             ptx::mbar_init(bar(DB_QDONE + i), 4);
-            ptx::mbar_init(bar(DB_PFULL + i), 4);
             ptx::mbar_init(bar(DB_PEMPTY + i), 1);
             ptx::mbar_init(bar(DB_ITEMFULL + i), 1);
-            ptx::mbar_init(bar(DB_ITEMEMPTY + i), 1 + 4 + 4); // MMA, softmax, quantizer warps
+            ptx::mbar_init(bar(DB_ITEMEMPTY + i), 1 + 4 + 4 + 4); // MMA, softmax, quantizer, epilogue warps
         }
         for (int s = 0; s < NS; ++s) {
             ptx::mbar_init(bar(DB_KVFULL + s), 1);
             ptx::mbar_init(bar(DB_KVEMPTY + s), 1);
         }
+        for (int i = 0; i < 4; ++i)
+            ptx::mbar_init(bar(DB_PFULL + i), 4);
         for (int b = 0; b < NB; ++b) {
             ptx::mbar_init(bar(DB_SFULL + b), 1);
             ptx::mbar_init(bar(DB_OFULL + b), 1);
@@ -167,7 +184,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
         ptx::fence_barrier_init();
     }
     if (warp == 1)
-        ptx::tmem_alloc<256>(sbase + C::OFF_TMEMPTR);
+        ptx::tmem_alloc<256>(sbase + C::OFF_TMEMPTR); // NB x 64 ring + 64 accumulator columns
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                     }
                     prog = true;
                 }
-                if (Tp < Tq && ptx::mbar_test(bar(DB_PFULL + (Tp & 1)), (Tp >> 1) & 1)) {
+                if (Tp < Tq && ptx::mbar_test(bar(DB_PFULL + (Tp & 3)), (Tp >> 2) & 1)) {
                     ptx::tc_fence_after();
                     const uint32_t s = Tp % NS, b = Tp & 1, tb = tmem + (Tp % NB) * 64;
                     const uint32_t f = pvf >> (2 * (Tp % NB));
@@ -376,7 +393,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 // -------- pass 1: integer row extremes (4 independent chains)
                 int32_t mx[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN},
                         mn[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
-#pragma unroll
+#pragma unroll kDecUnroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     uint32_t xs[32];
                     ptx::tmem_ld32(s_addr + h2 * 32, xs);
@@ -420,7 +437,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 // -------- pass 2: p, row sum; p parked in TMEM over the row's S
                 const uint64_t c00 = pk(c0, c0), nm = pk(dmax, dmax);
                 uint64_t sum2 = pk(0.f, 0.f);
-#pragma unroll
+#pragma unroll kDecUnroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     uint32_t xs[32];
                     ptx::tmem_ld32(s_addr + h2 * 32, xs);
@@ -484,8 +501,8 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[i], prof[i]);
 #endif
-    } else {
-        // ------------------------------------------------ quantizer + dequant
+    } else if (warp < 12) {
+        // -------------------------------------------------------- quantizer
         ptx::setmaxnreg_inc<C::REG_QUANT>();
         const uint32_t quad = warp & 3;
         const uint32_t side = lane >> 4;
@@ -493,6 +510,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
         const uint32_t lane_base = (quad * 32) << 16;
         const uint32_t tail = L.N & 63;
         uint16_t* xlist = reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + quad * 512;
+        float4* rmeta = reinterpret_cast<float4*>(smem + C::OFF_RM);
         uint32_t T = 0, I = 0;
         unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t rr = 0;; ++rr) {
@@ -510,56 +528,6 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
             const bool valid_row = has_qb && qb * 64 + r < L.N && qb * 64 + r >= L.dp;
             const float sq = L.qsc[(size_t)x.h * L.kb2 + qb];
             const int32_t dslot = DUMP && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
-            uint64_t acc[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                acc[c] = 0ull;
-            float l_fin = 0.f;
-            if (L.dp && valid_row) {
-                const size_t srow = (size_t)x.h * L.kb2 * 64 + qb * 64 + r;
-                const float2* a0 = reinterpret_cast<const float2*>(L.init_acc + srow * 64);
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    acc[c] = pk(a0[c].x, a0[c].y);
-                l_fin = L.init_l[srow];
-            }
-            float g_prev = 1.f, ss_prev = 0.f;
-            // acc = gamma * acc + (pscale * vscale) * ip + u_c for step U (its own row's gamma, ss)
-            auto dequant = [&](uint32_t U, float g, float ss) {
-                PROF_T(te0);
-                // PFULL(U) orders the other quantizer warps' column offsets before these reads
-                dwait(bar(DB_OFULL + U % NB), (U / NB) & 1);
-                dwait(bar(DB_PFULL + (U & 1)), (U >> 1) & 1);
-                ptx::tc_fence_after();
-                PROF_T(te1);
-                const uint64_t g2 = pk(g, g), ss2 = pk(ss, ss);
-                const float4* u4 = reinterpret_cast<const float4*>(usm + ((U % NB) * 2 + side) * 64);
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t raw[16];
-                    tmem_ld16(tmem + lane_base + (U % NB) * 64 + ch * 16, raw);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const float4 uu = u4[ch * 4 + q4];
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const int j = q4 * 4 + hh * 2;
-                            const uint64_t x2 =
-                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
-                            const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
-                            acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
-                        }
-                    }
-                }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0)
-                    ptx::mbar_arrive(bar(DB_BEMPTY + U % NB));
-                PROF_T(te2);
-                PROF_ADD(4, te1 - te0);
-                PROF_ADD(5, te2 - te1);
-            };
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T % NB, par = T & 1;
                 const bool live = t < nmine;
@@ -571,9 +539,9 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 PROF_T(tqa);
                 PROF_ADD(3, tqa - tq0);
 #endif
-                // the step's p and row stats; its stage (meta, K tiles). The P tile is free:
-                // this warp's dequant of step T - 2 already waited for that P.V to complete.
+                // the step's p and row stats; its P tile free (P.V of step T - 2); its stage (meta, K tiles)
                 dwait(bar(DB_RED + par), (T >> 1) & 1);
+                dwait(bar(DB_PEMPTY + par), ((T >> 1) & 1) ^ 1);
                 dwait(bar(DB_KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
                 PROF_T(tq1);
@@ -582,7 +550,6 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 const float2* red_r = red + par * 8 + side; // [quad q] at red_r[2 q]
                 const RowStatD* rs_r = rowstat + par * 128;
                 const RowStatD me = rs_r[side * 64 + r];
-                l_fin = me.l;
                 uint8_t* prow = smem + C::OFF_P + (par * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
                 float lo = red_r[0].x, hi = red_r[0].y;
 #pragma unroll
@@ -598,7 +565,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
                 const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
                 uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
-#pragma unroll
+#pragma unroll kDecUnroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     uint32_t xs[32];
                     ptx::tmem_ld32(tmem + lane_base + b * 64 + h2 * 32, xs);
@@ -782,55 +749,140 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 // when idle (an idle side's meta slot is not loaded: stale smem, maybe NaN)
                 const float vsc = meta[2];
                 usm[(b * 2 + side) * 64 + r] = live ? (lo * vsc) * meta[4 + r] : 0.f;
-                const float g_cur = live ? me.gamma : 1.f, ss_cur = live ? pscale * vsc : 0.f;
+                // the epilogue's row meta of the step: gamma, (pscale * vscale), the row sum after it
+                rmeta[(b * 2 + side) * 64 + r] = make_float4(live ? me.gamma : 1.f, live ? pscale * vsc : 0.f, me.l, 0.f);
                 ptx::fence_proxy_async_smem(); // P codes -> the tensor core's view
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::mbar_arrive(bar(DB_PFULL + par));
+                    ptx::mbar_arrive(bar(DB_PFULL + (T & 3)));
                     ptx::mbar_arrive(bar(DB_QDONE + par));
                 }
                 PROF_ADD(0, tq1 - tq0);
                 PROF_ADD(1, tq2 - tq1);
                 PROF_ADD(2, tq3 - tq2);
                 PROF_ADD(7, 1);
-                if (t > 0) // its P.V was issued a step earlier
-                    dequant(T - 1, g_prev, ss_prev);
-                g_prev = g_cur;
-                ss_prev = ss_cur;
             }
-            if (x.n > 0)
-                dequant(T - 1, g_prev, ss_prev);
             __syncwarp();
             if (lane == 0)
                 ptx::mbar_arrive(bar(DB_QEMPTY + (I & 1))); // no more exact-path reads of the item's Q tiles
             ++I;
-            if (valid_row) {
-                const float l = l_fin;
-                const uint32_t orig = perm_src(L.perm[x.h], qb * 64 + r);
-                float4* dst = reinterpret_cast<float4*>(P.out + ((size_t)x.h * L.N + orig) * 64);
-                if (l == 0.f) {
-#pragma unroll
-                    for (int c = 0; c < 16; ++c)
-                        dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-                } else {
-                    const float il = 1.0f / l;
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        float a0, a1, a2, a3;
-                        upk(acc[2 * c], a0, a1);
-                        upk(acc[2 * c + 1], a2, a3);
-                        dst[c] = make_float4(a0 * il, a1 * il, a2 * il, a3 * il);
-                    }
-                }
-                if (P.zeroed)
-                    P.zeroed[(size_t)x.h * L.N + orig] = l == 0.f ? 1 : 0;
-            }
         }
 #ifdef PARO_K3_PROF
         if (lane == 0)
             for (int i = 0; i < 8; ++i)
                 atomicAdd(&g_prof[8 + i], prof[i]);
+#endif
+    } else {
+        // --------------------------------------------------------- epilogue
+        // acc (fp32, TMEM columns 192-255, the row's lane) = gamma acc + (pscale vscale) ip + u_c
+        // per step, then O = acc / l at the ORIGINAL token row
+        ptx::setmaxnreg_dec<C::REG_EPI>();
+        const uint32_t quad = warp & 3;
+        const uint32_t side = lane >> 4;
+        const uint32_t r = quad * 16 + (lane & 15);
+        const uint32_t lane_base = (quad * 32) << 16;
+        const uint32_t tacc = tmem + lane_base + C::TM_ACC;
+        const float4* rmeta = reinterpret_cast<const float4*>(smem + C::OFF_RM);
+        uint32_t T = 0;
+        unsigned long long prof[4] = {0, 0, 0, 0};
+        for (uint32_t rr = 0;; ++rr) {
+            const int it = next_item(rr);
+            __syncwarp();
+            if (lane == 0)
+                ptx::mbar_arrive(bar(DB_ITEMEMPTY + (rr & 1)));
+            if (it < 0)
+                break;
+            const Item x = load_item(L, (uint32_t)it);
+            const bool has_qb = side ? x.qb != 0xffffu : true;
+            const uint32_t qb = side ? (has_qb ? x.qb : 0u) : x.qa;
+            const bool valid_row = has_qb && qb * 64 + r < L.N && qb * 64 + r >= L.dp;
+            float l_fin = 0.f;
+            { // the row's starting accumulators: 0, or K4's dense-prefix state
+                const size_t srow = (size_t)x.h * L.kb2 * 64 + qb * 64 + r;
+                const bool init = L.dp && valid_row;
+                if (init)
+                    l_fin = L.init_l[srow];
+#pragma unroll kDecUnroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t a[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        a[j] = init ? __float_as_uint(L.init_acc[srow * 64 + ch * 16 + j]) : 0u;
+                    tmem_st16(tacc + ch * 16, a);
+                }
+            }
+            for (uint32_t t = 0; t < x.n; ++t, ++T) {
+                const uint32_t b = T % NB;
+                PROF_T(te0);
+                // PFULL orders the quantizers' column offsets and row meta before these reads
+                dwait(bar(DB_OFULL + b), (T / NB) & 1);
+                dwait(bar(DB_PFULL + (T & 3)), (T >> 2) & 1);
+                ptx::tc_fence_after();
+                PROF_T(te1);
+                const float4 rm = rmeta[(b * 2 + side) * 64 + r];
+                l_fin = rm.z;
+                const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
+                const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + side) * 64);
+                ptx::tmem_st_wait(); // the previous step's accumulator stores
+#pragma unroll kDecUnroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t raw[16], a[16];
+                    tmem_ld16(tmem + lane_base + b * 64 + ch * 16, raw);
+                    tmem_ld16(tacc + ch * 16, a);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 uu = u4[ch * 4 + q4];
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int j = q4 * 4 + hh * 2;
+                            const uint64_t x2 =
+                                pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                            const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
+                            const uint64_t a2 = fma2(pk(__uint_as_float(a[j]), __uint_as_float(a[j + 1])), g2, t2);
+                            float y0, y1;
+                            upk(a2, y0, y1);
+                            a[j] = __float_as_uint(y0);
+                            a[j + 1] = __float_as_uint(y1);
+                        }
+                    }
+                    tmem_st16(tacc + ch * 16, a);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    ptx::mbar_arrive(bar(DB_BEMPTY + b));
+                PROF_T(te2);
+                PROF_ADD(0, te1 - te0);
+                PROF_ADD(1, te2 - te1);
+                PROF_ADD(3, 1);
+            }
+            ptx::tmem_st_wait();
+            // (tcgen05.ld is warp-collective: every lane loads, valid rows store)
+            const float l = l_fin;
+            const uint32_t orig = valid_row ? perm_src(L.perm[x.h], qb * 64 + r) : 0u;
+            float4* dst = reinterpret_cast<float4*>(P.out + ((size_t)x.h * L.N + orig) * 64);
+            const float il = l == 0.f ? 0.f : 1.0f / l;
+#pragma unroll kDecUnroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t a[16];
+                tmem_ld16(tacc + ch * 16, a);
+                ptx::tmem_ld_wait();
+                if (valid_row) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        dst[ch * 4 + c] = make_float4(__uint_as_float(a[4 * c]) * il, __uint_as_float(a[4 * c + 1]) * il,
+                                                      __uint_as_float(a[4 * c + 2]) * il, __uint_as_float(a[4 * c + 3]) * il);
+                }
+            }
+            if (valid_row && P.zeroed)
+                P.zeroed[(size_t)x.h * L.N + orig] = l == 0.f ? 1 : 0;
+        }
+#ifdef PARO_K3_PROF
+        if (lane == 0)
+            for (int i = 0; i < 4; ++i)
+                atomicAdd(&g_prof[16 + i], prof[i]);
 #endif
     }
 
@@ -856,11 +908,13 @@ cudaError_t launch_k3_dec(const K3Params& p, const CUtensorMap& tq, const CUtens
         cudaDeviceSynchronize();
         cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
         const double n = (double)(h[7] ? h[7] : 1), m = (double)(h[15] ? h[15] : 1);
+        const double e = (double)(h[19] ? h[19] : 1);
         fprintf(stderr,
-                "[k3dec prof] softmax warp/step: wait %.0f (QDONE %.0f then S %.0f) pass1 %.0f pass2+publish %.0f | quantizer warp/step: "
-                "wait %.0f (RED %.0f) quantize %.0f exact %.0f dequant-wait %.0f dequant %.0f (exact entries %.4f)\n",
-                h[0] / n, h[3] / n, h[4] / n, h[1] / n, h[2] / n, h[8] / m, h[11] / m, h[9] / m, h[10] / m, h[12] / m,
-                h[13] / m, h[14] / m);
+                "[k3dec prof] softmax warp/step: wait %.0f (QDONE %.0f then S %.0f) pass1 %.0f pass2+publish %.0f | "
+                "quantizer: wait %.0f (RED %.0f) quantize %.0f exact %.0f (exact entries %.4f) | epilogue: wait %.0f "
+                "dequant %.0f\n",
+                h[0] / n, h[3] / n, h[4] / n, h[1] / n, h[2] / n, h[8] / m, h[11] / m, h[9] / m, h[10] / m, h[14] / m,
+                h[16] / e, h[17] / e);
         memset(h, 0, sizeof(h));
         cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }

@@ -114,10 +114,32 @@ __device__ __forceinline__ void watchdog_trip() {
 // The suspending try_wait also returns early when other barrier traffic in a busy
 // CTA wakes it; the probe loop (one L1 load of the limit and a clock read between
 // probes) measured faster than tighter loops in K3 (round 1).
+#ifndef PARO_WAIT_V2
+#define PARO_WAIT_V2 0
+#endif
+static __device__ uint32_t g_zero_word = 0;
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity))
         return;
     const uint64_t t0 = globaltimer();
+    if (PARO_WAIT_V2) {
+        // fewer instructions per probe: the suspending try_wait returns whenever
+        // barrier traffic wakes the warp, so the loop body is what spinning costs
+        // the sub-partition. One L1 hit (folded into the parity operand) paces the
+        // probes; the watchdog clock is read every 64th probe.
+        for (uint32_t it = 1;; ++it) {
+            if (mbar_try_wait_sleep(bar, parity))
+                return;
+            uint32_t z;
+            asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(z) : "l"(&g_zero_word));
+            parity ^= z;
+            if ((it & 63u) == 0) {
+                const unsigned long long lim = g_watchdog_ns;
+                if (lim && globaltimer() - t0 > lim)
+                    __trap();
+            }
+        }
+    }
     while (!mbar_try_wait_sleep(bar, parity)) {
         const unsigned long long lim = g_watchdog_ns;
         if (lim && globaltimer() - t0 > lim)
