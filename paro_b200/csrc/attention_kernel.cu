@@ -1250,7 +1250,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const bool live = t < nmine;
                 const uint32_t bj = live ? list[t] : 0u;
                 PROF_T(tw0);
-                mbar_wait3(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
+                mbar_wait3t(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
                 PROF_T(tw1);
                 PROF_ADD(0, tw1 - tw0);
@@ -1374,7 +1374,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const float4 rm = rowmeta[(b * 2 + side) * 64 + r];
                 const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
                 const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + side) * D);
-#pragma unroll kK3Unroll
+#pragma unroll
                 for (int ch = 0; ch < D / 16; ++ch) {
                     uint32_t raw[16];
                     tmem_ld16(tmem + lane_base + C::TM_O + b * D + ch * 16, raw);
@@ -1546,7 +1546,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const bool live = t < nmine;
                 const uint32_t bj = live ? list[t] : 0u;
                 PROF_T(tw0);
-                mbar_wait3(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
+                mbar_wait3t(bar(BR::SFULL + b), ph, bar(BR::PEMPTY + b), ph ^ 1, bar(BR::KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
                 PROF_T(tw1);
                 PROF_ADD(0, tw1 - tw0);

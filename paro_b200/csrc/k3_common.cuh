@@ -183,6 +183,18 @@ __device__ __forceinline__ void mbar_wait3(uint32_t b0, uint32_t p0, uint32_t b1
         ptx::mbar_wait(b2, p2);
 }
 
+// the same with non-suspending probes first: a completed phase costs a test_wait,
+// not a suspending try_wait (PARO_WAIT_TEST=0 restores mbar_wait3)
+#ifndef PARO_WAIT_TEST
+#define PARO_WAIT_TEST 1
+#endif
+__device__ __forceinline__ void mbar_wait3t(uint32_t b0, uint32_t p0, uint32_t b1, uint32_t p1, uint32_t b2,
+                                            uint32_t p2) {
+    if (PARO_WAIT_TEST && ptx::mbar_test(b0, p0) && ptx::mbar_test(b1, p1) && ptx::mbar_test(b2, p2))
+        return;
+    mbar_wait3(b0, p0, b1, p1, b2, p2);
+}
+
 __device__ __forceinline__ uint64_t fma2_rm(uint64_t a, uint64_t b, uint64_t c) {
     uint64_t r;
     asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
