@@ -71,6 +71,9 @@ struct KDec {
 #ifndef PARO_DEC_MMA_NS
 #define PARO_DEC_MMA_NS 64
 #endif
+#ifndef PARO_DEC_RS3
+#define PARO_DEC_RS3 1
+#endif
 #ifndef PARO_DEC_REG_SOFT
 #define PARO_DEC_REG_SOFT 96
 #endif
@@ -90,9 +93,12 @@ struct KDec {
     static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES;        // [2 parity][2 side] P codes
     static constexpr uint32_t OFF_U = OFF_P + 4 * P_BYTES;                 // [NB][2 side][64] column offsets
     static constexpr uint32_t OFF_RM = OFF_U + NB * 2 * 64 * 4;            // [NB][2 side][64] float4 row meta
-    static constexpr uint32_t OFF_RED = OFF_RM + NB * 2 * 64 * 16;         // [2 parity][4 quad][2 side] float2
-    static constexpr uint32_t OFF_ROWSTAT = OFF_RED + 2 * 4 * 2 * 8;       // [2 parity][2 side][64] RowStatD
-    static constexpr uint32_t OFF_XLIST = OFF_ROWSTAT + 2 * 2 * 64 * 48;   // [4 quantizer warps][512] u16
+    // row statistics / P extremes ring: RS deep. RS = NB needs no quantizer -> softmax hand-back (the
+    // S buffer ring already keeps the softmax within NB steps of the epilogue); RS = 2 uses QDONE
+    static constexpr int RS = PARO_DEC_RS3 ? NB : 2;
+    static constexpr uint32_t OFF_RED = OFF_RM + NB * 2 * 64 * 16;         // [RS][4 quad][2 side] float2
+    static constexpr uint32_t OFF_ROWSTAT = OFF_RED + RS * 4 * 2 * 8;      // [RS][2 side][64] RowStatD
+    static constexpr uint32_t OFF_XLIST = OFF_ROWSTAT + RS * 2 * 64 * 48;  // [4 quantizer warps][512] u16
     static constexpr uint32_t OFF_BAR = OFF_XLIST + 4 * 512 * 2;
     static constexpr uint32_t NBAR = 34;
     static constexpr uint32_t OFF_TMEMPTR = OFF_BAR + NBAR * 8;
@@ -111,16 +117,16 @@ enum : uint32_t {
     DB_KVFULL = 4,    // [NS]
     DB_KVEMPTY = 7,   // [NS] MMA commit after the step's P.V
     DB_SFULL = 10,    // [NB] QK of the step landed in its buffer
-    DB_RED = 13,      // [2] 4 softmax warps: row stats, P extremes and p of the step published
-    DB_QDONE = 15,    // [2] 4 quantizer warps: done with the step's row stats / extremes
-    DB_PFULL = 17,    // [4] 4 quantizer warps: P codes, column offsets and row meta of the step written.
+    DB_RED = 13,      // [RS] 4 softmax warps: row stats, P extremes and p of the step published
+    DB_QDONE = 16,    // [2] (RS = 2 only) 4 quantizer warps: done with the step's row stats / extremes
+    DB_PFULL = 18,    // [4] 4 quantizer warps: P codes, column offsets and row meta of the step written.
                       //     Four deep: the epilogue tests it after the quantizers may have run two steps
                       //     further (a two-deep ring would have wrapped its phase parity)
-    DB_PEMPTY = 21,   // [2] MMA commit after the step's P.V (P tile free)
-    DB_OFULL = 23,    // [NB] P.V of the step landed in its buffer
-    DB_BEMPTY = 26,   // [NB] 4 epilogue warps: the step's P.V read (buffer free for QK of step + NB)
-    DB_ITEMFULL = 29, // [2]
-    DB_ITEMEMPTY = 31 // [2]
+    DB_PEMPTY = 22,   // [2] MMA commit after the step's P.V (P tile free)
+    DB_OFULL = 24,    // [NB] P.V of the step landed in its buffer
+    DB_BEMPTY = 27,   // [NB] 4 epilogue warps: the step's P.V read (buffer free for QK of step + NB)
+    DB_ITEMFULL = 30, // [2]
+    DB_ITEMEMPTY = 32 // [2]
 };
 static_assert(DB_ITEMEMPTY + 2 <= KDec::NBAR, "barrier block");
 
@@ -164,7 +170,6 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar(DB_QFULL + i), 1);
             ptx::mbar_init(bar(DB_QEMPTY + i), 1 + 4);
-            ptx::mbar_init(bar(DB_RED + i), 4);
             ptx::mbar_init(bar(DB_QDONE + i), 4);
             ptx::mbar_init(bar(DB_PEMPTY + i), 1);
             ptx::mbar_init(bar(DB_ITEMFULL + i), 1);
@@ -176,6 +181,8 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
         }
         for (int i = 0; i < 4; ++i)
             ptx::mbar_init(bar(DB_PFULL + i), 4);
+        for (int i = 0; i < C::RS; ++i)
+            ptx::mbar_init(bar(DB_RED + i), 4);
         for (int b = 0; b < NB; ++b) {
             ptx::mbar_init(bar(DB_SFULL + b), 1);
             ptx::mbar_init(bar(DB_OFULL + b), 1);
@@ -367,20 +374,23 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
             }
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T % NB, par = T & 1;
+                const uint32_t rsl = T % C::RS, rsp = (T / C::RS) & 1; // row-stat ring slot, phase parity
                 const bool live = t < nmine;
                 const bool valid = live && valid_row;
                 const uint32_t bj = live ? list[t] : 0u;
                 PROF_T(tw0);
                 // S of the step; the step's K/V stage (meta); the quantizers are done with step T - 2's stats
 #ifdef PARO_K3_PROF
-                ptx::mbar_wait(bar(DB_QDONE + par), ((T >> 1) & 1) ^ 1);
+                if (C::RS == 2)
+                    ptx::mbar_wait(bar(DB_QDONE + par), ((T >> 1) & 1) ^ 1);
                 PROF_T(twa);
                 ptx::mbar_wait(bar(DB_SFULL + b), (T / NB) & 1);
                 PROF_T(twb);
                 PROF_ADD(3, twa - tw0);
                 PROF_ADD(4, twb - twa);
 #endif
-                dwait(bar(DB_QDONE + par), ((T >> 1) & 1) ^ 1);
+                if (C::RS == 2)
+                    dwait(bar(DB_QDONE + par), ((T >> 1) & 1) ^ 1);
                 dwait(bar(DB_SFULL + b), (T / NB) & 1);
                 dwait(bar(DB_KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                     gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
                 }
                 if ((lane & 15) == 0)
-                    red[(par * 4 + quad) * 2 + side] = make_float2(gmin, gmax);
+                    red[(rsl * 4 + quad) * 2 + side] = make_float2(gmin, gmax);
                 PROF_T(tw2);
                 // -------- pass 2: p, row sum; p parked in TMEM over the row's S
                 const uint64_t c00 = pk(c0, c0), nm = pk(dmax, dmax);
@@ -482,13 +492,13 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                     st.m32 = m32;
                     st.m64 = m64;
                 }
-                rowstat[(par * 2 + side) * 64 + r] =
+                rowstat[(rsl * 2 + side) * 64 + r] =
                     RowStatD{tmin64, tmax64, m64,   valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f,
                              live ? gamma : 1.f, st.l, smax, valid ? 1u : 0u};
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0)
-                    ptx::mbar_arrive(bar(DB_RED + par));
+                    ptx::mbar_arrive(bar(DB_RED + rsl));
                 PROF_T(tw3);
                 PROF_ADD(0, tw1 - tw0);
                 PROF_ADD(1, tw2 - tw1);
@@ -530,25 +540,26 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
             const int32_t dslot = DUMP && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T % NB, par = T & 1;
+                const uint32_t rsl = T % C::RS, rsp = (T / C::RS) & 1; // row-stat ring slot, phase parity
                 const bool live = t < nmine;
                 const bool valid = live && valid_row;
                 const uint32_t bj = live ? list[t] : 0u;
                 PROF_T(tq0);
 #ifdef PARO_K3_PROF
-                ptx::mbar_wait(bar(DB_RED + par), (T >> 1) & 1);
+                ptx::mbar_wait(bar(DB_RED + rsl), rsp);
                 PROF_T(tqa);
                 PROF_ADD(3, tqa - tq0);
 #endif
                 // the step's p and row stats; its P tile free (P.V of step T - 2); its stage (meta, K tiles)
-                dwait(bar(DB_RED + par), (T >> 1) & 1);
+                dwait(bar(DB_RED + rsl), rsp);
                 dwait(bar(DB_PEMPTY + par), ((T >> 1) & 1) ^ 1);
                 dwait(bar(DB_KVFULL + s), (T / NS) & 1);
                 ptx::tc_fence_after();
                 PROF_T(tq1);
                 const float* meta = reinterpret_cast<const float*>(smem + C::OFF_STAGE + s * C::STAGE_BYTES +
                                                                    4 * C::KV_BYTES + side * C::META_BYTES);
-                const float2* red_r = red + par * 8 + side; // [quad q] at red_r[2 q]
-                const RowStatD* rs_r = rowstat + par * 128;
+                const float2* red_r = red + rsl * 8 + side; // [quad q] at red_r[2 q]
+                const RowStatD* rs_r = rowstat + rsl * 128;
                 const RowStatD me = rs_r[side * 64 + r];
                 uint8_t* prow = smem + C::OFF_P + (par * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
                 float lo = red_r[0].x, hi = red_r[0].y;
@@ -625,7 +636,7 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                     for (int sd = 0; sd < 2; ++sd) {
                         if (!((sd ? rmask >> 16 : rmask & 0xffffu)))
                             continue;
-                        const float2* rd = red + par * 8 + sd;
+                        const float2* rd = red + rsl * 8 + sd;
                         float lo_a = rd[0].x, hi_a = rd[0].y;
 #pragma unroll
                         for (int q = 1; q < 4; ++q) {
@@ -756,7 +767,8 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 __syncwarp();
                 if (lane == 0) {
                     ptx::mbar_arrive(bar(DB_PFULL + (T & 3)));
-                    ptx::mbar_arrive(bar(DB_QDONE + par));
+                    if (C::RS == 2)
+                        ptx::mbar_arrive(bar(DB_QDONE + par));
                 }
                 PROF_ADD(0, tq1 - tq0);
                 PROF_ADD(1, tq2 - tq1);
