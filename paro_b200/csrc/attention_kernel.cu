@@ -54,6 +54,12 @@ namespace paro {
 
 // d=64 per-half (softmax) and per-chunk (epilogue) loops: unrolled (rolling them
 // measured c2 4.39 -> 4.76 ms here; the decoupled kernel is the opposite case)
+// PFULL: one arrival per compute THREAD (each releases its own smem writes -- the
+// P codes, row meta and column offsets the MMA and the epilogue read) instead of
+// __syncwarp + one lane
+#ifndef PARO_PFULL_ALL
+#define PARO_PFULL_ALL 1
+#endif
 #ifndef PARO_K3_UNROLL
 #define PARO_K3_UNROLL 4
 #endif
@@ -561,13 +567,13 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 #endif
     if constexpr (kOverlap) {
         __syncwarp();
-        if (lane == 0)
+        if (PARO_PFULL_ALL || lane == 0) // every lane releases its own row stats / extremes
             ptx::mbar_arrive(red_bar);
         compute_p((int)half, pv0, true);
         ptx::mbar_wait(red_bar, red_par);
     } else if constexpr (kStash) {
         __syncwarp();
-        if (lane == 0)
+        if (PARO_PFULL_ALL || lane == 0) // every lane releases its own row stats / extremes
             ptx::mbar_arrive(red_bar);
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -962,20 +968,22 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(bar(BR::SFULL + b), 1);
             ptx::mbar_init(bar(BR::SEMPTY + b), C::NCW);
-            ptx::mbar_init(bar(BR::PFULL + b), C::NCW);
+            ptx::mbar_init(bar(BR::PFULL + b), C::NCW * (PARO_PFULL_ALL ? 32 : 1));
             ptx::mbar_init(bar(BR::PEMPTY + b), 1 + C::NCW);
             ptx::mbar_init(bar(BR::OFULL + b), 1);
             ptx::mbar_init(bar(BR::OEMPTY + b), C::NCW);
         }
-        ptx::mbar_init(bar(BR::RED), C::NCW); // P-group extremes published (one arrival per compute warp)
+        // P-group extremes and row stats published (one arrival per compute thread)
+        ptx::mbar_init(bar(BR::RED), C::NCW * (PARO_PFULL_ALL ? 32 : 1));
         for (int i = 0; i < 2; ++i) { // item queue: producer -> the other roles
             ptx::mbar_init(bar(BR::ITEMFULL + i), 1);
             ptx::mbar_init(bar(BR::ITEMEMPTY + i), C::NCONS);
         }
         for (int s = 0; s < NS; ++s)
             ptx::mbar_init(bar(BR::VFULL + s), C::NVFULL);
-        ptx::mbar_init(bar(BR::LFULL), 4); // !SPLIT: softmax -> epilogue row sums
-        ptx::mbar_init(bar(BR::LEMPTY), 4);
+        // !SPLIT: softmax -> epilogue row sums (one arrival per thread, as PFULL)
+        ptx::mbar_init(bar(BR::LFULL), 4 * (PARO_PFULL_ALL ? 32 : 1));
+        ptx::mbar_init(bar(BR::LEMPTY), 4 * (PARO_PFULL_ALL ? 32 : 1));
         ptx::fence_barrier_init();
     }
     if (warp == 1)
@@ -1298,7 +1306,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                     u[r + 64 * c] = live ? os * meta[4 + r + 64 * c] : 0.f;
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0)
+                if (PARO_PFULL_ALL || lane == 0) // every lane releases its own P codes / row meta / offsets
                     ptx::mbar_arrive(bar(BR::PFULL + b));
                 PROF_T(tw3);
                 PROF_ADD(5, tw3 - tw2);
@@ -1311,7 +1319,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_wait(bar(BR::LEMPTY), (I & 1) ^ 1);
             lsm[side * 64 + r] = st.l;
             __syncwarp();
-            if (lane == 0)
+            if (PARO_PFULL_ALL || lane == 0)
                 ptx::mbar_arrive(bar(BR::LFULL));
             ++I;
         }
@@ -1406,7 +1414,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_wait(bar(BR::LFULL), I & 1);
             const float l = lsm[side * 64 + r];
             __syncwarp();
-            if (lane == 0)
+            if (PARO_PFULL_ALL || lane == 0)
                 ptx::mbar_arrive(bar(BR::LEMPTY));
             ++I;
             if (valid_row) {
@@ -1593,7 +1601,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0)
+                if (PARO_PFULL_ALL || lane == 0) // every lane releases its own P codes / row meta / offsets
                     ptx::mbar_arrive(bar(BR::PFULL + b));
                 PROF_T(tw3);
                 PROF_ADD(4, tw3 - tw2);
