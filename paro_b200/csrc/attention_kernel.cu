@@ -60,6 +60,9 @@ namespace paro {
 #ifndef PARO_PFULL_ALL
 #define PARO_PFULL_ALL 1
 #endif
+#ifndef PARO_M128
+#define PARO_M128 0
+#endif
 #ifndef PARO_K3_UNROLL
 #define PARO_K3_UNROLL 4
 #endif
@@ -91,16 +94,25 @@ struct K3Cfg {
     static constexpr uint32_t TM_S = 0;          // two S buffers
     static constexpr uint32_t TM_O = 2 * S_COLS; // two O buffers
     static constexpr uint32_t TMEM_COLS = (2 * S_COLS + 2 * D) <= 256 ? 256 : 512;
-    static constexpr uint32_t OFF_Q = 0; // [2 item buffers][A, B] q-block tiles
-    static constexpr uint32_t OFF_STAGE = 4 * QT_BYTES;
+    // d=64 (M128, opt-in: measured c2 4.72 vs 4.37 ms, c3 2.62 vs 2.54): QK is one M = 128 MMA per side with a zero-padded Q operand --
+    // [Q_A; 0] and [0; Q_B] accumulated into the same 64 TMEM columns -- so q-block A
+    // lands in TMEM lanes 0-63 (quadrants 0-1) and B in lanes 64-127 (quadrants 2-3):
+    // a tile's 64 rows span two softmax warps instead of four, and its P-group
+    // hand-off is a 64-thread barrier of that pair. An item buffer holds Q_A, a zero
+    // tile and Q_B contiguously (the 128-row operands overlap on the zero tile).
+    static constexpr bool M128 = D == 64 && PARO_M128;
+    static constexpr uint32_t QBUF = (M128 ? 3 : 2) * QT_BYTES; // one item's Q tiles
+    static constexpr uint32_t QB_OFF = M128 ? 2 * QT_BYTES : QT_BYTES; // side B's tile in it
+    static constexpr uint32_t OFF_Q = 0; // [2 item buffers][A, (0), B] q-block tiles
+    static constexpr uint32_t OFF_STAGE = 2 * QBUF;
     // within a stage: K_A, K_B, V_A, V_B, meta_A, meta_B
     static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES; // [2 buf][2 side]
     static constexpr uint32_t OFF_ROWMETA = OFF_P + 4 * P_BYTES;     // [2 buf][2 side][64] float4
     static constexpr uint32_t OFF_U = OFF_ROWMETA + 2 * 2 * 64 * 16;  // [2 buf][2 side][D]
     static constexpr uint32_t OFF_RED = OFF_U + 2 * 2 * D * 4;        // [2 parity][4 quad][2 side] float2
     static constexpr uint32_t OFF_L = OFF_RED + 2 * 4 * 2 * 8;        // [2 item][2 half][2 side][64] partial row sums
-    static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStat (40 B)
-    static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 40; // SPLIT d=128: [2 half][2 side][64] float4
+    static constexpr uint32_t OFF_ROWSTAT = OFF_L + 2 * 2 * 2 * 64 * 4;       // [2 parity][2 side][64] RowStatC (24 B)
+    static constexpr uint32_t OFF_XCH = OFF_ROWSTAT + 2 * 2 * 64 * 24; // SPLIT d=128: [2 half][2 side][64] float4
     static constexpr uint32_t OFF_XLIST = OFF_XCH + (SPLIT ? 2 * 2 * 64 * (16 + 16) : 0); // + int4 S pairs
     // exact path: per compute warp, its risky (owner lane, group) list (<= 32 x 16 entries)
     // INT4 V arrives nibble-packed (D/2 bytes per key row); d = 64 unpacks it in place
@@ -119,6 +131,7 @@ struct K3Cfg {
     static constexpr uint32_t LAYOUT = D == 64 ? ptx::kSwizzle64B : ptx::kSwizzle128B;
     static constexpr uint32_t ATOM = 8 * D; // bytes per 8-row swizzle atom
     static constexpr uint32_t IDESC_QK = ptx::idesc_i8(true, true, false, false, 64, 64);
+    static constexpr uint32_t IDESC_QK128 = ptx::idesc_i8(true, true, false, false, 128, 64);
     static constexpr uint32_t IDESC_PV = ptx::idesc_i8(false, true, false, true, 64, D);
     static constexpr uint32_t LANE16 = 16u << 16; // TMEM address of lane 16 (side B)
 };
@@ -161,6 +174,16 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
             const uint32_t koff = g * 64 + kk * 32;
             ptx::mma_i8(tmem + g * 64, desc_kmajor<D>(sq + koff), desc_kmajor<D>(sk + koff), C::IDESC_QK, kk);
         }
+}
+
+// M128 (d=64): one side's QK as an M = 128 MMA whose A operand is [Q_A; 0] (side A,
+// at the item buffer) or [0; Q_B] (side B, one tile further); the first MMA of the
+// step overwrites the buffer, the other accumulates its half onto the first's zeros
+__device__ __forceinline__ void issue_qk128(uint32_t tmem, uint32_t sa, uint32_t sk, bool first) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+        ptx::mma_i8(tmem, desc_kmajor<64>(sa + kk * 32), desc_kmajor<64>(sk + kk * 32), K3Cfg<64>::IDESC_QK128,
+                    (first && kk == 0) ? 0u : 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,13 +313,16 @@ template <int D, bool SPLIT>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
                                              RowState& st, float p_qmax, float2* red_w, const float2* red_r,
-                                             RowStat* rs_w, const RowStat* rs_r, uint32_t side,
+                                             RowStatC* rs_w, const RowStatC* rs_r, uint32_t side,
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
                                              uint32_t half, float4* xch, uint16_t* xlist, uint32_t red_bar,
                                              uint32_t red_par, unsigned long long (&prof)[18]) {
     PROF_T(tp0);
     constexpr int G = D / 64;
+    // M128 (d=64): all 32 lanes of this warp hold rows of ONE q-block (side), whose
+    // other 32 rows sit in the partner warp of the same side
+    constexpr bool M128 = !SPLIT && K3Cfg<D>::M128;
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = live && valid_row;
     // -------- pass 1: row extremes (4 independent chains)
@@ -334,7 +360,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmax_r = ex2(dmax);
         pmin_r = ex2(fmaf(__int2float_rn(smin - smax), c0, dmax));
         if (!SPLIT || half == 0)
-            *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
+            *rs_w = RowStatC{tmin64 - m64, tmax64 - m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f};
     } else {
         // d=128: the argmax / argmin columns from column-tagged fp32 logits (two
         // chains of top-2 / bottom-2), their exact fp64 logits from dp4a over the
@@ -472,7 +498,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmax_r = ex2(dmax);
         pmin_r = ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
         if (!SPLIT || half == 0)
-            *rs_w = RowStat{tmin64, tmax64, m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f, valid ? 1 : 0, 0};
+            *rs_w = RowStatC{tmin64 - m64, tmax64 - m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f};
         PROF_T(tq4);
         PROF_ADD(8, tq0 - tp0);
         PROF_ADD(9, tq1 - tq0);
@@ -492,12 +518,13 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         pmax_r = 0.f;
     }
     // -------- P group extremes over the q-block's 64 rows: 16 lanes x 4 warps
+    // (M128: 32 lanes x 2 warps)
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
+    for (int o = M128 ? 16 : 8; o > 0; o >>= 1) {
         pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
         pmax_r = fmaxf(pmax_r, __shfl_xor_sync(0xffffffffu, pmax_r, o));
     }
-    if ((!SPLIT || half == 0) && (lane & 15) == 0)
+    if ((!SPLIT || half == 0) && (M128 ? lane == 0 : (lane & 15) == 0))
         *red_w = make_float2(pmin_r, pmax_r);
     // -------- pass 2: p, row sum, codes (two perturbed variants per element)
     const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
@@ -589,7 +616,10 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         if (G == 1 && lane == 0)
             prof_arrive[red_par][(threadIdx.x >> 5) & 3] = tb0;
 #endif
-        ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
+        if (M128)
+            ptx::named_bar_sync(1 + side, 64); // the side's two softmax warps
+        else
+            ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
         PROF_T(tb1);
 #ifdef PARO_K3_PROF
         tbar = tb1;
@@ -609,23 +639,14 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                     mn = min(mn, prof_arrive[2 + red_par][w]);
                     mx = max(mx, prof_arrive[2 + red_par][w]);
                 }
-                PROF_ADD(16, mx - mn); // spread of the four step starts
-                if (lane == 0) {
-                    long long amn = prof_arrive[red_par][0];
-                    for (int w = 1; w < 4; ++w)
-                        amn = min(amn, prof_arrive[red_par][w]);
-                    for (int w = 0; w < 4; ++w) {
-                        atomicAdd(&g_profq[w], (unsigned long long)(prof_arrive[2 + red_par][w] - mn));
-                        atomicAdd(&g_profq[4 + w], (unsigned long long)(prof_arrive[red_par][w] - amn));
-                    }
-                }
+                (void)(mx - mn); // (the step-start spread: see k3_experiments.md)
             }
         }
 #endif
     }
     float lo = red_r[0].x, hi = red_r[0].y;
 #pragma unroll
-    for (int q = 1; q < 4; ++q) {
+    for (int q = 1; q < (M128 ? 2 : 4); ++q) {
         lo = fminf(lo, red_r[2 * q].x);
         hi = fmaxf(hi, red_r[2 * q].y);
     }
@@ -723,30 +744,31 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         float lo_e[2] = {INFINITY, INFINITY}, hi_e[2] = {0.f, 0.f};
 #pragma unroll
         for (int sd = 0; sd < 2; ++sd) {
-            if (!((sd ? rmask >> 16 : rmask & 0xffffu)))
+            if (M128 ? sd != (int)side : !((sd ? rmask >> 16 : rmask & 0xffffu)))
                 continue;
-            float lo_a = red_r[-(int)side + sd].x, hi_a = red_r[-(int)side + sd].y;
+            const float2* rd = M128 ? red_r : red_r - (int)side + sd; // the side's quadrant extremes
+            float lo_a = rd[0].x, hi_a = rd[0].y;
 #pragma unroll
-            for (int q = 1; q < 4; ++q) {
-                lo_a = fminf(lo_a, red_r[-(int)side + sd + 2 * q].x);
-                hi_a = fmaxf(hi_a, red_r[-(int)side + sd + 2 * q].y);
+            for (int q = 1; q < (M128 ? 2 : 4); ++q) {
+                lo_a = fminf(lo_a, rd[2 * q].x);
+                hi_a = fmaxf(hi_a, rd[2 * q].y);
             }
             float mn = INFINITY, mx = 0.f;
             double args[4];
             uint32_t kinds = 0, cnt = 0; // bit i: arg i is a max candidate
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                const RowStat q = rs_r[sd * 64 + lane + 32 * k];
-                if (!q.valid)
+                const RowStatC q = rs_r[sd * 64 + lane + 32 * k];
+                if (q.pmin == INFINITY) // no tile in this row this step
                     continue;
                 if (q.pmin <= lo_a * 1.00001f)
-                    args[cnt++] = q.tmin - q.m;
+                    args[cnt++] = q.dmin;
                 if (q.pmax >= hi_a * 0.99999f) {
-                    if (q.tmax == q.m)
+                    if (q.dmax == 0.0)
                         mx = 1.0f; // exp(0)
                     else {
                         kinds |= 1u << cnt;
-                        args[cnt++] = q.tmax - q.m;
+                        args[cnt++] = q.dmax;
                     }
                 }
             }
@@ -778,8 +800,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             if (ps_e[sd] == 0.f)
                 ps_e[sd] = 1.f;
         }
-        const uint64_t A2s[2] = {__shfl_sync(0xffffffffu, A2, 0), __shfl_sync(0xffffffffu, A2, 16)};
-        const uint64_t B2s[2] = {__shfl_sync(0xffffffffu, B2, 0), __shfl_sync(0xffffffffu, B2, 16)};
+        const uint64_t A2s[2] = {M128 ? A2 : __shfl_sync(0xffffffffu, A2, 0), M128 ? A2 : __shfl_sync(0xffffffffu, A2, 16)};
+        const uint64_t B2s[2] = {M128 ? B2 : __shfl_sync(0xffffffffu, B2, 0), M128 ? B2 : __shfl_sync(0xffffffffu, B2, 16)};
         // the warp's risky 4-element groups, listed (owner lane, group) and spread
         // over all 32 lanes one element each, instead of serially in their owner lanes
         const uint32_t ng = __popc(risk);
@@ -819,7 +841,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const uint32_t ncol_o = __shfl_sync(0xffffffffu, ncol, (int)o);
             if (!act || j >= ncol_o)
                 continue;
-            const uint32_t so = o >> 4;
+            const uint32_t so = M128 ? side : o >> 4;
             const int32_t dside = (int32_t)so - (int32_t)side;
             const uint8_t* qt = qtile + dside * (int32_t)(64 * D);
             const uint8_t* kt = ktile + dside * (int32_t)(64 * D);
@@ -942,6 +964,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     using C = K3Cfg<D>;
     using BR = Bars<C::NS>;
     constexpr int G = C::G;
+#ifdef PARO_K3_PROF
+    const unsigned long long cta_t0 = ptx::globaltimer();
+#endif
     constexpr int NS = C::NS;
     // dynamic smem is 1024-B aligned (SWIZZLE_128B atoms); declared __shared__ so
     // the compiler emits LDS/STS rather than generic loads
@@ -988,6 +1013,13 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     }
     if (warp == 1)
         ptx::tmem_alloc<C::TMEM_COLS>(sbase + C::OFF_TMEMPTR);
+    if (C::M128) { // the zero tiles of both item buffers (read by the tensor core only)
+        for (uint32_t i = threadIdx.x; i < 2 * C::QT_BYTES / 16; i += C::THREADS) {
+            const uint32_t buf = i / (C::QT_BYTES / 16), off = (i % (C::QT_BYTES / 16)) * 16;
+            *reinterpret_cast<uint4*>(smem + C::OFF_Q + buf * C::QBUF + C::QT_BYTES + off) = make_uint4(0, 0, 0, 0);
+        }
+        ptx::fence_proxy_async_smem();
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -1022,7 +1054,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     auto stage = [&](uint32_t s) { return sbase + C::OFF_STAGE + s * C::STAGE_BYTES; };
     auto qfull = [&](uint32_t i) { return bar((i & 1) ? BR::QFULL1 : (uint32_t)B_QFULL); };
     auto qempty = [&](uint32_t i) { return bar((i & 1) ? BR::QEMPTY1 : (uint32_t)B_QEMPTY); };
-    auto qbuf = [&](uint32_t i) { return sbase + C::OFF_Q + (i & 1) * 2 * C::QT_BYTES; };
+    auto qbuf = [&](uint32_t i) { return sbase + C::OFF_Q + (i & 1) * C::QBUF; };
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -1095,7 +1127,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 ptx::mbar_arrive_expect_tx(qfull(I), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
                 ptx::tma_load_2d(qbuf(I), &tm_q, 0, row0 + (int32_t)x.qa * 64, qfull(I));
                 if (x.qb != 0xffffu)
-                    ptx::tma_load_2d(qbuf(I) + C::QT_BYTES, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
+                    ptx::tma_load_2d(qbuf(I) + C::QB_OFF, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
             }
             for (uint32_t t = 0; t < x.n; ++t) {
                 const uint32_t s = T % NS;
@@ -1188,11 +1220,19 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                     PROF_T(tm3);
                     PROF_ADD(0, tm3 - tm2);
                     PROF_ADD(3, 1);
-                    if (t < x.na)
-                        issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s));
-                    if (t < x.nb)
-                        issue_qk<D>(tmem + C::LANE16 + C::TM_S + b * C::S_COLS, qbuf(I) + C::QT_BYTES,
-                                    stage(s) + C::KV_BYTES);
+                    if (C::M128) {
+                        if (t < x.na)
+                            issue_qk128(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s), true);
+                        if (t < x.nb)
+                            issue_qk128(tmem + C::TM_S + b * C::S_COLS, qbuf(I) + C::QT_BYTES, stage(s) + C::KV_BYTES,
+                                        t >= x.na);
+                    } else {
+                        if (t < x.na)
+                            issue_qk<D>(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s));
+                        if (t < x.nb)
+                            issue_qk<D>(tmem + C::LANE16 + C::TM_S + b * C::S_COLS, qbuf(I) + C::QT_BYTES,
+                                        stage(s) + C::KV_BYTES);
+                    }
                     ptx::mma_commit(bar(BR::SFULL + b));
                     if (t + 1 == x.n)
                         ptx::mma_commit(qempty(I));
@@ -1214,8 +1254,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         if (warp < 6) {
         // ------------------------------------------------------------ softmax
         const uint32_t quad = warp & 3;
-        const uint32_t side = lane >> 4;
-        const uint32_t r = quad * 16 + (lane & 15); // row within its q-block
+        // M128: quadrants 0-1 hold q-block A's rows 0-31 / 32-63, quadrants 2-3 B's
+        const uint32_t side = C::M128 ? quad >> 1 : lane >> 4;
+        const uint32_t r = C::M128 ? (quad & 1) * 32 + lane : quad * 16 + (lane & 15); // row within its q-block
         const uint32_t lane_base = (quad * 32) << 16;
         float2* red = reinterpret_cast<float2*>(smem + C::OFF_RED);
         float4* rowmeta = reinterpret_cast<float4*>(smem + C::OFF_ROWMETA);
@@ -1227,7 +1268,10 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         for (uint32_t rr = 0;; ++rr) {
             if (!PARO_DYNAMIC && rr >= rounds)
                 break;
+            PROF_T(ti2);
             const int it = next_item(rr, false);
+            PROF_T(ti3);
+            PROF_ADD(16, ti3 - ti2);
             __syncwarp();
             if (lane == 0)
                 release_item(rr);
@@ -1251,7 +1295,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 st.m32 = (float)(st.m64 * kLog2e);
                 st.l = L.init_l[srow];
             }
-            RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
+            RowStatC* rowstat = reinterpret_cast<RowStatC*>(smem + C::OFF_ROWSTAT);
             const int32_t dslot = DUMP && has_qb ? P.dump.slot[(size_t)x.h * L.kb2 + qb] : -1;
             for (uint32_t t = 0; t < x.n; ++t, ++T) {
                 const uint32_t s = T % NS, b = T & 1, ph = (T >> 1) & 1;
@@ -1271,12 +1315,13 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                                    side * C::META_BYTES);
                 uint8_t* prow = smem + C::OFF_P + (b * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
                 const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
-                float2* red_w = red + ((T & 1) * 4 + quad) * 2 + side;
-                const float2* red_r = red + (T & 1) * 8 + side;
+                // M128: one extreme pair per quadrant, a side's two quadrants at red_r[0], red_r[2]
+                float2* red_w = C::M128 ? red + (T & 1) * 8 + quad * 2 : red + ((T & 1) * 4 + quad) * 2 + side;
+                const float2* red_r = red + (T & 1) * 8 + (C::M128 ? side * 4 : side);
                 const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
-                RowStat* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
-                const RowStat* rs_r = rowstat + (T & 1) * 128;
-                const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
+                RowStatC* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
+                const RowStatC* rs_r = rowstat + (T & 1) * 128;
+                const uint8_t* qtile = smem + C::OFF_Q + (I & 1) * C::QBUF + side * C::QB_OFF;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
                 softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
@@ -1313,10 +1358,13 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 PROF_ADD(6, 1);
             }
             PROF_ADD(7, 1);
+            PROF_T(ti0);
             __syncwarp();
             if (lane == 0)
                 ptx::mbar_arrive(qempty(I)); // this warp no longer reads the item's Q tiles
             ptx::mbar_wait(bar(BR::LEMPTY), (I & 1) ^ 1);
+            PROF_T(ti1);
+            PROF_ADD(17, ti1 - ti0);
             lsm[side * 64 + r] = st.l;
             __syncwarp();
             if (PARO_PFULL_ALL || lane == 0)
@@ -1462,7 +1510,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         float4* rowmeta = reinterpret_cast<float4*>(smem + C::OFF_ROWMETA);
         float* usm = reinterpret_cast<float*>(smem + C::OFF_U);
         float* lsm = reinterpret_cast<float*>(smem + C::OFF_L); // [2 item parity][2 half][2 side][64]
-        RowStat* rowstat = reinterpret_cast<RowStat*>(smem + C::OFF_ROWSTAT);
+        RowStatC* rowstat = reinterpret_cast<RowStatC*>(smem + C::OFF_ROWSTAT);
         const uint32_t tail = L.N & 63;
         constexpr int DH = D / 2; // O columns per warp
         uint32_t T = 0, I = 0;
@@ -1566,9 +1614,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 float2* red_w = red + ((T & 1) * 4 + quad) * 2 + side;
                 const float2* red_r = red + (T & 1) * 8 + side;
                 const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
-                RowStat* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
-                const RowStat* rs_r = rowstat + (T & 1) * 128;
-                const uint8_t* qtile = smem + C::OFF_Q + ((I & 1) * 2 + side) * C::QT_BYTES;
+                RowStatC* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
+                const RowStatC* rs_r = rowstat + (T & 1) * 128;
+                const uint8_t* qtile = smem + C::OFF_Q + (I & 1) * C::QBUF + side * C::QB_OFF;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
                 softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
@@ -1691,6 +1739,13 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         }
     }
 
+#ifdef PARO_K3_PROF
+    if (threadIdx.x == 0) { // CTA lifetime (globaltimer ns): sum, and the latest end
+        atomicAdd(&g_profq[6], (unsigned long long)(ptx::globaltimer() - cta_t0));
+        atomicMax(&g_profq[7], (unsigned long long)ptx::globaltimer());
+        atomicMin(&g_profq[5], (unsigned long long)cta_t0);
+    }
+#endif
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1)
@@ -1711,7 +1766,9 @@ __global__ void __launch_bounds__(128, 1)
     using C = K3Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t sq = sbase, sk = sbase + C::QT_BYTES;
+    // M128: [0 | Q | 0 | K] -- side A reads [Q; 0], side B (after an A-side MMA, as K3
+    // accumulates B onto A) reads [0; Q]; otherwise [Q | K]
+    const uint32_t sq = sbase + (C::M128 ? C::QT_BYTES : 0u), sk = sbase + (C::M128 ? 3 : 1) * C::QT_BYTES;
     const uint32_t bar_ld = sk + C::KV_BYTES, bar_mma = bar_ld + 8, tptr = bar_ld + 16;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t h = tiles[3 * blockIdx.x], qb = tiles[3 * blockIdx.x + 1], bj = tiles[3 * blockIdx.x + 2];
@@ -1723,6 +1780,13 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (warp == 0)
         ptx::tmem_alloc<128>(tptr);
+    if (C::M128) {
+        for (uint32_t i = threadIdx.x; i < C::QT_BYTES / 16; i += 128) {
+            *reinterpret_cast<uint4*>(smem + i * 16) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(smem + 2 * C::QT_BYTES + i * 16) = make_uint4(0, 0, 0, 0);
+        }
+        ptx::fence_proxy_async_smem();
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -1734,18 +1798,25 @@ __global__ void __launch_bounds__(128, 1)
         ptx::tma_load_2d(sk, &tm_k, 0, row0 + (int32_t)bj * 64, bar_ld);
         ptx::mbar_wait(bar_ld, 0);
         ptx::tc_fence_after();
-        issue_qk<D>(tmem + (side ? C::LANE16 : 0u), sq, sk);
+        if (C::M128) {
+            issue_qk128(tmem, sq, sk, true);
+            if (side)
+                issue_qk128(tmem, sq - C::QT_BYTES, sk, false);
+        } else {
+            issue_qk<D>(tmem + (side ? C::LANE16 : 0u), sq, sk);
+        }
         ptx::mma_commit(bar_mma);
     }
     ptx::mbar_wait(bar_mma, 0);
     ptx::tc_fence_after();
-    const uint32_t row = warp * 16 + (lane & 15);
+    const uint32_t row = C::M128 ? (warp & 1) * 32 + lane : warp * 16 + (lane & 15);
+    const uint32_t my_side = C::M128 ? (uint32_t)warp >> 1 : (uint32_t)lane >> 4;
     for (int g = 0; g < C::G; ++g)
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t raw[32];
             ptx::tmem_ld32(tmem + ((warp * 32) << 16) + g * 64 + h2 * 32, raw);
             ptx::tmem_ld_wait();
-            if ((uint32_t)(lane >> 4) == side) {
+            if (my_side == side) {
                 int32_t* dst = S + (((size_t)blockIdx.x * C::G + g) * 64 + row) * 64 + h2 * 32;
                 for (int j = 0; j < 32; ++j)
                     dst[j] = (int32_t)raw[j];
@@ -1781,6 +1852,15 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
+    // two CTAs per SM at d=64 need the largest shared-memory carveout (-1: driver default)
+#ifndef PARO_K3_CARVEOUT
+#define PARO_K3_CARVEOUT 100
+#endif
+    if (PARO_K3_CARVEOUT >= 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, PARO_K3_CARVEOUT);
+        if (e != cudaSuccess)
+            return e;
+    }
     kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv, tvp);
     return cudaGetLastError();
 }
@@ -1827,6 +1907,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
     }
 #endif
 #ifdef PARO_K3_PROF
+    static unsigned long long gridDim_last = 1;
     if (getenv("PARO_K3_PROF_PRINT")) {
         unsigned long long h[32];
         cudaDeviceSynchronize();
@@ -1846,13 +1927,15 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
             unsigned long long q[8];
             cudaMemcpyFromSymbol(q, g_profq, sizeof(q));
             const double ns = (double)(h[23] ? h[23] : 1);
-            fprintf(stderr, "[k3 prof] per quad lateness: start %.0f %.0f %.0f %.0f arrival %.0f %.0f %.0f %.0f\n", q[0] / ns,
-                    q[1] / ns, q[2] / ns, q[3] / ns, q[4] / ns, q[5] / ns, q[6] / ns, q[7] / ns);
+            fprintf(stderr, "[k3 prof] CTA lifetime: mean %.1f us, kernel span %.1f us (first start to last end)\n",
+                    q[6] / 1e3 / (double)gridDim_last, (q[7] - q[5]) / 1e3);
             memset(q, 0, sizeof(q));
+            q[5] = ~0ull;
             cudaMemcpyToSymbol(g_profq, q, sizeof(q));
         }
-        fprintf(stderr, "[k3 prof] d=64 reduce: to-barrier %.0f barrier %.0f after %.0f; arrival spread %.0f start spread %.0f per CTA step\n",
-                h[19] / n, h[20] / n, h[21] / n, (double)h[22] / (h[23] ? h[23] : 1), (double)h[24] / (h[23] ? h[23] : 1));
+        fprintf(stderr, "[k3 prof] d=64 softmax per warp-step: item-queue wait %.0f, item-end LEMPTY wait %.0f\n", h[24] / n, h[25] / n);
+        fprintf(stderr, "[k3 prof] d=64 reduce: to-barrier %.0f barrier %.0f after %.0f; arrival spread %.0f per CTA step\n",
+                h[19] / n, h[20] / n, h[21] / n, (double)h[22] / (h[23] ? h[23] : 1));
         memset(h, 0, sizeof(h));
         cudaMemcpyToSymbol(g_prof, h, sizeof(h));
     }
@@ -1867,6 +1950,9 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
         return launch_k3_dec(p, tq, tk, tv, num_sms, st);
     const uint32_t slots = (uint32_t)num_sms * (L.D == 64 ? K3Cfg<64>::MINB : K3Cfg<128>::MINB);
     const int grid = (int)(p.n_items < slots ? p.n_items : slots);
+#ifdef PARO_K3_PROF
+    gridDim_last = (unsigned long long)grid;
+#endif
     return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, grid, st) : launch_k3_t<128>(p, tq, tk, tv, tvp, grid, st);
 }
 
@@ -1875,7 +1961,7 @@ cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUte
     if (n_tiles == 0)
         return cudaSuccess;
     if (L.D == 64) {
-        const uint32_t smem = K3Cfg<64>::QT_BYTES + K3Cfg<64>::KV_BYTES + 64;
+        const uint32_t smem = (K3Cfg<64>::M128 ? 3 : 1) * K3Cfg<64>::QT_BYTES + K3Cfg<64>::KV_BYTES + 64;
         cudaFuncSetAttribute(k3_debug_qk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k3_debug_qk<64><<<n_tiles, 128, smem, st>>>(L, tq, tk, tiles, S);
     } else {

@@ -210,6 +210,14 @@ struct RowStat { // 40 bytes
     int valid, pad;
 };
 static_assert(sizeof(RowStat) == 40, "RowStat layout");
+// The same, compact (K3 proper): the exact fp64 extreme logits relative to the
+// running max, as the reference forms them (logit - m_new, attention.cpp:183),
+// and the fast-path extremes; pmin = INF marks a row without a tile this step.
+struct RowStatC { // 24 bytes
+    double dmin, dmax; // tmin - m, tmax - m
+    float pmin, pmax;
+};
+static_assert(sizeof(RowStatC) == 24, "RowStatC layout");
 
 constexpr double kLog2e = 1.4426950408889634;
 // Relative band of the fast-path quotient q = (p - lo) / pscale at d=64. The
