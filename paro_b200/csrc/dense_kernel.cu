@@ -98,22 +98,40 @@ struct K4Cfg {
 // instead of once per (q-block, tile) in every K4 CTA.
 template <int D>
 __global__ void __launch_bounds__(256) k4_vsplit(LayerDev L, const float* __restrict__ v, uint32_t head_begin) {
+    // HBM-bound: one permutation lookup per row (not per element), 16-byte streaming
+    // row loads, 16-byte stores of four packed key pairs
     __shared__ float tile[64][D + 1];
+    __shared__ uint32_t src[64];
     const uint32_t bj = blockIdx.x, h = head_begin + blockIdx.y, tid = threadIdx.x;
-    const PermDesc pd = L.perm[h];
-    for (uint32_t e = tid; e < 64 * D; e += 256) {
-        const uint32_t j = e / D, c = e % D, kj = bj * 64 + j;
-        tile[j][c] = kj < L.N ? v[((size_t)h * L.N + perm_src(pd, kj)) * D + c] : 0.f;
+    if (tid < 64) {
+        const uint32_t kj = bj * 64 + tid;
+        src[tid] = kj < L.N ? perm_src(L.perm[h], kj) : 0xffffffffu;
     }
     __syncthreads();
-    uint32_t* hi = reinterpret_cast<uint32_t*>(L.vsplit_hi) + ((size_t)h * L.kb2 + bj) * D * 32;
-    uint32_t* lo = reinterpret_cast<uint32_t*>(L.vsplit_lo) + ((size_t)h * L.kb2 + bj) * D * 32;
-    for (uint32_t e = tid; e < D * 32; e += 256) {
-        const uint32_t c = e / 32, jp = e % 32;
-        uint32_t wh, wl;
-        bf16_split2(tile[2 * jp][c], tile[2 * jp + 1][c], wh, wl);
-        hi[e] = wh;
-        lo[e] = wl;
+    constexpr uint32_t C4 = D / 4; // float4 per row
+#pragma unroll
+    for (uint32_t e = tid; e < 64 * C4; e += 256) {
+        const uint32_t j = e / C4, c4 = e % C4, sj = src[j];
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sj != 0xffffffffu)
+            x = __ldcs(reinterpret_cast<const float4*>(v + ((size_t)h * L.N + sj) * D) + c4);
+        tile[j][4 * c4] = x.x;
+        tile[j][4 * c4 + 1] = x.y;
+        tile[j][4 * c4 + 2] = x.z;
+        tile[j][4 * c4 + 3] = x.w;
+    }
+    __syncthreads();
+    uint4* hi = reinterpret_cast<uint4*>(L.vsplit_hi) + ((size_t)h * L.kb2 + bj) * D * 8;
+    uint4* lo = reinterpret_cast<uint4*>(L.vsplit_lo) + ((size_t)h * L.kb2 + bj) * D * 8;
+#pragma unroll
+    for (uint32_t e = tid; e < D * 8; e += 256) { // row c of V^T, key pairs 4q..4q+3
+        const uint32_t c = e / 8, q = e % 8;
+        uint32_t wh[4], wl[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            bf16_split2(tile[8 * q + 2 * k][c], tile[8 * q + 2 * k + 1][c], wh[k], wl[k]);
+        hi[e] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        lo[e] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
     }
 }
 
