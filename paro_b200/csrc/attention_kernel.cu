@@ -94,16 +94,22 @@ struct K3Cfg {
     static constexpr uint32_t TM_S = 0;          // two S buffers
     static constexpr uint32_t TM_O = 2 * S_COLS; // two O buffers
     static constexpr uint32_t TMEM_COLS = (2 * S_COLS + 2 * D) <= 256 ? 256 : 512;
-    // d=64 (M128, opt-in: measured c2 4.72 vs 4.37 ms, c3 2.62 vs 2.54): QK is one M = 128 MMA per side with a zero-padded Q operand --
+    // d=64 (M128, opt-in: measured c2 4.74 vs 4.28 ms, c3 2.71 vs 2.53): QK is one M = 128 MMA per side with a zero-padded Q operand --
     // [Q_A; 0] and [0; Q_B] accumulated into the same 64 TMEM columns -- so q-block A
     // lands in TMEM lanes 0-63 (quadrants 0-1) and B in lanes 64-127 (quadrants 2-3):
     // a tile's 64 rows span two softmax warps instead of four, and its P-group
     // hand-off is a 64-thread barrier of that pair. An item buffer holds Q_A, a zero
     // tile and Q_B contiguously (the 128-row operands overlap on the zero tile).
     static constexpr bool M128 = D == 64 && PARO_M128;
-    static constexpr uint32_t QBUF = (M128 ? 3 : 2) * QT_BYTES; // one item's Q tiles
-    static constexpr uint32_t QB_OFF = M128 ? 2 * QT_BYTES : QT_BYTES; // side B's tile in it
-    static constexpr uint32_t OFF_Q = 0; // [2 item buffers][A, (0), B] q-block tiles
+    // M128 layout of one item buffer, in 32-row (2 KB) slots: [A0 | 0 | A1 | 0 | B0 | 0 | B1]
+    // (X0 / X1 = rows 0-31 / 32-63). Side A's operand [A0; 0; A1; 0] starts at slot 0 and
+    // puts its rows in TMEM quadrants 0 and 2; side B's [0; B0; 0; B1] starts at slot 3,
+    // quadrants 1 and 3 -- each q-block's pair of warps on sub-partitions {0, 2} or {1, 3}.
+    static constexpr uint32_t HALF = QT_BYTES / 2;
+    static constexpr uint32_t QBUF = M128 ? 7 * HALF : 2 * QT_BYTES; // one item's Q tiles
+    static constexpr uint32_t QB_OFF = M128 ? 4 * HALF : QT_BYTES;   // side B's rows 0-31 in it
+    static constexpr uint32_t QOP_B = M128 ? 3 * HALF : QT_BYTES;    // side B's MMA operand
+    static constexpr uint32_t OFF_Q = 0; // [2 item buffers][A, B] q-block tiles
     static constexpr uint32_t OFF_STAGE = 2 * QBUF;
     // within a stage: K_A, K_B, V_A, V_B, meta_A, meta_B
     static constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES; // [2 buf][2 side]
@@ -176,9 +182,9 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem, uint32_t sq, uint32_t sk
         }
 }
 
-// M128 (d=64): one side's QK as an M = 128 MMA whose A operand is [Q_A; 0] (side A,
-// at the item buffer) or [0; Q_B] (side B, one tile further); the first MMA of the
-// step overwrites the buffer, the other accumulates its half onto the first's zeros
+// M128 (d=64): one side's QK as an M = 128 MMA whose A operand interleaves the
+// q-block's two 32-row halves with zero slots (K3Cfg::QBUF); the first MMA of the
+// step overwrites the buffer, the other accumulates its rows onto the first's zeros
 __device__ __forceinline__ void issue_qk128(uint32_t tmem, uint32_t sa, uint32_t sk, bool first) {
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk)
@@ -616,8 +622,12 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         if (G == 1 && lane == 0)
             prof_arrive[red_par][(threadIdx.x >> 5) & 3] = tb0;
 #endif
-        if (M128)
-            ptx::named_bar_sync(1 + side, 64); // the side's two softmax warps
+        if (M128) { // the side's two softmax warps
+            if (side)
+                ptx::named_bar_sync_c<2>(64);
+            else
+                ptx::named_bar_sync_c<1>(64);
+        }
         else
             ptx::named_bar_sync(1, SPLIT ? 256 : 128); // the compute (softmax) warps
         PROF_T(tb1);
@@ -847,7 +857,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const uint8_t* kt = ktile + dside * (int32_t)(64 * D);
             int32_t Sj, S1j = 0;
             if (G == 1)
-                Sj = dot_row64(qt, kt, r_o, j);
+                Sj = dot_row64(qt + (M128 ? (r_o >> 5) * K3Cfg<64>::HALF : 0u), kt, r_o, j); // M128: rows 32-63 one slot on
             else
                 dot_row128(qt, kt, r_o, j, Sj, S1j);
             { // re-run the two fast variants of this element; only a split pair needs fp64
@@ -960,7 +970,7 @@ template <int D, bool DUMP, bool PACKED>
 __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     k3_attention(const __grid_constant__ K3Params P, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                 const __grid_constant__ CUtensorMap tm_vp) {
+                 const __grid_constant__ CUtensorMap tm_vp, const __grid_constant__ CUtensorMap tm_q32) {
     using C = K3Cfg<D>;
     using BR = Bars<C::NS>;
     constexpr int G = C::G;
@@ -1013,10 +1023,11 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     }
     if (warp == 1)
         ptx::tmem_alloc<C::TMEM_COLS>(sbase + C::OFF_TMEMPTR);
-    if (C::M128) { // the zero tiles of both item buffers (read by the tensor core only)
-        for (uint32_t i = threadIdx.x; i < 2 * C::QT_BYTES / 16; i += C::THREADS) {
-            const uint32_t buf = i / (C::QT_BYTES / 16), off = (i % (C::QT_BYTES / 16)) * 16;
-            *reinterpret_cast<uint4*>(smem + C::OFF_Q + buf * C::QBUF + C::QT_BYTES + off) = make_uint4(0, 0, 0, 0);
+    if (C::M128) { // the zero slots (1, 3, 5) of both item buffers (read by the tensor core only)
+        constexpr uint32_t W = C::HALF / 16;
+        for (uint32_t i = threadIdx.x; i < 2 * 3 * W; i += C::THREADS) {
+            const uint32_t buf = i / (3 * W), slot = 1 + 2 * ((i / W) % 3), off = (i % W) * 16;
+            *reinterpret_cast<uint4*>(smem + C::OFF_Q + buf * C::QBUF + slot * C::HALF + off) = make_uint4(0, 0, 0, 0);
         }
         ptx::fence_proxy_async_smem();
     }
@@ -1125,9 +1136,19 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
             ptx::mbar_wait(qempty(I), ((I >> 1) & 1) ^ 1);
             if (lane == 0) {
                 ptx::mbar_arrive_expect_tx(qfull(I), (x.qb != 0xffffu ? 2 : 1) * C::QT_BYTES);
-                ptx::tma_load_2d(qbuf(I), &tm_q, 0, row0 + (int32_t)x.qa * 64, qfull(I));
-                if (x.qb != 0xffffu)
-                    ptx::tma_load_2d(qbuf(I) + C::QB_OFF, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
+                if (C::M128) { // 32-row halves into slots 0, 2 (A) and 4, 6 (B)
+                    ptx::tma_load_2d(qbuf(I), &tm_q32, 0, row0 + (int32_t)x.qa * 64, qfull(I));
+                    ptx::tma_load_2d(qbuf(I) + 2 * C::HALF, &tm_q32, 0, row0 + (int32_t)x.qa * 64 + 32, qfull(I));
+                    if (x.qb != 0xffffu) {
+                        ptx::tma_load_2d(qbuf(I) + 4 * C::HALF, &tm_q32, 0, row0 + (int32_t)x.qb * 64, qfull(I));
+                        ptx::tma_load_2d(qbuf(I) + 6 * C::HALF, &tm_q32, 0, row0 + (int32_t)x.qb * 64 + 32,
+                                         qfull(I));
+                    }
+                } else {
+                    ptx::tma_load_2d(qbuf(I), &tm_q, 0, row0 + (int32_t)x.qa * 64, qfull(I));
+                    if (x.qb != 0xffffu)
+                        ptx::tma_load_2d(qbuf(I) + C::QB_OFF, &tm_q, 0, row0 + (int32_t)x.qb * 64, qfull(I));
+                }
             }
             for (uint32_t t = 0; t < x.n; ++t) {
                 const uint32_t s = T % NS;
@@ -1224,7 +1245,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                         if (t < x.na)
                             issue_qk128(tmem + C::TM_S + b * C::S_COLS, qbuf(I), stage(s), true);
                         if (t < x.nb)
-                            issue_qk128(tmem + C::TM_S + b * C::S_COLS, qbuf(I) + C::QT_BYTES, stage(s) + C::KV_BYTES,
+                            issue_qk128(tmem + C::TM_S + b * C::S_COLS, qbuf(I) + C::QOP_B, stage(s) + C::KV_BYTES,
                                         t >= x.na);
                     } else {
                         if (t < x.na)
@@ -1254,9 +1275,9 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         if (warp < 6) {
         // ------------------------------------------------------------ softmax
         const uint32_t quad = warp & 3;
-        // M128: quadrants 0-1 hold q-block A's rows 0-31 / 32-63, quadrants 2-3 B's
-        const uint32_t side = C::M128 ? quad >> 1 : lane >> 4;
-        const uint32_t r = C::M128 ? (quad & 1) * 32 + lane : quad * 16 + (lane & 15); // row within its q-block
+        // M128: quadrants 0 / 2 hold q-block A's rows 0-31 / 32-63, quadrants 1 / 3 B's
+        const uint32_t side = C::M128 ? quad & 1 : lane >> 4;
+        const uint32_t r = C::M128 ? (quad >> 1) * 32 + lane : quad * 16 + (lane & 15); // row within its q-block
         const uint32_t lane_base = (quad * 32) << 16;
         float2* red = reinterpret_cast<float2*>(smem + C::OFF_RED);
         float4* rowmeta = reinterpret_cast<float4*>(smem + C::OFF_ROWMETA);
@@ -1316,7 +1337,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 uint8_t* prow = smem + C::OFF_P + (b * 2 + side) * C::P_BYTES + (r >> 3) * 512 + (r & 7) * 64;
                 const uint32_t s_addr = tmem + lane_base + C::TM_S + b * C::S_COLS;
                 // M128: one extreme pair per quadrant, a side's two quadrants at red_r[0], red_r[2]
-                float2* red_w = C::M128 ? red + (T & 1) * 8 + quad * 2 : red + ((T & 1) * 4 + quad) * 2 + side;
+                float2* red_w = C::M128 ? red + (T & 1) * 8 + side * 4 + (quad >> 1) * 2
+                                        : red + ((T & 1) * 4 + quad) * 2 + side;
                 const float2* red_r = red + (T & 1) * 8 + (C::M128 ? side * 4 : side);
                 const bool tail_tile = tail != 0 && live && bj == L.kb - 1;
                 RowStatC* rs_w = rowstat + ((T & 1) * 2 + side) * 64 + r;
@@ -1762,13 +1784,15 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
 template <int D>
 __global__ void __launch_bounds__(128, 1)
     k3_debug_qk(const __grid_constant__ LayerDev L, const __grid_constant__ CUtensorMap tm_q,
-                const __grid_constant__ CUtensorMap tm_k, const uint32_t* __restrict__ tiles, int32_t* S) {
+                const __grid_constant__ CUtensorMap tm_q32, const __grid_constant__ CUtensorMap tm_k,
+                const uint32_t* __restrict__ tiles, int32_t* S) {
     using C = K3Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = ptx::smem_u32(smem);
-    // M128: [0 | Q | 0 | K] -- side A reads [Q; 0], side B (after an A-side MMA, as K3
-    // accumulates B onto A) reads [0; Q]; otherwise [Q | K]
-    const uint32_t sq = sbase + (C::M128 ? C::QT_BYTES : 0u), sk = sbase + (C::M128 ? 3 : 1) * C::QT_BYTES;
+    // M128: 2 KB slots [0 | Q0 | 0 | Q1 | 0 | K] -- side A's operand [Q0; 0; Q1; 0] at slot 1,
+    // side B's [0; Q0; 0; Q1] at slot 0 (after an A-side MMA, as K3 accumulates B onto A);
+    // otherwise [Q | K]
+    const uint32_t sq = sbase + (C::M128 ? C::HALF : 0u), sk = sbase + (C::M128 ? 5 * C::HALF : C::QT_BYTES);
     const uint32_t bar_ld = sk + C::KV_BYTES, bar_mma = bar_ld + 8, tptr = bar_ld + 16;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t h = tiles[3 * blockIdx.x], qb = tiles[3 * blockIdx.x + 1], bj = tiles[3 * blockIdx.x + 2];
@@ -1780,10 +1804,10 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (warp == 0)
         ptx::tmem_alloc<128>(tptr);
-    if (C::M128) {
-        for (uint32_t i = threadIdx.x; i < C::QT_BYTES / 16; i += 128) {
-            *reinterpret_cast<uint4*>(smem + i * 16) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(smem + 2 * C::QT_BYTES + i * 16) = make_uint4(0, 0, 0, 0);
+    if (C::M128) { // zero slots 0, 2, 4
+        for (uint32_t i = threadIdx.x; i < 3 * C::HALF / 16; i += 128) {
+            const uint32_t slot = 2 * (i / (C::HALF / 16)), off = (i % (C::HALF / 16)) * 16;
+            *reinterpret_cast<uint4*>(smem + slot * C::HALF + off) = make_uint4(0, 0, 0, 0);
         }
         ptx::fence_proxy_async_smem();
     }
@@ -1794,14 +1818,19 @@ __global__ void __launch_bounds__(128, 1)
     if (threadIdx.x == 0) {
         const int32_t row0 = (int32_t)(h * L.kb2 * 64);
         ptx::mbar_arrive_expect_tx(bar_ld, C::QT_BYTES + C::KV_BYTES);
-        ptx::tma_load_2d(sq, &tm_q, 0, row0 + (int32_t)qb * 64, bar_ld);
+        if (C::M128) {
+            ptx::tma_load_2d(sq, &tm_q32, 0, row0 + (int32_t)qb * 64, bar_ld);
+            ptx::tma_load_2d(sq + 2 * C::HALF, &tm_q32, 0, row0 + (int32_t)qb * 64 + 32, bar_ld);
+        } else {
+            ptx::tma_load_2d(sq, &tm_q, 0, row0 + (int32_t)qb * 64, bar_ld);
+        }
         ptx::tma_load_2d(sk, &tm_k, 0, row0 + (int32_t)bj * 64, bar_ld);
         ptx::mbar_wait(bar_ld, 0);
         ptx::tc_fence_after();
         if (C::M128) {
             issue_qk128(tmem, sq, sk, true);
             if (side)
-                issue_qk128(tmem, sq - C::QT_BYTES, sk, false);
+                issue_qk128(tmem, sq - C::HALF, sk, false);
         } else {
             issue_qk<D>(tmem + (side ? C::LANE16 : 0u), sq, sk);
         }
@@ -1809,8 +1838,8 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::mbar_wait(bar_mma, 0);
     ptx::tc_fence_after();
-    const uint32_t row = C::M128 ? (warp & 1) * 32 + lane : warp * 16 + (lane & 15);
-    const uint32_t my_side = C::M128 ? (uint32_t)warp >> 1 : (uint32_t)lane >> 4;
+    const uint32_t row = C::M128 ? (warp >> 1) * 32 + lane : warp * 16 + (lane & 15);
+    const uint32_t my_side = C::M128 ? (uint32_t)warp & 1 : (uint32_t)lane >> 4;
     for (int g = 0; g < C::G; ++g)
         for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t raw[32];
@@ -1844,7 +1873,8 @@ static void init_watchdog() {
 
 template <int D>
 static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                               const CUtensorMap& tv, const CUtensorMap& tvp, int grid, cudaStream_t st) {
+                               const CUtensorMap& tv, const CUtensorMap& tvp, const CUtensorMap& tq32, int grid,
+                               cudaStream_t st) {
     init_watchdog();
     const uint32_t smem = K3Cfg<D>::SMEM_BYTES;
     auto kern = p.L.v_packed ? (p.dump.slot ? k3_attention<D, true, true> : k3_attention<D, false, true>)
@@ -1861,7 +1891,7 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
         if (e != cudaSuccess)
             return e;
     }
-    kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv, tvp);
+    kern<<<grid, K3Cfg<D>::THREADS, smem, st>>>(p, tq, tk, tv, tvp, tq32);
     return cudaGetLastError();
 }
 
@@ -1871,7 +1901,7 @@ cudaError_t launch_k3_dec(const K3Params& p, const CUtensorMap& tq, const CUtens
                           int num_sms, cudaStream_t st);
 
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      const CUtensorMap& tvp, const CUtensorMap& tq32, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
                       uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump) {
     if (head_count == 0)
         return cudaSuccess;
@@ -1953,21 +1983,23 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
 #ifdef PARO_K3_PROF
     gridDim_last = (unsigned long long)grid;
 #endif
-    return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, grid, st) : launch_k3_t<128>(p, tq, tk, tv, tvp, grid, st);
+    return L.D == 64 ? launch_k3_t<64>(p, tq, tk, tv, tvp, tq32, grid, st)
+                     : launch_k3_t<128>(p, tq, tk, tv, tvp, tq32, grid, st);
 }
 
-cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
+cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tq32, const CUtensorMap& tk,
+                            uint32_t n_tiles,
                             const uint32_t* tiles, int32_t* S, cudaStream_t st) {
     if (n_tiles == 0)
         return cudaSuccess;
     if (L.D == 64) {
-        const uint32_t smem = (K3Cfg<64>::M128 ? 3 : 1) * K3Cfg<64>::QT_BYTES + K3Cfg<64>::KV_BYTES + 64;
+        const uint32_t smem = (K3Cfg<64>::M128 ? 5 * K3Cfg<64>::HALF : K3Cfg<64>::QT_BYTES) + K3Cfg<64>::KV_BYTES + 64;
         cudaFuncSetAttribute(k3_debug_qk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k3_debug_qk<64><<<n_tiles, 128, smem, st>>>(L, tq, tk, tiles, S);
+        k3_debug_qk<64><<<n_tiles, 128, smem, st>>>(L, tq, tq32, tk, tiles, S);
     } else {
         const uint32_t smem = K3Cfg<128>::QT_BYTES + K3Cfg<128>::KV_BYTES + 64;
         cudaFuncSetAttribute(k3_debug_qk<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k3_debug_qk<128><<<n_tiles, 128, smem, st>>>(L, tq, tk, tiles, S);
+        k3_debug_qk<128><<<n_tiles, 128, smem, st>>>(L, tq, tq32, tk, tiles, S);
     }
     return cudaGetLastError();
 }

@@ -50,12 +50,12 @@ cudaError_t launch_perm_block_stats(const float* map, size_t ld, uint32_t n, con
                                     float eps, double* sums, float* maxs, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_k2_order(const LayerDev& L, cudaStream_t st);
 cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      const CUtensorMap& tvp, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
+                      const CUtensorMap& tvp, const CUtensorMap& tq32, double scale, int pv_bits, float* out, uint8_t* zeroed, int num_sms, cudaStream_t st,
                       uint32_t head_begin, uint32_t head_count, bool chunked, const K3Dump* dump = nullptr);
 cudaError_t launch_k1_quant_proof(uint32_t lo, uint32_t count, uint32_t nx, uint32_t seed, unsigned long long* bad,
                                   uint32_t* first, int num_sms, cudaStream_t st);
-cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tk, uint32_t n_tiles,
-                            const uint32_t* tiles, int32_t* S, cudaStream_t st);
+cudaError_t launch_debug_qk(const LayerDev& L, const CUtensorMap& tq, const CUtensorMap& tq32, const CUtensorMap& tk,
+                            uint32_t n_tiles, const uint32_t* tiles, int32_t* S, cudaStream_t st);
 } // namespace paro
 
 using paro::LayerDev;
@@ -299,6 +299,7 @@ struct paro_layer {
     int last_v_bits = 0;
     int last_launches = 0;
     CUtensorMap tm_q, tm_k, tm_v, tm_vp; // tm_vp: nibble-packed INT4 V (D/2 bytes per row)
+    CUtensorMap tm_q32;                  // Q codes in 32-row boxes (K3's M = 128 layout, PARO_M128)
     CUtensorMap tm_vh, tm_vl;            // dense prefix: K4a's bf16 V^T hi / lo tiles (K4 on tcgen05)
     // e2e staging
     float* rope = nullptr; // [2][N - dp][D]: cos, sin (paro_layer_set_rope)
@@ -564,7 +565,7 @@ void run_attention(paro_layer* l, cudaStream_t st, float scale, int pv_bits, flo
                                    &l->tm_vl),
                    "k4 launch");
     }
-    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, l->tm_vp, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
+    cuda_check(paro::launch_k3(l->L, l->tm_q, l->tm_k, l->tm_v, l->tm_vp, l->tm_q32, eff, pv_bits, out, zeroed, l->ctx->num_sms, st,
                                head_begin, head_count, chunked, dump),
                "k3_attention launch");
 }
@@ -1434,6 +1435,7 @@ int paro_layer_create_prefix(paro_ctx* ctx, uint32_t heads, uint32_t head_dim, c
                        "cudaMemcpy perm");
             cuda_check(paro::launch_perm_tables(L.perm, heads, L.N, l->fwd, l->inv, 0), "perm tables");
             encode_codes_map(ctx, &l->tm_q, L.q, head_dim, rows, 64);
+            encode_codes_map(ctx, &l->tm_q32, L.q, head_dim, rows, 32);
             encode_codes_map(ctx, &l->tm_k, L.k, head_dim, rows, 64);
             encode_codes_map(ctx, &l->tm_v, L.v, head_dim, rows, 64);
             encode_packed_map(ctx, &l->tm_vp, L.v, head_dim, rows, 64);
@@ -1912,7 +1914,8 @@ int paro_layer_debug_qk(paro_layer* layer, paro_stream_t stream, uint32_t n_tile
     return guarded([&] {
         check_layer(layer);
         set_device(layer->ctx);
-        cuda_check(paro::launch_debug_qk(layer->L, layer->tm_q, layer->tm_k, n_tiles, tiles, S, (cudaStream_t)stream),
+        cuda_check(paro::launch_debug_qk(layer->L, layer->tm_q, layer->tm_q32, layer->tm_k, n_tiles, tiles, S,
+                                         (cudaStream_t)stream),
                    "debug_qk launch");
     });
 }
