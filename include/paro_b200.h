@@ -263,7 +263,9 @@ int paro_layer_set_masks_pmsk(paro_layer* layer, paro_stream_t stream, const uin
 int paro_layer_set_rope(paro_layer* layer, paro_stream_t stream, const float* cos, const float* sin);
 
 /* K1: permuted gather + per-block quantization into layer-owned buffers (with a
- * dense prefix also K4a: the bf16 hi/lo V^T tiles of the dense path). Q/K/V are
+ * dense prefix also K4a: the bf16 hi/lo V^T tiles of the dense path). Device
+ * buffers (Q/K/V here, out in attention / forward) must be 16-byte aligned
+ * (PARO_E_CONFIG otherwise): rows are read and written as 16-byte vectors. Q/K/V are
  * read only by the kernels queued here: once they have run on `stream` the caller
  * may free or reuse them -- attention works from the layer-owned buffers alone. */
 int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const float* q, const float* k,

@@ -540,6 +540,12 @@ void check_bits(int bits) {
         fail(PARO_E_CONFIG, "quantization bitwidth must be 4 or 8, got " + std::to_string(bits)); // quant.cpp:15-17
 }
 
+// K1 / K4a read Q/K/V rows and K3 writes O rows with 16-byte vector accesses
+void check_aligned16(const void* p, const char* what) {
+    if (reinterpret_cast<uintptr_t>(p) & 15u)
+        fail(PARO_E_CONFIG, std::string(what) + " must be 16-byte aligned (vectorised row access)");
+}
+
 void check_layer(const paro_layer* l) {
     if (!l)
         fail(PARO_E_CONFIG, "null layer");
@@ -1658,6 +1664,9 @@ int paro_layer_reorder_quantize(paro_layer* layer, paro_stream_t stream, const f
         check_bits(v_bits);
         if (!q || !k || !v)
             fail(PARO_E_CONFIG, "null Q/K/V");
+        check_aligned16(q, "Q");
+        check_aligned16(k, "K");
+        check_aligned16(v, "V");
         set_device(layer->ctx);
         layer->L.v_packed = v_bits == 4 && layer->v_pack;
         cuda_check(paro::launch_k1(layer->L, q, k, v, v_bits, 0, layer->L.H, (cudaStream_t)stream), "k1 launch");
@@ -1670,6 +1679,7 @@ int paro_layer_attention(paro_layer* layer, paro_stream_t stream, float scale, i
                          uint8_t* zeroed) {
     return guarded([&] {
         check_layer(layer);
+        check_aligned16(out, "out");
         set_device(layer->ctx);
         run_attention(layer, (cudaStream_t)stream, scale, pv_bits, out, zeroed);
     });
@@ -1682,6 +1692,12 @@ int paro_layer_forward(paro_layer* layer, paro_stream_t stream, const float* q, 
         check_bits(pv_bits);
         if (!layer->masks_set)
             fail(PARO_E_CONFIG, "paro_layer_set_masks must be called before forward");
+        if (!q || !k || !v)
+            fail(PARO_E_CONFIG, "null Q/K/V");
+        check_aligned16(q, "Q");
+        check_aligned16(k, "K");
+        check_aligned16(v, "V");
+        check_aligned16(out, "out");
         set_device(layer->ctx);
         cudaStream_t st = (cudaStream_t)stream;
         layer->L.v_packed = pv_bits == 4 && layer->v_pack;

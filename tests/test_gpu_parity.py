@@ -258,6 +258,27 @@ def test_gpu_errors(paro, ctx):
         ctx.quantized_blocked_attention(paro.AttnInputs(q[0], q[0], q[0]), None, paro.QuantConfig(16))
 
 
+def test_misaligned_device_buffers_rejected(paro, ctx):
+    # K1 / K4a read rows and K3 writes rows with 16-byte vector accesses: a device
+    # pointer that is not 16-byte aligned is a ConfigError, not a fault
+    H, d, grid = 1, 64, "H:8,W:8"
+    q = randn(3, (H, 64, d))
+    layer = paro.Layer(ctx, H, d, grid)
+    layer.set_masks(None)
+    buf = paro.DeviceBuffer(q.nbytes + 64)
+    out = paro.DeviceBuffer(q.nbytes + 64)
+    for off in (4, 8):
+        with pytest.raises(paro.ConfigError):
+            layer.reorder_quantize(buf.ptr + off, buf.ptr, buf.ptr, 8)
+        with pytest.raises(paro.ConfigError):
+            layer.forward(buf.ptr, buf.ptr, buf.ptr + off, 0.0, 8, out.ptr, None)
+        with pytest.raises(paro.ConfigError):
+            layer.forward(buf.ptr, buf.ptr, buf.ptr, 0.0, 8, out.ptr + off, None)
+    layer.forward(buf.ptr + 16, buf.ptr + 16, buf.ptr + 16, 0.0, 8, out.ptr + 16, None)  # 16-byte offsets are fine
+    paro.stream_sync()
+    layer.close()
+
+
 # dense-prefix tiles are unquantized: K4 runs P.V on the tensor cores as a
 # 3-term bf16 split (16 significant bits per operand, fp32 accumulation);
 # observed <= 7e-6, bound set 10x under the north_star 1e-3.
