@@ -1345,6 +1345,8 @@ int paro_quantize_sym_device(paro_ctx* ctx, paro_stream_t stream, const float* i
         check_bits(bits);
         if (cols != 64 && cols != 128)
             fail(PARO_E_CONFIG, "device quantize supports 64 or 128 columns, got " + std::to_string(cols));
+        check_aligned16(in, "input");
+        check_aligned16(codes, "codes"); // 4-byte code stores: 16 is the documented contract
         set_device(ctx);
         if (rows == 0)
             return;
