@@ -63,6 +63,12 @@ namespace paro {
 #ifndef PARO_M128
 #define PARO_M128 0
 #endif
+// exact path: the tile's exact P extremes from one fp64 exp each (monotone in the
+// reduced argument) instead of exp over the candidate rows. 1: at d=128 only
+// (measured c5 123.9 -> 120.4 ms; at d=64 the code change costs c2 3%), 2: both
+#ifndef PARO_EXACT_MONO
+#define PARO_EXACT_MONO 1
+#endif
 #ifndef PARO_K3_UNROLL
 #define PARO_K3_UNROLL 4
 #endif
@@ -764,37 +770,59 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 hi_a = fmaxf(hi_a, rd[2 * q].y);
             }
             float mn = INFINITY, mx = 0.f;
-            double args[4];
-            uint32_t kinds = 0, cnt = 0; // bit i: arg i is a max candidate
+            if (PARO_EXACT_MONO == 2 || (PARO_EXACT_MONO == 1 && G == 2)) {
+                // exp and the fp32 rounding are monotone, so the tile's exact extremes are
+                // float(exp()) of the smallest / largest (logit - m) over its valid rows:
+                // reduce the fp64 arguments over the 64 rows, then one exp each
+                double dmn = INFINITY, dmx = -INFINITY;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const RowStatC q = rs_r[sd * 64 + lane + 32 * k];
-                if (q.pmin == INFINITY) // no tile in this row this step
-                    continue;
-                if (q.pmin <= lo_a * 1.00001f)
-                    args[cnt++] = q.dmin;
-                if (q.pmax >= hi_a * 0.99999f) {
-                    if (q.dmax == 0.0)
-                        mx = 1.0f; // exp(0)
-                    else {
-                        kinds |= 1u << cnt;
-                        args[cnt++] = q.dmax;
+                for (int k = 0; k < 2; ++k) {
+                    const RowStatC q = rs_r[sd * 64 + lane + 32 * k];
+                    if (q.pmin == INFINITY) // no tile in this row this step
+                        continue;
+                    dmn = fmin(dmn, q.dmin);
+                    dmx = fmax(dmx, q.dmax);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+                    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+                }
+                mn = dmn == INFINITY ? INFINITY : (float)exp(dmn);
+                mx = dmx == -INFINITY ? 0.f : (dmx == 0.0 ? 1.0f : (float)exp(dmx));
+            } else {
+                double args[4];
+                uint32_t kinds = 0, cnt = 0; // bit i: arg i is a max candidate
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const RowStatC q = rs_r[sd * 64 + lane + 32 * k];
+                    if (q.pmin == INFINITY) // no tile in this row this step
+                        continue;
+                    if (q.pmin <= lo_a * 1.00001f)
+                        args[cnt++] = q.dmin;
+                    if (q.pmax >= hi_a * 0.99999f) {
+                        if (q.dmax == 0.0)
+                            mx = 1.0f; // exp(0)
+                        else {
+                            kinds |= 1u << cnt;
+                            args[cnt++] = q.dmax;
+                        }
                     }
                 }
-            }
-            for (uint32_t it = 0; __any_sync(0xffffffffu, it < cnt); ++it) {
-                if (it < cnt) {
-                    const float e = (float)exp(args[it]);
-                    if ((kinds >> it) & 1u)
-                        mx = fmaxf(mx, e);
-                    else
-                        mn = fminf(mn, e);
+                for (uint32_t it = 0; __any_sync(0xffffffffu, it < cnt); ++it) {
+                    if (it < cnt) {
+                        const float e = (float)exp(args[it]);
+                        if ((kinds >> it) & 1u)
+                            mx = fmaxf(mx, e);
+                        else
+                            mn = fminf(mn, e);
+                    }
                 }
-            }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
             }
             lo_e[sd] = mn;
             hi_e[sd] = mx;
