@@ -403,9 +403,13 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 const uint32_t ja = h2 * 32 + 2 * k, jb = ja + 1;
-                const float ya = fmaf(__int2float_rn((int32_t)x1[2 * k]), c1, __int2float_rn((int32_t)x0[2 * k]) * c0);
-                const float yb =
-                    fmaf(__int2float_rn((int32_t)x1[2 * k + 1]), c1, __int2float_rn((int32_t)x0[2 * k + 1]) * c0);
+                // y = fma(S_1, c1, S_0 * c0) per column, two columns per packed FMUL2 / FFMA2
+                const uint64_t y2 = fma2(pk(__int2float_rn((int32_t)x1[2 * k]), __int2float_rn((int32_t)x1[2 * k + 1])),
+                                         pk(c1, c1),
+                                         mul2(pk(__int2float_rn((int32_t)x0[2 * k]), __int2float_rn((int32_t)x0[2 * k + 1])),
+                                              pk(c0, c0)));
+                float ya, yb;
+                upk(y2, ya, yb);
                 const float ka = tagf(ya, ja), kb = tagf(yb, jb);
                 const float hi = fmaxf(ka, kb), lo = fminf(ka, kb);
                 const int c = k & 3;
