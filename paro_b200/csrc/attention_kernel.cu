@@ -66,6 +66,11 @@ namespace paro {
 // exact path: the tile's exact P extremes from one fp64 exp each (monotone in the
 // reduced argument) instead of exp over the candidate rows. 1: at d=128 only
 // (measured c5 123.9 -> 120.4 ms; at d=64 the code change costs c2 3%), 2: both
+// d=128 pass 1: re-test an unsure argmax / argmin gap with the row's own largest
+// |S_g| before the fp64 rescan
+#ifndef PARO_TIGHT_SLACK
+#define PARO_TIGHT_SLACK 1
+#endif
 #ifndef PARO_EXACT_MONO
 #define PARO_EXACT_MONO 1
 #endif
@@ -474,8 +479,29 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         asm volatile("" ::"d"(tmax64 + tmin64));
 #endif
         PROF_T(tq2);
-        if (__any_sync(0xffffffffu, unsure && valid)) {
-            const float thr_hi = mA - slack, thr_lo = nA + slack;
+        bool unsure_t = unsure;
+        float slack_t = slack;
+        if (PARO_TIGHT_SLACK && __any_sync(0xffffffffu, unsure && valid)) {
+            // the bound above assumes |S_g| = 64 * 127^2; the row's own largest |S_g|
+            // (both key halves) usually settles the gap test without the fp64 rescan
+            int32_t M0 = 0, M1 = 0;
+#pragma unroll 1
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t x0[32], x1[32];
+                ptx::tmem_ld32(s_addr + h2 * 32, x0);
+                ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    M0 = max(M0, abs((int32_t)x0[j]));
+                    M1 = max(M1, abs((int32_t)x1[j]));
+                }
+            }
+            slack_t = kErrS * (c0 * (float)M0 + c1 * (float)M1) + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
+            unsure_t = unsure && (!(mA - mB > slack_t) || !(nB - nA > slack_t));
+        }
+        if (__any_sync(0xffffffffu, unsure_t && valid)) {
+            const float thr_hi = mA - slack_t, thr_lo = nA + slack_t;
 #pragma unroll 1
             for (int h2 = 0; h2 < 2; ++h2) {
                 uint32_t x0[32], x1[32];
@@ -486,7 +512,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 for (int j = 0; j < 32; ++j) {
                     const float y =
                         fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
-                    if (unsure && (uint32_t)(h2 * 32 + j) < ncol && (y >= thr_hi || y <= thr_lo)) {
+                    if (unsure_t && (uint32_t)(h2 * 32 + j) < ncol && (y >= thr_hi || y <= thr_lo)) {
                         const int32_t a = (int32_t)x0[j], b = (int32_t)x1[j];
                         const double L = logit128(scale64, a64, a64b, a, b);
                         if (L > tmax64) {
