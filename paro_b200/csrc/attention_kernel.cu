@@ -499,6 +499,15 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             }
             slack_t = kErrS * (c0 * (float)M0 + c1 * (float)M1) + kGapSlack * fmaxf(fabsf(mA), fabsf(nA));
             unsure_t = unsure && (!(mA - mB > slack_t) || !(nB - nA > slack_t));
+#ifdef PARO_K3_PROF
+            if (lane == 0) {
+                atomicAdd(&g_profq[0], 1ull);
+                if (__any_sync(0xffffffffu, unsure_t && valid))
+                    atomicAdd(&g_profq[1], 1ull);
+            } else {
+                (void)__any_sync(0xffffffffu, unsure_t && valid);
+            }
+#endif
         }
         if (__any_sync(0xffffffffu, unsure_t && valid)) {
             const float thr_hi = mA - slack_t, thr_lo = nA + slack_t;
@@ -508,23 +517,31 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 ptx::tmem_ld32(s_addr + h2 * 32, x0);
                 ptx::tmem_ld32(s_addr + 64 + h2 * 32, x1);
                 ptx::tmem_ld_wait();
+                // the half's candidate columns as a bitmask (branch-free), then each lane
+                // walks its own few candidates in ascending order (the same order and
+                // tie-breaking as a column loop, without 32 warp-divergent fp64 branches)
+                uint32_t cm = 0;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const float y =
                         fmaf(__int2float_rn((int32_t)x1[j]), c1, __int2float_rn((int32_t)x0[j]) * c0);
-                    if (unsure_t && (uint32_t)(h2 * 32 + j) < ncol && (y >= thr_hi || y <= thr_lo)) {
-                        const int32_t a = (int32_t)x0[j], b = (int32_t)x1[j];
-                        const double L = logit128(scale64, a64, a64b, a, b);
-                        if (L > tmax64) {
-                            tmax64 = L;
-                            s0x = a;
-                            s1x = b;
-                        }
-                        if (L < tmin64) {
-                            tmin64 = L;
-                            s0n = a;
-                            s1n = b;
-                        }
+                    const bool cand = unsure_t && (uint32_t)(h2 * 32 + j) < ncol && (y >= thr_hi || y <= thr_lo);
+                    cm |= (cand ? 1u : 0u) << j;
+                }
+                while (cm) {
+                    const uint32_t j = __ffs(cm) - 1;
+                    cm &= cm - 1;
+                    const int32_t a = (int32_t)sel32(x0, j), b = (int32_t)sel32(x1, j);
+                    const double L = logit128(scale64, a64, a64b, a, b);
+                    if (L > tmax64) {
+                        tmax64 = L;
+                        s0x = a;
+                        s1x = b;
+                    }
+                    if (L < tmin64) {
+                        tmin64 = L;
+                        s0n = a;
+                        s1n = b;
                     }
                 }
             }
@@ -2015,6 +2032,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
             unsigned long long q[8];
             cudaMemcpyFromSymbol(q, g_profq, sizeof(q));
             const double ns = (double)(h[23] ? h[23] : 1);
+            fprintf(stderr, "[k3 prof] d=128 unsure warp-steps: loose %llu, after the tight re-test %llu\n", q[0], q[1]);
             fprintf(stderr, "[k3 prof] CTA lifetime: mean %.1f us, kernel span %.1f us (first start to last end)\n",
                     q[6] / 1e3 / (double)gridDim_last, (q[7] - q[5]) / 1e3);
             memset(q, 0, sizeof(q));
