@@ -341,6 +341,10 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     // other 32 rows sit in the partner warp of the same side
     constexpr bool M128 = !SPLIT && K3Cfg<D>::M128;
     const uint32_t lane = threadIdx.x & 31;
+    // M128: this warp's side as a vote result, so the compiler sees it warp-uniform (a
+    // branch on a threadIdx-derived value makes it wrap every later shuffle in
+    // divergence handling: +13% code and instruction-fetch stalls)
+    const uint32_t wside = M128 ? (__ballot_sync(0xffffffffu, side != 0) ? 1u : 0u) : side;
     const bool valid = live && valid_row;
     // -------- pass 1: row extremes (4 independent chains)
     float m32, pmax_r, pmin_r, c0, c1 = 0.f, dmax = 0.f;
@@ -676,7 +680,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             prof_arrive[red_par][(threadIdx.x >> 5) & 3] = tb0;
 #endif
         if (M128) { // the side's two softmax warps
-            if (side)
+            if (wside)
                 ptx::named_bar_sync_c<2>(64);
             else
                 ptx::named_bar_sync_c<1>(64);
@@ -807,7 +811,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         float lo_e[2] = {INFINITY, INFINITY}, hi_e[2] = {0.f, 0.f};
 #pragma unroll
         for (int sd = 0; sd < 2; ++sd) {
-            if (M128 ? sd != (int)side : !((sd ? rmask >> 16 : rmask & 0xffffu)))
+            if (M128 ? sd != (int)wside : !((sd ? rmask >> 16 : rmask & 0xffffu)))
                 continue;
             const float2* rd = M128 ? red_r : red_r - (int)side + sd; // the side's quadrant extremes
             float lo_a = rd[0].x, hi_a = rd[0].y;
@@ -926,7 +930,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const uint32_t ncol_o = __shfl_sync(0xffffffffu, ncol, (int)o);
             if (!act || j >= ncol_o)
                 continue;
-            const uint32_t so = M128 ? side : o >> 4;
+            const uint32_t so = M128 ? wside : o >> 4;
             const int32_t dside = (int32_t)so - (int32_t)side;
             const uint8_t* qt = qtile + dside * (int32_t)(64 * D);
             const uint8_t* kt = ktile + dside * (int32_t)(64 * D);
