@@ -71,6 +71,11 @@ namespace paro {
 #ifndef PARO_TIGHT_SLACK
 #define PARO_TIGHT_SLACK 1
 #endif
+// the P-group extremes within a warp by redux.sync on the fp32 bit patterns. 1: at
+// d=128 only (c5 111.8 -> 110.5 ms; at d=64 it costs c2 2%), 2: both
+#ifndef PARO_REDUX
+#define PARO_REDUX 1
+#endif
 #ifndef PARO_EXACT_MONO
 #define PARO_EXACT_MONO 1
 #endif
@@ -582,10 +587,28 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     }
     // -------- P group extremes over the q-block's 64 rows: 16 lanes x 4 warps
     // (M128: 32 lanes x 2 warps)
+    if (PARO_REDUX == 2 || (PARO_REDUX == 1 && G == 2)) {
+        // p >= 0 (INF marks an idle row), so the fp32 bit patterns order like the values:
+        // one redux.sync per side and extreme instead of a 4-level shuffle chain
+        const uint32_t bmin = __float_as_uint(pmin_r), bmax = __float_as_uint(pmax_r);
+        if (M128) {
+            pmin_r = __uint_as_float(__reduce_min_sync(0xffffffffu, bmin));
+            pmax_r = __uint_as_float(__reduce_max_sync(0xffffffffu, bmax));
+        } else {
+            const bool sb = lane >= 16;
+            const uint32_t mnA = __reduce_min_sync(0xffffffffu, sb ? 0xffffffffu : bmin);
+            const uint32_t mnB = __reduce_min_sync(0xffffffffu, sb ? bmin : 0xffffffffu);
+            const uint32_t mxA = __reduce_max_sync(0xffffffffu, sb ? 0u : bmax);
+            const uint32_t mxB = __reduce_max_sync(0xffffffffu, sb ? bmax : 0u);
+            pmin_r = __uint_as_float(sb ? mnB : mnA);
+            pmax_r = __uint_as_float(sb ? mxB : mxA);
+        }
+    } else {
 #pragma unroll
-    for (int o = M128 ? 16 : 8; o > 0; o >>= 1) {
-        pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
-        pmax_r = fmaxf(pmax_r, __shfl_xor_sync(0xffffffffu, pmax_r, o));
+        for (int o = M128 ? 16 : 8; o > 0; o >>= 1) {
+            pmin_r = fminf(pmin_r, __shfl_xor_sync(0xffffffffu, pmin_r, o));
+            pmax_r = fmaxf(pmax_r, __shfl_xor_sync(0xffffffffu, pmax_r, o));
+        }
     }
     if ((!SPLIT || half == 0) && (M128 ? lane == 0 : (lane & 15) == 0))
         *red_w = make_float2(pmin_r, pmax_r);
