@@ -68,6 +68,9 @@ namespace paro {
 // (measured c5 123.9 -> 120.4 ms; at d=64 the code change costs c2 3%), 2: both
 // d=128 pass 1: re-test an unsure argmax / argmin gap with the row's own largest
 // |S_g| before the fp64 rescan
+#ifndef PARO_DQ_BATCH
+#define PARO_DQ_BATCH 0  // 1: d=128 dequant issues every O chunk load before one wait (measured neutral)
+#endif
 #ifndef PARO_TIGHT_SLACK
 #define PARO_TIGHT_SLACK 1
 #endif
@@ -1694,11 +1697,23 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const float4 rm = rowmeta[(b * 2 + side) * 64 + r];
                 const uint64_t g2 = pk(rm.x, rm.x), ss2 = pk(rm.y, rm.y);
                 const float4* u4 = reinterpret_cast<const float4*>(usm + (b * 2 + side) * D + half * DH);
+#if PARO_DQ_BATCH
+                // every chunk's TMEM load issued before the single wait: one round trip
+                uint32_t rawv[DH / 16][16];
+#pragma unroll
+                for (int ch = 0; ch < DH / 16; ++ch)
+                    tmem_ld16(tmem + lane_base + C::TM_O + b * D + half * DH + ch * 16, rawv[ch]);
+                ptx::tmem_ld_wait();
+#endif
 #pragma unroll
                 for (int ch = 0; ch < DH / 16; ++ch) {
+#if PARO_DQ_BATCH
+                    const uint32_t (&raw)[16] = rawv[ch];
+#else
                     uint32_t raw[16];
                     tmem_ld16(tmem + lane_base + C::TM_O + b * D + half * DH + ch * 16, raw);
                     ptx::tmem_ld_wait();
+#endif
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const float4 uu = u4[ch * 4 + q4];

@@ -151,6 +151,26 @@ def test_schedule_at_matches_golden(paro, kat):
         paro.schedule_at(b"PSCHxxxx", 0)
 
 
+def test_schedule_at_is_positional(paro):
+    """MaskSchedule::at(t) returns distinct[t] by position and ignores the stored
+    timestep field (mask.cpp:132-140, load_schedule mask.cpp:282-292): an image
+    whose stored fields are permuted / duplicated selects the same masks."""
+    import struct
+
+    rng = np.random.default_rng(11)
+    T = 7
+    masks = [(rng.random((5, 5)) < 0.5).astype(np.uint8) for _ in range(T // 2 + 1)]
+    blobs = [paro.serialize_mask(paro.BlockMask(5, 5, 64, m)) for m in masks]
+    stored = [2, 2, 0]  # non-canonical: duplicated and out of order
+    img = b"PSCH" + struct.pack("<II", T, T // 2)
+    for s, b in zip(stored, blobs[:-1]):
+        img += struct.pack("<I", s) + b
+    img += blobs[-1]
+    for t in range(T):
+        want = masks[t] if t < T // 2 else masks[-1]
+        assert np.array_equal(paro.schedule_at(img, t).bits, want), t
+
+
 # ------------------------------------------------------------------ synthetic inputs
 def test_synth_randn_matches_reference_generator(paro, reference):
     """gen_attention_inputs' V is the documented MT19937-64 Box-Muller stream
