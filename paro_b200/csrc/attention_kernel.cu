@@ -82,6 +82,9 @@ namespace paro {
 #ifndef PARO_EXACT_MONO
 #define PARO_EXACT_MONO 1
 #endif
+#ifndef PARO_K3_W12
+#define PARO_K3_W12 0
+#endif
 #ifndef PARO_K3_UNROLL
 #define PARO_K3_UNROLL 4
 #endif
@@ -99,7 +102,13 @@ struct K3Cfg {
     // split's two warps per quadrant contend for one SMSP in the synchronised
     // pass 2; measured 5.71 vs 4.86 ms at c2, while d=128 gains 188 -> 165 ms).
     static constexpr bool SPLIT = D == 128;
-    static constexpr int THREADS = SPLIT ? 384 : 320;
+    // d=64 W12 (opt-in PARO_K3_W12): the same roles on 12 warps -- warpgroup 0 = producer,
+    // MMA, 2 idle (setmaxnreg down), softmax on warps 4-7, epilogue on 8-11, so the
+    // softmax and epilogue warpgroups get REG_COMPUTE registers instead of the 96 of
+    // the 10-warp launch
+    static constexpr bool W12 = D == 64 && PARO_K3_W12 && !PARO_M128;
+    static constexpr int THREADS = (SPLIT || W12) ? 384 : 320;
+    static constexpr uint32_t SM0 = W12 ? 4 : 2; // first softmax warp (d=64)
     static constexpr uint32_t NCW = SPLIT ? 8 : 4; // warps arriving on the S / P / O barriers
     static constexpr uint32_t REG_LAUNCH = (65536 / (THREADS * MINB)) / 8 * 8;
     static constexpr uint32_t REG_LOW = 32;
@@ -1178,7 +1187,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         // each stage's nibble-packed V tiles into the i8 swizzled layout the P.V MMA
         // reads (Blackwell has no INT4 MMA), one step behind the loads, and releases
         // them with VFULL -- QK waits only for K.
-        if (C::SPLIT)
+        if (C::SPLIT || C::W12)
             ptx::setmaxnreg_dec<C::REG_LOW>();
         constexpr bool packed = PACKED;
         if (lane == 0) {
@@ -1294,7 +1303,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
         unpack_pending();
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (C::SPLIT)
+        if (C::SPLIT || C::W12)
             ptx::setmaxnreg_dec<C::REG_LOW>();
         if (lane == 0) {
             uint32_t T = 0, I = 0;
@@ -1376,8 +1385,10 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 atomicAdd(&g_prof[12 + i], prof[i]);
 #endif
         }
-    } else if (!C::SPLIT) {
-        if (warp < 6) {
+    } else if (!C::SPLIT && (!C::W12 || warp >= 4)) {
+        if (C::W12)
+            ptx::setmaxnreg_inc<C::REG_COMPUTE>();
+        if (warp < C::SM0 + 4) {
         // ------------------------------------------------------------ softmax
         const uint32_t quad = warp & 3;
         // M128: quadrants 0 / 2 hold q-block A's rows 0-31 / 32-63, quadrants 1 / 3 B's
@@ -1621,6 +1632,8 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 atomicAdd(&g_prof[8 + i], prof[i]);
 #endif
         }
+    } else if (C::W12) {
+        ptx::setmaxnreg_dec<C::REG_LOW>(); // warps 2-3 of the d=64 W12 layout: idle
     } else if (warp >= 4) {
         // ------------------------------------------------------------ compute warps
         // warp 4 + 4*half + quad: TMEM lane quadrant `quad` (rows 16q..16q+15 of
