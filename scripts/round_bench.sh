@@ -22,6 +22,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 PARO_WATCHDOG_S=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k3_attention -s 1 -c 1 -o gpurun_out/${TAG}_k3_c2 python bench.py --profile --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 PARO_WATCHDOG_S=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k1_reorder -s 1 -c 1 -o gpurun_out/${TAG}_k1_c2 python bench.py --profile --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 PARO_WATCHDOG_S=0 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k3_attention -s 1 -c 1 -o gpurun_out/${TAG}_k3_c5 python bench.py --config c5 --profile --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+PARO_WATCHDOG_S=0 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k3_attention -s 1 -c 1 -o gpurun_out/${TAG}_k3_c4 python bench.py --config c4 --profile --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 PARO_WATCHDOG_S=0 timeout 900 compute-sanitizer --tool memcheck --leak-check full python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_memcheck_smoke.log 2>&1
 PARO_WATCHDOG_S=0 timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_racecheck_smoke.log 2>&1
 PARO_WATCHDOG_S=0 timeout 900 compute-sanitizer --tool synccheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_synccheck_smoke.log 2>&1
