@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "layer.cuh"
 
@@ -294,6 +295,162 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 2) k1_reorder_quantize(Laye
 }
 
 // ---------------------------------------------------------------------------
+// K1, one tensor per CTA: grid (kb2, H, 3), blockIdx.z = 0 Q, 1 K, 2 V -- the
+// same per-element arithmetic, reductions and outputs as k1_reorder_quantize,
+// with a third of its registers, so 4 CTAs fit an SM at d=128 and a small layer
+// (c4: 1536 blocks) is not cut into 5.2 waves of 2 CTAs per SM
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256, 4) k1_reorder_quantize_split(LayerDev L, const float* __restrict__ q,
+                                                                 const float* __restrict__ k,
+                                                                 const float* __restrict__ v, int v_bits,
+                                                                 uint32_t head_begin) {
+    constexpr int F4 = D / 4;
+    constexpr int RPP = 256 / F4;
+    constexpr int PASSES = 64 / RPP;
+    constexpr int G = D / 64;
+    const uint32_t b = blockIdx.x, h = head_begin + blockIdx.y, which = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c4 = tid % F4;
+    const int r0 = tid / F4;
+    const int grp = (c4 * 4) / 64;
+
+    __shared__ float s_amax[8][2];
+    __shared__ int s_colsum[8][D];
+    __shared__ uint32_t s_src[64];
+
+    const size_t head_in = (size_t)h * L.N * D;
+    if (tid < 64) {
+        const PermDesc pd = L.perm[h];
+        const uint32_t i = b * 64 + tid;
+        s_src[tid] = i < L.N ? perm_src(pd, i) : (b * 64 < L.N ? perm_src(pd, b * 64) : 0xffffffffu);
+    }
+    __syncthreads();
+    const float* __restrict__ in = which == 0 ? q : (which == 1 ? k : v);
+    float4 x[PASSES];
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const uint32_t rr = r0 + RPP * j, i = b * 64 + rr, src = s_src[rr];
+        const size_t off = head_in + (size_t)src * D + c4 * 4;
+        if (i < L.N)
+            x[j] = ld_stream(in + off);
+        else // K padding rows repeat the block's first row; Q / V padding rows are zero
+            x[j] = which == 1 && src != 0xffffffffu ? ld_stream(in + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (L.rope_cos && which < 2) {
+        auto rot = [](float4 x, float4 c, float4 s) {
+            return make_float4(__fsub_rn(__fmul_rn(x.x, c.x), __fmul_rn(x.y, s.x)),
+                               __fadd_rn(__fmul_rn(x.y, c.y), __fmul_rn(x.x, s.y)),
+                               __fsub_rn(__fmul_rn(x.z, c.z), __fmul_rn(x.w, s.z)),
+                               __fadd_rn(__fmul_rn(x.w, c.w), __fmul_rn(x.z, s.w)));
+        };
+#pragma unroll
+        for (int j = 0; j < PASSES; ++j) {
+            const uint32_t rr = r0 + RPP * j, i = b * 64 + rr, src = s_src[rr];
+            if (src == 0xffffffffu || src < L.dp)
+                continue;
+            const size_t t = (size_t)(src - L.dp) * D + c4 * 4;
+            const float4 c = __ldg(reinterpret_cast<const float4*>(L.rope_cos + t));
+            const float4 sn = __ldg(reinterpret_cast<const float4*>(L.rope_sin + t));
+            if (which == 1 || i < L.N)
+                x[j] = rot(x[j], c, sn);
+        }
+    }
+    float a = 0.f;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j)
+        a = fmaxf(a, amax4(x[j]));
+    if (which < 2) { // Q / K: per 64-column group (d=128: lanes 0-15 group 0, 16-31 group 1)
+#pragma unroll
+        for (int o = (G == 2 ? 8 : 16); o > 0; o >>= 1)
+            a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    }
+    if (lane == 0 || (G == 2 && lane == 16))
+        s_amax[warp][(G == 2 && lane == 16) ? 1 : 0] = a;
+    __syncthreads();
+    const int gsel = which < 2 ? grp : 0;
+    float gm = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+        gm = fmaxf(gm, s_amax[w][gsel]);
+    const float qmax = which < 2 ? 127.0f : (v_bits == 4 ? 7.0f : 127.0f);
+    float sc;
+    if (which < 2) {
+        sc = __fdiv_rn(gm, 127.0f);
+        if (sc == 0.0f)
+            sc = 1.0f;
+    } else {
+        sc = gm == 0.0f ? 1.0f : __fdiv_rn(gm, qmax);
+    }
+    const float rs = __frcp_rn(sc);
+
+    const size_t head_codes = (size_t)h * L.kb2 * 64 * D;
+    int cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
+#pragma unroll
+    for (int j = 0; j < PASSES; ++j) {
+        const size_t off = head_codes + (size_t)(b * 64 + r0 + RPP * j) * D + c4 * 4;
+        int e0, e1, e2, e3;
+        quant_sym4(x[j], sc, rs, qmax, e0, e1, e2, e3);
+        if (which == 0) {
+            *reinterpret_cast<uint32_t*>(L.q + off) = pack4(e0, e1, e2, e3);
+        } else if (which == 1) {
+            *reinterpret_cast<uint32_t*>(L.k + off) = pack4(e0, e1, e2, e3);
+        } else {
+            if (L.v_packed)
+                *reinterpret_cast<uint16_t*>(L.v + off / 2) =
+                    (uint16_t)((e0 & 15) | ((e1 & 15) << 4) | ((e2 & 15) << 8) | ((e3 & 15) << 12));
+            else
+                *reinterpret_cast<uint32_t*>(L.v + off) = pack4(e0, e1, e2, e3);
+            cs0 += e0;
+            cs1 += e1;
+            cs2 += e2;
+            cs3 += e3;
+        }
+    }
+    float* meta = L.meta + ((size_t)h * L.kb2 + b) * meta_stride(D);
+    if (which == 2) {
+        if (G == 1) {
+            cs0 += __shfl_xor_sync(0xffffffffu, cs0, 16);
+            cs1 += __shfl_xor_sync(0xffffffffu, cs1, 16);
+            cs2 += __shfl_xor_sync(0xffffffffu, cs2, 16);
+            cs3 += __shfl_xor_sync(0xffffffffu, cs3, 16);
+        }
+        if (G == 2 || lane < 16) {
+            s_colsum[warp][c4 * 4 + 0] = cs0;
+            s_colsum[warp][c4 * 4 + 1] = cs1;
+            s_colsum[warp][c4 * 4 + 2] = cs2;
+            s_colsum[warp][c4 * 4 + 3] = cs3;
+        }
+        __syncthreads();
+        if (tid < D) {
+            int sum = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+                sum += s_colsum[w][tid];
+            meta[4 + tid] = (float)sum;
+        }
+        if (tid == 0) {
+            meta[2] = sc;
+            meta[3] = 0.f;
+        }
+    } else if (which == 1) {
+        if (tid == 0)
+            meta[0] = sc;
+        if (tid == F4 - 1)
+            meta[1] = G == 2 ? sc : 0.f;
+    } else {
+        if (tid == 0)
+            L.qsc[((size_t)h * L.kb2 + b) * G + 0] = sc;
+        if (G == 2 && tid == F4 - 1)
+            L.qsc[((size_t)h * L.kb2 + b) * G + 1] = sc;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Standalone quantize(m, {bits, Symmetric, PerBlock, 64}) for cols in {64,128}
 // (same arithmetic as K1's Q/K path, identity row order).
 // ---------------------------------------------------------------------------
@@ -543,10 +700,29 @@ __device__ void k2_lpt_range(const LayerDev& L, uint32_t h0, uint32_t h1, uint32
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
+// d=128 layers below ~16 waves of the fused kernel (2 CTAs per SM) take the split
+// kernel: c4 (1536 blocks) K1 45.5 -> 41.8 us; at c5 (47k blocks) the fused kernel
+// wins, 0.960 vs 1.005 ms, as it does at d=64 (c2 0.134 vs 0.173 ms)
+constexpr size_t kK1SplitBelow = 296 * 16;
 cudaError_t launch_k1(const LayerDev& L, const float* q, const float* k, const float* v, int v_bits,
                       uint32_t head_begin, uint32_t head_count, cudaStream_t st) {
     if (head_count == 0)
         return cudaSuccess;
+    // one CTA per tensor where the fused kernel's CTAs (2 per SM at d=128, 4 at d=64)
+    // would leave a ragged last wave; PARO_K1_SPLIT=0 / 1 forces either
+    static const int force = [] {
+        const char* e = getenv("PARO_K1_SPLIT");
+        return e ? atoi(e) : -1;
+    }();
+    const bool split = force >= 0 ? force != 0 : L.D == 128 && (size_t)L.kb2 * head_count < kK1SplitBelow;
+    if (split) {
+        dim3 grid(L.kb2, head_count, 3);
+        if (L.D == 64)
+            k1_reorder_quantize_split<64><<<grid, 256, 0, st>>>(L, q, k, v, v_bits, head_begin);
+        else
+            k1_reorder_quantize_split<128><<<grid, 256, 0, st>>>(L, q, k, v, v_bits, head_begin);
+        return cudaGetLastError();
+    }
     dim3 grid(L.kb2, head_count);
     if (L.D == 64)
         k1_reorder_quantize<64><<<grid, 256, 0, st>>>(L, q, k, v, v_bits, head_begin);
