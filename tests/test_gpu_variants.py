@@ -4,6 +4,10 @@ per process).
 
   PARO_K3_DEC=1  d=64 decoupled softmax / quantizer / epilogue kernel
                  (paro_b200/csrc/attention_dec_kernel.cu)
+  PARO_K1_SPLIT  0 / 1: K1 fused (one CTA per q-block for Q, K and V) or split (one
+                 CTA per tensor) regardless of the layer size, so both K1 kernels
+                 meet the oracle at d=64 and d=128 (by default small d=128 layers
+                 take the split kernel and everything else the fused one)
 """
 import os
 import subprocess
@@ -39,4 +43,12 @@ def test_decoupled_kernel_layers_match_oracle():
 def test_decoupled_kernel_pcodes_full_shape():
     # the final P codes of sampled q-blocks at the BASELINE shapes, code for code
     rc, out = run_child({"PARO_K3_DEC": "1"}, ["tests/test_gpu_fullshape_int.py", "-k", "p_codes_bit_exact"])
+    assert rc == 0, out
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_k1_kernels_match_oracle(split):
+    rc, out = run_child({"PARO_K1_SPLIT": split},
+                        ["tests/test_gpu_parity.py", "-k", "reorder_quantize or attention_matches or rope_fused or tiny",
+                         "tests/test_gpu_vpack.py"])
     assert rc == 0, out
