@@ -82,6 +82,13 @@ namespace paro {
 #ifndef PARO_EXACT_MONO
 #define PARO_EXACT_MONO 1
 #endif
+#ifndef PARO_I2F_FMA
+// int32 -> fp32 conversions on the FMA pipe (IMAD + FADD2, k3_common.cuh i2f2_fma)
+// instead of ALU I2F: bit 0 = the d=128 pass-1 scan, bit 1 = pass 2 at d=128,
+// bit 2 = pass 2 at d=64 (measured: bit 2 c2 K3 4.280 -> 4.213 ms; bits 0 / 1 cost
+// d=128 3% / 5%, c5 109.8 -> 112.9 / 115.0 ms)
+#define PARO_I2F_FMA 4
+#endif
 #ifndef PARO_K3_W12
 #define PARO_K3_W12 0
 #endif
@@ -351,7 +358,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                                              const uint8_t* qtile, const uint8_t* ktile, uint8_t* prow, uint32_t r,
                                              float sq1, float& gamma_out, float& lo_out, float& pscale_out,
                                              uint32_t half, float4* xch, uint16_t* xlist, uint32_t red_bar,
-                                             uint32_t red_par, unsigned long long (&prof)[18]) {
+                                             uint32_t red_par, unsigned long long (&prof)[18], uint32_t one) {
     PROF_T(tp0);
     constexpr int G = D / 64;
     // M128 (d=64): all 32 lanes of this warp hold rows of ONE q-block (side), whose
@@ -430,10 +437,11 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             for (int k = 0; k < 16; ++k) {
                 const uint32_t ja = h2 * 32 + 2 * k, jb = ja + 1;
                 // y = fma(S_1, c1, S_0 * c0) per column, two columns per packed FMUL2 / FFMA2
-                const uint64_t y2 = fma2(pk(__int2float_rn((int32_t)x1[2 * k]), __int2float_rn((int32_t)x1[2 * k + 1])),
-                                         pk(c1, c1),
-                                         mul2(pk(__int2float_rn((int32_t)x0[2 * k]), __int2float_rn((int32_t)x0[2 * k + 1])),
-                                              pk(c0, c0)));
+                const uint64_t f1 = (PARO_I2F_FMA & 1) ? i2f2_fma((int32_t)x1[2 * k], (int32_t)x1[2 * k + 1], one)
+                                                       : pk(__int2float_rn((int32_t)x1[2 * k]), __int2float_rn((int32_t)x1[2 * k + 1]));
+                const uint64_t f0 = (PARO_I2F_FMA & 1) ? i2f2_fma((int32_t)x0[2 * k], (int32_t)x0[2 * k + 1], one)
+                                                       : pk(__int2float_rn((int32_t)x0[2 * k]), __int2float_rn((int32_t)x0[2 * k + 1]));
+                const uint64_t y2 = fma2(f1, pk(c1, c1), mul2(f0, pk(c0, c0)));
                 float ya, yb;
                 upk(y2, ya, yb);
                 const float ka = tagf(ya, ja), kb = tagf(yb, jb);
@@ -635,9 +643,10 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                const uint64_t y2 = fma2(pk(__int2float_rn((int32_t)x[2 * k] - smax_i),
-                                            __int2float_rn((int32_t)x[2 * k + 1] - smax_i)),
-                                         c00, nm);
+                const uint64_t y2 =
+                    fma2((PARO_I2F_FMA & 4) ? i2f2_fma_b((int32_t)x[2 * k], (int32_t)x[2 * k + 1], one, 0x4B400000u - (uint32_t)smax_i)
+                                            : pk(__int2float_rn((int32_t)x[2 * k] - smax_i), __int2float_rn((int32_t)x[2 * k + 1] - smax_i)),
+                         c00, nm);
                 float ya, yb;
                 upk(y2, ya, yb);
                 pv[2 * k] = ex2(ya);
@@ -650,10 +659,12 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                const uint64_t d0 = pk(__int2float_rn((int32_t)x0[2 * k] - smax_i),
-                                       __int2float_rn((int32_t)x0[2 * k + 1] - smax_i));
-                const uint64_t d1 = pk(__int2float_rn((int32_t)x1[2 * k] - smax1_i),
-                                       __int2float_rn((int32_t)x1[2 * k + 1] - smax1_i));
+                const uint64_t d0 = (PARO_I2F_FMA & 2) ? i2f2_fma_b((int32_t)x0[2 * k], (int32_t)x0[2 * k + 1], one, 0x4B400000u - (uint32_t)smax_i)
+                                                       : pk(__int2float_rn((int32_t)x0[2 * k] - smax_i),
+                                                            __int2float_rn((int32_t)x0[2 * k + 1] - smax_i));
+                const uint64_t d1 = (PARO_I2F_FMA & 2) ? i2f2_fma_b((int32_t)x1[2 * k], (int32_t)x1[2 * k + 1], one, 0x4B400000u - (uint32_t)smax1_i)
+                                                       : pk(__int2float_rn((int32_t)x1[2 * k] - smax1_i),
+                                                            __int2float_rn((int32_t)x1[2 * k + 1] - smax1_i));
                 const uint64_t y2 = fma2(d1, c11, fma2(d0, c00, nm));
                 float ya, yb;
                 upk(y2, ya, yb);
@@ -1466,7 +1477,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
                                 gamma, lo, pscale, 0u, nullptr,
                                 reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + quad * 512, bar(BR::RED),
-                                T & 1, prof);
+                                T & 1, prof, P.one);
                 if (DUMP && dslot >= 0 && live) {
                     dump_row(P.dump, dslot, t, r, prow, 0, 4);
                     if (r == 0)
@@ -1776,7 +1787,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                                       side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half,
                                       reinterpret_cast<float4*>(smem + C::OFF_XCH),
                                       reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + (warp - 4) * 512,
-                                      bar(BR::RED), T & 1, prof);
+                                      bar(BR::RED), T & 1, prof, P.one);
                 if (DUMP && dslot >= 0 && live) {
                     dump_row(P.dump, dslot, t, r, prow, (int)half * 2, 2);
                     if (r == 0 && half == 0)
@@ -2037,6 +2048,7 @@ cudaError_t launch_k3(const LayerDev& L, const CUtensorMap& tq, const CUtensorMa
         return cudaSuccess;
     K3Params p;
     p.L = L;
+    p.one = 1;
     p.scale64 = scale;
     p.scale_log2 = (float)(scale * kLog2e);
     p.p_qmax = pv_bits == 4 ? 15.0f : 255.0f;

@@ -47,6 +47,27 @@ __device__ __forceinline__ uint64_t add2_rm(uint64_t a, uint64_t b) {
     asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+// int32 pair -> fp32 pair exactly (|x| < 2^22) on the FMA pipe instead of two ALU
+// I2F: IMAD x * 1 + 0x4B400000 gives the bits of 1.5 * 2^23 + x, one packed FADD2
+// of -1.5 * 2^23 leaves float(x). `one` must be a runtime 1 (a kernel parameter)
+// or ptxas folds the IMAD into an ALU IADD3.
+__device__ __forceinline__ uint64_t i2f2_fma(int32_t a, int32_t b, uint32_t one) {
+    uint32_t ua, ub;
+    asm("mad.lo.u32 %0, %1, %2, 1262485504;" : "=r"(ua) : "r"(a), "r"(one));
+    asm("mad.lo.u32 %0, %1, %2, 1262485504;" : "=r"(ub) : "r"(b), "r"(one));
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(((uint64_t)ub << 32) | ua), "l"(0xCB400000CB400000ull));
+    return r;
+}
+// the same for (x - s) with base = 0x4B400000 - s folded into the IMAD addend (|x - s| < 2^22)
+__device__ __forceinline__ uint64_t i2f2_fma_b(int32_t a, int32_t b, uint32_t one, uint32_t base) {
+    uint32_t ua, ub;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ua) : "r"(a), "r"(one), "r"(base));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ub) : "r"(b), "r"(one), "r"(base));
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(((uint64_t)ub << 32) | ua), "l"(0xCB400000CB400000ull));
+    return r;
+}
 __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -97,6 +118,7 @@ struct K3Params {
     uint32_t* work_counter; // next index into `order` (zeroed before the launch; DYNAMIC)
     unsigned long long* stats; // optional debug counters: [0] warp-steps, [1] exact-path entries, [2] risky groups
     K3Dump dump;               // P-code dump test hook (dump.slot == nullptr: off)
+    uint32_t one;              // 1, opaque to ptxas (i2f2_fma)
 };
 
 // P-code dump of one row's final codes for step t (cols [c0, c0 + 16*nch) of the
