@@ -85,9 +85,13 @@ namespace paro {
 #ifndef PARO_I2F_FMA
 // int32 -> fp32 conversions on the FMA pipe (IMAD + FADD2, k3_common.cuh i2f2_fma)
 // instead of ALU I2F: bit 0 = the d=128 pass-1 scan, bit 1 = pass 2 at d=128,
-// bit 2 = pass 2 at d=64 (measured: bit 2 c2 K3 4.280 -> 4.213 ms; bits 0 / 1 cost
+// bit 2 = pass 2 at d=64, bit 3 = the d=64 epilogue's P.V dequant, bit 4 = the d=128
+// dequant (|P.V| <= 64 * 255 * 127 < 2^22) (measured: bit 2 c2 K3 4.280 -> 4.213 ms; bits 0 / 1 cost
 // d=128 3% / 5%, c5 109.8 -> 112.9 / 115.0 ms)
 #define PARO_I2F_FMA 4
+#endif
+#ifndef PARO_PACK_IMAD
+#define PARO_PACK_IMAD 0 // P-code word packing by IMAD (FMA pipe): bit 0 = the low variant, bit 1 = the stored high one
 #endif
 #ifndef PARO_K3_W12
 #define PARO_K3_W12 0
@@ -778,6 +782,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
     const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
     uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
+    const uint32_t m8 = one << 8, m16 = one << 16, m24 = one << 24; // runtime 256^e: IMAD, not SHF / LEA
     auto quantize_store = [&](int h2, const float (&pv)[32]) {
         uint32_t whi[8];
 #pragma unroll
@@ -790,13 +795,16 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 const uint64_t u2 = add2_rm(fma2_rm(pk(pv[k], pv[k]), A2, B2), magic2);
                 float ul, uh;
                 upk(u2, ul, uh);
+                // PARO_PACK_IMAD: the word as sum_e 256^e * bits(u_e) - 0x4B000000 mod 2^32 (bits(u_e) =
+                // 0x4B000000 + code_e; every higher multiple of 0x4B000000 vanishes mod 2^32) on the FMA pipe
                 if (e == 0) {
-                    hi4 = __float_as_uint(uh);
-                    lo4 = __float_as_uint(ul);
+                    hi4 = (PARO_PACK_IMAD & 2) ? imad_u32(__float_as_uint(uh), one, 0xB5000000u) : __float_as_uint(uh);
+                    lo4 = (PARO_PACK_IMAD & 1) ? imad_u32(__float_as_uint(ul), one, 0xB5000000u) : __float_as_uint(ul);
                 } else { // insert byte 0 of the code word at byte e
                     const uint32_t sel = e == 1 ? 0x3240u : (e == 2 ? 0x3410u : 0x4210u);
-                    hi4 = __byte_perm(hi4, __float_as_uint(uh), sel);
-                    lo4 = __byte_perm(lo4, __float_as_uint(ul), sel);
+                    const uint32_t m = e == 1 ? m8 : (e == 2 ? m16 : m24);
+                    hi4 = (PARO_PACK_IMAD & 2) ? imad_u32(__float_as_uint(uh), m, hi4) : __byte_perm(hi4, __float_as_uint(uh), sel);
+                    lo4 = (PARO_PACK_IMAD & 1) ? imad_u32(__float_as_uint(ul), m, lo4) : __byte_perm(lo4, __float_as_uint(ul), sel);
                 }
             }
             whi[w] = hi4;
@@ -1591,7 +1599,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                         for (int hh = 0; hh < 2; ++hh) {
                             const int j = q4 * 4 + hh * 2;
                             const uint64_t x2 =
-                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : (PARO_I2F_FMA & 8) ? i2f2_fma((int32_t)raw[j], (int32_t)raw[j + 1], P.one) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
                             const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
                             acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
                         }
@@ -1745,7 +1753,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                         for (int hh = 0; hh < 2; ++hh) {
                             const int j = q4 * 4 + hh * 2;
                             const uint64_t x2 =
-                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
+                                PARO_DIAG_NOI2F ? pk(__int_as_float(raw[j]), __int_as_float(raw[j + 1])) : (PARO_I2F_FMA & 16) ? i2f2_fma((int32_t)raw[j], (int32_t)raw[j + 1], P.one) : pk(__int2float_rn((int32_t)raw[j]), __int2float_rn((int32_t)raw[j + 1]));
                             const uint64_t t2 = fma2(ss2, x2, hh ? pk(uu.z, uu.w) : pk(uu.x, uu.y));
                             acc[(ch * 16 + j) / 2] = fma2(acc[(ch * 16 + j) / 2], g2, t2);
                         }

@@ -59,6 +59,11 @@ __device__ __forceinline__ uint64_t i2f2_fma(int32_t a, int32_t b, uint32_t one)
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(((uint64_t)ub << 32) | ua), "l"(0xCB400000CB400000ull));
     return r;
 }
+__device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 // the same for (x - s) with base = 0x4B400000 - s folded into the IMAD addend (|x - s| < 2^22)
 __device__ __forceinline__ uint64_t i2f2_fma_b(int32_t a, int32_t b, uint32_t one, uint32_t base) {
     uint32_t ua, ub;
