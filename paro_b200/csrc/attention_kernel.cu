@@ -337,13 +337,16 @@ constexpr float kErrS = 5e-7f, kGapSlack = 2e-5f;
 // reduction -> pass 2 p / codes).
 //   d=64 (G=1): the row extremes are integer maxima of S, so the reference's
 //   exact fp64 logits of the extremes and the exact running max m64 are known
-//   every step. P codes are made BIT-EXACT with the reference's fp32
-//   quantizer of the fp64 p: the fast path computes each code twice from
-//   (1 -/+ kappa)-perturbed quotients (one packed FFMA2.RM per element); where
-//   the two differ (~1e-4 of elements) the code is recomputed in fp64 from the
-//   exact tile lo/hi (from every row's published extremes) and S re-derived
-//   with dp4a from the Q/K tiles still in smem.
-//   d=128 (G=2): fp32 fast path only (codes tolerance-level).
+//   every step. d=128 (G=2): the logit is c0 * S_0 + c1 * S_1, so the extremes
+//   come from a column-tagged fp32 scan (top-2 / bottom-2 per row), their fp64
+//   logits from the selected columns' (S_0, S_1), and a near tie within the
+//   fp32 error bound sends the row to an exact fp64 rescan of its candidates.
+//   Both: P codes are made BIT-EXACT with the reference's fp32 quantizer of
+//   the fp64 p: the fast path computes each code twice from (1 -/+ kappa)-
+//   perturbed quotients (one packed FFMA2.RM per element); where the two
+//   differ (~1e-4 of elements) the code is recomputed in fp64 from the exact
+//   tile lo/hi (from every row's published extremes) and S re-derived with
+//   dp4a from the Q/K tiles still in smem.
 // Lanes whose q-block has no tile this step (`live` false) run the same
 // instructions but change no state and contribute neutral extremes.
 // ---------------------------------------------------------------------------
@@ -852,7 +855,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         risk = 0;
     PROF_T(tp3);
     PROF_ADD(3, tp3 - tp2);
-    // -------- exact boundary path (d=64): rare, warp-uniform entry
+    // -------- exact boundary path: rare, warp-uniform entry
 #ifdef PARO_EXP_NOEXACT
     risk = 0;
 #endif
