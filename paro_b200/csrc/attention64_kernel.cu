@@ -197,8 +197,8 @@ __device__ __forceinline__ void softmax_pass2(const Pass1& a, uint32_t s_addr, d
         pscale = 1.f;
     const float inv = __frcp_rn(pscale);
     const uint64_t c00 = pk(a.c0, a.c0), nm = pk(a.dmax, a.dmax);
-    const float inv_lo = inv * (1.0f - kKappa), inv_hi = inv * (1.0f + kKappa);
-    const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
+    uint64_t A2, B2;
+    pgroup_consts<3>(lo, hi, inv, p_qmax, A2, B2);
     const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
     const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
     uint64_t sum2 = pk(0.f, 0.f);

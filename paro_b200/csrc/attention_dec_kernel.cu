@@ -572,8 +572,8 @@ __global__ void __launch_bounds__(KDec::THREADS, KDec::MINB)
                 if (pscale == 0.f)
                     pscale = 1.f;
                 const float inv = __frcp_rn(pscale);
-                const float inv_lo = inv * (1.0f - kKappa), inv_hi = inv * (1.0f + kKappa);
-                const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
+                uint64_t A2, B2;
+                pgroup_consts<3>(lo, hi, inv, P.p_qmax, A2, B2);
                 const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
                 uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
 #pragma unroll kDecUnroll

@@ -780,9 +780,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     if (G == 1 && !kOverlap && !kStash)
         PROF_ADD(13, tp2 - tbar);
 #endif
-    const float kap = kKappa;
-    const float inv_lo = inv * (1.0f - kap), inv_hi = inv * (1.0f + kap);
-    const uint64_t A2 = pk(inv_lo, inv_hi), B2 = pk(0.5f - lo * inv_lo, 0.5f - lo * inv_hi);
+    uint64_t A2, B2;
+    pgroup_consts<G == 1 ? 3 : 1>(lo, hi, inv, p_qmax, A2, B2);
     const uint64_t magic2 = pk(8388608.0f, 8388608.0f);
     uint32_t risk = 0; // bit g: 4-element group g has a code that needs the exact path
     const uint32_t m8 = one << 8, m16 = one << 16, m24 = one << 24; // runtime 256^e: IMAD, not SHF / LEA

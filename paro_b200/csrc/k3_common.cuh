@@ -247,14 +247,20 @@ struct RowStatC { // 24 bytes
 static_assert(sizeof(RowStatC) == 24, "RowStatC layout");
 
 constexpr double kLog2e = 1.4426950408889634;
-// Relative band of the fast-path quotient q = (p - lo) / pscale at d=64. The
+// Band of the fast-path quotient q = (p - lo) / pscale (pgroup_consts below). The
 // fp32 path forms the exp2 argument as (S - smax) * c + d with d = exact
-// (tmax - m) * log2e, so its error is ~6e-8 * |arg| + the ex2.approx error
-// (~2.4e-7); with lo/hi from the same formula the quotient is within ~4-6e-7
-// of the reference's. A code is trusted only if q*(1-kappa) and q*(1+kappa)
-// round to the same integer, else it is recomputed exactly in fp64.
-// Measured on c2/c3 (8M sampled elements each): kappa 0 leaves code flips
-// (max|dO|/max|O| 5.8e-4 INT8, 6.4e-3 INT4); 4e-7 and 8e-7 are exact.
+// (tmax - m) * log2e, so the argument's error is <= 2^-23 |arg| at d=64 (both
+// terms <= 0); ex2.approx.ftz.f32 is within 1.44e-7 relative over [-126, 0]
+// (every input, scripts/ex2_err.cu); the reference rounds p to fp32 (2^-24).
+// kappa / 2 = 3e-7 bounds each fast p's relative error for |arg| up to ~1
+// (with the A / B rounding of the quantizer FMA) -- the regime of narrow tiles,
+// where the error enters q absolutely, as (p + lo) / pscale; for the common
+// tile (lo << p) the band is kappa * q, and there kappa is empirical: measured
+// on c2/c3 (8M sampled elements each) kappa 0 leaves code flips (max|dO|/max|O|
+// 5.8e-4 INT8, 6.4e-3 INT4), 4e-7 and 8e-7 are exact, and every full-shape
+// P-code dump at c2-c5 and every adversarial tile family passes at 6e-7.
+// A code is trusted only if both variants round to the same integer, else it
+// is recomputed exactly in fp64.
 #ifndef PARO_RED_MBAR
 #define PARO_RED_MBAR 1
 #endif
@@ -266,6 +272,40 @@ constexpr double kLog2e = 1.4426950408889634;
 #define PARO_KAPPA 6e-7f
 #endif
 constexpr float kKappa = PARO_KAPPA;
+
+// Fast-path quantizer constants of one P group (lo, hi: the group's fast extremes,
+// inv = 1 / pscale). The code of t = (p - lo) / pscale is taken from the two variants
+// t -/+ D, D = kp * (p + lo) / pscale + kq * (p - lo) / pscale:
+//   kp = kappa / 2 bounds the relative error of each fast p (and of lo, hi) against
+//      the reference's fp32(exp(fp64)) -- as an ABSOLUTE error in t it scales with
+//      (p + lo) / pscale, which dominates on a narrow tile (hi - lo << lo: every p of the
+//      tile close to lo, e.g. near-uniform attention) where a band relative to t alone
+//      misses code flips (tests/test_gpu_pcode_adversarial.py "flat");
+//   kq = kp * (hi + lo) / (hi - lo) is pscale's relative error from those of hi and lo
+//      (capped at 1: a degenerate tile sends every code to the exact path).
+// For lo << p (the common tile) D = kappa * t, the band of the relative-only rule.
+// As FMAs: variant -/+ = p * A -/+ B with A = inv (1 -/+ (kq + kp)),
+// B = 0.5 - lo * inv * (1 -/+ (kq - kp)); packed (low variant, high variant).
+// FORM (measured, c2 / c3 / c5 K3): 3 at d=64 (kq from inv: 4.38 / 2.63 ms; with the
+// __fdividef of form 1, 4.44 / 2.68), 1 at d=128 (110.6 ms; form 3 112.7)
+template <int FORM>
+__device__ __forceinline__ void pgroup_consts(float lo, float hi, float inv, float qmax, uint64_t& A2, uint64_t& B2) {
+    const float kp = 0.5f * kKappa;
+    // FORM 3: (hi + lo) / (hi - lo) = (hi + lo) * inv / qmax (inv = qmax / (hi - lo) up to
+    // three roundings: 1.01 margin); a degenerate group (hi <= lo: pscale reset to 1)
+    // sends every code to the exact path
+    const float kq = FORM == 3 ? (hi > lo ? fminf(1.0f, (kp * 1.01f) * (hi + lo) * inv * (1.0f / qmax)) : 1.0f)
+                               : fminf(1.0f, kp * __fdividef(hi + lo, fmaxf(hi - lo, 1e-30f)));
+    if (FORM == 1) {
+        const float li = lo * inv;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(A2) : "f"(inv * (1.0f - (kq + kp))), "f"(inv * (1.0f + (kq + kp))));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(B2) : "f"(0.5f - li * (1.0f - (kq - kp))), "f"(0.5f - li * (1.0f + (kq - kp))));
+    } else {
+        const float kqp = kq + kp, kqm = kq - kp;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(A2) : "f"(inv * (1.0f - kqp)), "f"(inv * (1.0f + kqp)));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(B2) : "f"(0.5f - lo * (inv * (1.0f - kqm))), "f"(0.5f - lo * (inv * (1.0f + kqm))));
+    }
+}
 
 // int32 S of (row r, key j) recomputed from the smem Q/K tiles (64-byte rows, 64B swizzle)
 __device__ __forceinline__ int32_t dot_row64(const uint8_t* qtile, const uint8_t* ktile, uint32_t r, uint32_t j) {

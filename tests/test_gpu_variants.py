@@ -42,7 +42,8 @@ def test_decoupled_kernel_layers_match_oracle():
 
 def test_decoupled_kernel_pcodes_full_shape():
     # the final P codes of sampled q-blocks at the BASELINE shapes, code for code
-    rc, out = run_child({"PARO_K3_DEC": "1"}, ["tests/test_gpu_fullshape_int.py", "-k", "p_codes_bit_exact"])
+    rc, out = run_child({"PARO_K3_DEC": "1"}, ["tests/test_gpu_fullshape_int.py", "tests/test_gpu_pcode_adversarial.py",
+                                               "-k", "p_codes_bit_exact or p_codes_adversarial"])
     assert rc == 0, out
 
 
