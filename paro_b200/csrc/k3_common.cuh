@@ -288,8 +288,32 @@ constexpr float kKappa = PARO_KAPPA;
 // B = 0.5 - lo * inv * (1 -/+ (kq - kp)); packed (low variant, high variant).
 // FORM (measured, c2 / c3 / c5 K3): 3 at d=64 (kq from inv: 4.38 / 2.63 ms; with the
 // __fdividef of form 1, 4.44 / 2.68), 1 at d=128 (110.6 ms; form 3 112.7)
+#ifndef PARO_BAND_RIGOROUS
+#define PARO_BAND_RIGOROUS 0
+#endif
 template <int FORM>
 __device__ __forceinline__ void pgroup_consts(float lo, float hi, float inv, float qmax, uint64_t& A2, uint64_t& B2) {
+#if PARO_BAND_RIGOROUS
+    // every term bounded (d=64): a fast p = ex2.approx(arg) with |arg - exact| <= 2^-23 |arg|
+    // is within (E + L * |arg|) p of the reference's fp32 p, E = 1.44e-7 (ex2.approx, every
+    // input) + 2^-24 (the reference's rounding) + 6e-8 (the quantizer's A / B rounding),
+    // L = ln2 * 2^-23. Elements that can sit on a code boundary have p >= pb = lo + pscale/2,
+    // so |arg| <= -log2(pb) for them; lo's and hi's errors use their own |arg|.
+    {
+        constexpr float E = 2.64e-7f, L = 8.27e-8f;
+        const float ps = fmaxf(hi - lo, 1e-30f) * (1.0f / qmax);
+        const float a = E + L * (fmaxf(-__log2f(lo + 0.5f * ps), 0.f) + 0.02f);
+        const float elo = (E + L * (fminf(-__log2f(fmaxf(lo, 1e-37f)), 160.f) + 0.02f)) * lo + 1.2e-38f;
+        const float ehi = (E + L * (fmaxf(-__log2f(hi), 0.f) + 0.02f)) * hi;
+        // pscale's relative error from hi's and lo's, + 9 roundings of ours and the reference's
+        const float kq = hi > lo ? fminf(1.0f, (ehi + elo) * 1.01f * inv * (1.0f / qmax) + 5.4e-7f) : 1.0f;
+        const float c = elo * inv + 2.4e-7f; // lo's absolute error and the final RD rounding, in q units
+        const float kqp = kq + a;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(A2) : "f"(inv * (1.0f - kqp)), "f"(inv * (1.0f + kqp)));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(B2) : "f"(0.5f - lo * (inv * (1.0f - kq)) - c), "f"(0.5f - lo * (inv * (1.0f + kq)) + c));
+        return;
+    }
+#endif
     const float kp = 0.5f * kKappa;
     // FORM 3: (hi + lo) / (hi - lo) = (hi + lo) * inv / qmax (inv = qmax / (hi - lo) up to
     // three roundings: 1.01 margin); a degenerate group (hi <= lo: pscale reset to 1)
