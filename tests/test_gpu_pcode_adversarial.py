@@ -12,6 +12,9 @@ These layers build exactly those tiles:
   steep   queries scaled up: logits spread over hundreds of units, p down to the
           fp32 subnormal range
   mixed   flat and steep rows in one q-block (one P group spans both)
+  cancel  (d=128) the two 64-column groups' S terms large and of opposite sign, so the
+          exp2 argument is a small difference of large products (its fp32 error scales
+          with |S|, not with the argument)
 
 and compare every quantized tile's final codes (after the exact boundary path) with the
 oracle's quant_affine of the reference's fp32(exp(fp64 logit - m)).
@@ -36,6 +39,13 @@ def make_inputs(family, seed, N, d):
         k = base + eps * k
     elif family == "steep":
         q *= np.float32(rng.uniform(4.0, 16.0))
+    elif family == "cancel":  # d=128: the two 64-column halves' S terms large and opposite
+        if d == 128:
+            q[..., 64:] = -q[..., :64] * np.float32(rng.uniform(0.9, 1.1))
+            k[..., 64:] = k[..., :64] + np.float32(0.05) * k[..., 64:]
+            q *= np.float32(rng.uniform(2.0, 6.0))
+        else:
+            q *= np.float32(3.0)
     else:  # mixed: half the rows of every q-block flat against shared keys, half steep
         base = rng.standard_normal((H, 1, d)).astype(np.float32)
         k = base + np.float32(0.02) * k
@@ -43,10 +53,18 @@ def make_inputs(family, seed, N, d):
     return q, k, v
 
 
+KNOWN_GAP = pytest.mark.xfail(
+    reason="d=128 exactness gap (DESIGN.md section 8 item 2): the fp32 exp2 argument sums two S-group "
+    "terms whose rounding scales with |S|, not with the argument; with large opposite terms a code "
+    "can leave the band (1 flip in 215 tiles here)", strict=False)
+
+
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("pv_bits", [4, 8])
-@pytest.mark.parametrize("family", ["flat", "steep", "mixed"])
-def test_p_codes_adversarial(paro, ctx, oracle, family, pv_bits, d):
+@pytest.mark.parametrize("family", ["flat", "steep", "mixed", pytest.param("cancel", marks=[])])
+def test_p_codes_adversarial(paro, ctx, oracle, family, pv_bits, d, request):
+    if family == "cancel" and d == 128:
+        request.applymarker(KNOWN_GAP)
     g = paro.parse_grid(GRID)
     N = g.token_count()
     kb = (N + 63) // 64
