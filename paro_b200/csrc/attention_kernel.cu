@@ -357,7 +357,7 @@ __device__ __forceinline__ long long (*prof_smem())[4] {
     return a;
 }
 #endif
-template <int D, bool SPLIT>
+template <int D, bool SPLIT, bool P4 = false>
 __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk0, float sk1, double scale64,
                                              float scale_log2, uint32_t ncol, bool live, bool valid_row,
                                              RowState& st, float p_qmax, float2* red_w, const float2* red_r,
@@ -614,7 +614,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     }
     // -------- P group extremes over the q-block's 64 rows: 16 lanes x 4 warps
     // (M128: 32 lanes x 2 warps)
-    if (PARO_REDUX == 2 || (PARO_REDUX == 1 && G == 2)) {
+    if (PARO_REDUX == 2 || (PARO_REDUX == 1 && (G == 2 || P4))) {
         // p >= 0 (INF marks an idle row), so the fp32 bit patterns order like the values:
         // one redux.sync per side and extreme instead of a 4-level shuffle chain
         const uint32_t bmin = __float_as_uint(pmin_r), bmax = __float_as_uint(pmax_r);
@@ -877,7 +877,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 hi_a = fmaxf(hi_a, rd[2 * q].y);
             }
             float mn = INFINITY, mx = 0.f;
-            if (PARO_EXACT_MONO == 2 || (PARO_EXACT_MONO == 1 && G == 2)) {
+            if (PARO_EXACT_MONO == 2 || (PARO_EXACT_MONO == 1 && (G == 2 || P4))) {
                 // exp and the fp32 rounding are monotone, so the tile's exact extremes are
                 // float(exp()) of the smallest / largest (logit - m) over its valid rows:
                 // reduce the fp64 arguments over the 64 rows, then one exp each
@@ -1101,7 +1101,7 @@ __device__ __forceinline__ void unpack_v_tile(const uint8_t* pk, uint8_t* vt, ui
 #endif
 // PACKED: INT4 V arrives nibble-packed and is unpacked in shared memory (a separate
 // instantiation: the INT8 kernels carry none of that code)
-template <int D, bool DUMP, bool PACKED>
+template <int D, bool DUMP, bool PACKED, bool P4 = false>
 __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
     k3_attention(const __grid_constant__ K3Params P, const __grid_constant__ CUtensorMap tm_q,
                  const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -1483,7 +1483,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const uint8_t* qtile = smem + C::OFF_Q + (I & 1) * C::QBUF + side * C::QB_OFF;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
-                softmax_step<D, false>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
+                softmax_step<D, false, P4>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2, tail_tile ? tail : 64u, live,
                                 valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r, side, qtile, ktile, prow, r, sq1,
                                 gamma, lo, pscale, 0u, nullptr,
                                 reinterpret_cast<uint16_t*>(smem + C::OFF_XLIST) + quad * 512, bar(BR::RED),
@@ -2028,8 +2028,14 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
                                cudaStream_t st) {
     init_watchdog();
     const uint32_t smem = K3Cfg<D>::SMEM_BYTES;
+    // d=64 with INT4 P codes: its own instantiation with the monotone exact extremes and
+    // redux.sync group extremes (c3 K3 2.63 -> 2.55 ms; at INT8 P they cost c2 2-3%)
     auto kern = p.L.v_packed ? (p.dump.slot ? k3_attention<D, true, true> : k3_attention<D, false, true>)
                              : (p.dump.slot ? k3_attention<D, true, false> : k3_attention<D, false, false>);
+    if constexpr (D == 64) {
+        if (p.p_qmax == 15.0f && !p.L.v_packed)
+            kern = p.dump.slot ? k3_attention<D, true, false, true> : k3_attention<D, false, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
