@@ -93,6 +93,15 @@ namespace paro {
 #ifndef PARO_PACK_IMAD
 #define PARO_PACK_IMAD 0 // P-code word packing by IMAD (FMA pipe): bit 0 = the low variant, bit 1 = the stored high one
 #endif
+#ifndef PARO_ARG128_EXACT
+// d=128 exactness against S-group cancellation (opt-in, DESIGN.md section 8 item 2):
+// bit 1 = pass 2's exp2 argument (S0 - S0x) c0 + (S1 - S1x) c1 + dmax with c_g split in
+// fp32 hi + lo parts and the two products summed with one rounding (arg128_2), so its
+// error scales with the argument, not with the two terms; bit 0 = the row's fast min p
+// from the exact fp64 (tmin - m). Both (3): the adversarial "cancel" family passes;
+// c5 K3 +7% (bit 1) and +0.9% (bit 0)
+#define PARO_ARG128_EXACT 0
+#endif
 #ifndef PARO_K3_W12
 #define PARO_K3_W12 0
 #endif
@@ -379,6 +388,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const bool valid = live && valid_row;
     // -------- pass 1: row extremes (4 independent chains)
     float m32, pmax_r, pmin_r, c0, c1 = 0.f, dmax = 0.f;
+    float c0lo = 0.f, c1lo = 0.f; // d=128 (PARO_ARG128_EXACT): c_g - fp32(c_g)
     int32_t smax_i = 0, smax1_i = 0; // d=64: row max of S; d=128: (S_0, S_1) of the row's argmax column
     double a64 = 0.0, a64b = 0.0, m64 = st.m64;
     if (G == 1) {
@@ -420,8 +430,15 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         // top-2 / bottom-2 gap is within the fp32 error bound (rare)
         a64 = __dmul_rn((double)sq, (double)sk0);
         a64b = __dmul_rn((double)sq1, (double)sk1);
-        c0 = (float)(__dmul_rn(__dmul_rn(scale64, a64), kLog2e));
-        c1 = (float)(__dmul_rn(__dmul_rn(scale64, a64b), kLog2e));
+        {
+            const double c0d = __dmul_rn(__dmul_rn(scale64, a64), kLog2e), c1d = __dmul_rn(__dmul_rn(scale64, a64b), kLog2e);
+            c0 = (float)c0d;
+            c1 = (float)c1d;
+            if (PARO_ARG128_EXACT) {
+                c0lo = (float)(c0d - (double)c0);
+                c1lo = (float)(c1d - (double)c1);
+            }
+        }
         // 4 chains (pair k -> chain k & 3) for latency; top-2 / bottom-2 merges with
         // 3-input min / max: M2' = max(M2, min(M1, hi), lo), M1' = max(M1, hi)
         float M1[4], M2[4], N1[4], N2[4];
@@ -591,7 +608,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         smax1_i = s1x;
         // exp2 argument of element j = (S0_j - S0x) * c0 + (S1_j - S1x) * c1 + dmax
         pmax_r = ex2(dmax);
-        pmin_r = ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
+        pmin_r = (PARO_ARG128_EXACT & 1) ? ex2((float)((tmin64 - m64) * kLog2e)) // no S-group cancellation
+                                   : ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
         if (!SPLIT || half == 0)
             *rs_w = RowStatC{tmin64 - m64, tmax64 - m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f};
         PROF_T(tq4);
@@ -641,6 +659,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         *red_w = make_float2(pmin_r, pmax_r);
     // -------- pass 2: p, row sum, codes (two perturbed variants per element)
     const uint64_t c00 = pk(c0, c0), c11 = pk(c1, c1), nm = pk(dmax, dmax);
+    const uint64_t c0lo2 = pk(c0lo, c0lo), c1lo2 = pk(c1lo, c1lo);
     uint64_t sum2 = pk(0.f, 0.f);
     const bool tail_any = __any_sync(0xffffffffu, ncol < 64u);
     auto compute_p = [&](int h2, float (&pv)[32], bool mask_tail) { // p of the row's 32 columns of half h2, + row sum
@@ -672,7 +691,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 const uint64_t d1 = (PARO_I2F_FMA & 2) ? i2f2_fma_b((int32_t)x1[2 * k], (int32_t)x1[2 * k + 1], one, 0x4B400000u - (uint32_t)smax1_i)
                                                        : pk(__int2float_rn((int32_t)x1[2 * k] - smax1_i),
                                                             __int2float_rn((int32_t)x1[2 * k + 1] - smax1_i));
-                const uint64_t y2 = fma2(d1, c11, fma2(d0, c00, nm));
+                const uint64_t y2 = (PARO_ARG128_EXACT & 2) ? arg128_2(d0, d1, c00, c11, c0lo2, c1lo2, nm)
+                                                      : fma2(d1, c11, fma2(d0, c00, nm));
                 float ya, yb;
                 upk(y2, ya, yb);
                 pv[2 * k] = ex2(ya);
@@ -979,6 +999,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const int32_t smax1_o = __shfl_sync(0xffffffffu, smax1_i, (int)o);
             const float c0_o = __shfl_sync(0xffffffffu, c0, (int)o);
             const float c1_o = __shfl_sync(0xffffffffu, c1, (int)o);
+            const float c0lo_o = (G == 2 && PARO_ARG128_EXACT) ? __shfl_sync(0xffffffffu, c0lo, (int)o) : 0.f;
+            const float c1lo_o = (G == 2 && PARO_ARG128_EXACT) ? __shfl_sync(0xffffffffu, c1lo, (int)o) : 0.f;
             const float dmax_o = __shfl_sync(0xffffffffu, dmax, (int)o);
             const double a64_o = __shfl_sync(0xffffffffu, a64, (int)o);
             const double a64b_o = __shfl_sync(0xffffffffu, a64b, (int)o);
@@ -996,9 +1018,17 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             else
                 dot_row128(qt, kt, r_o, j, Sj, S1j);
             { // re-run the two fast variants of this element; only a split pair needs fp64
-                const float pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o))
-                                        : ex2(fmaf(__int2float_rn(S1j - smax1_o), c1_o,
-                                                   fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o)));
+                float pf;
+                if (G == 1 || !(PARO_ARG128_EXACT & 2)) {
+                    pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o))
+                                : ex2(fmaf(__int2float_rn(S1j - smax1_o), c1_o, fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o)));
+                } else { // the same arithmetic as pass 2 (arg128_2), one lane of the pair
+                    const float d0f = __int2float_rn(Sj - smax_o), d1f = __int2float_rn(S1j - smax1_o);
+                    float ya, yb;
+                    upk(arg128_2(pk(d0f, d0f), pk(d1f, d1f), pk(c0_o, c0_o), pk(c1_o, c1_o), pk(c0lo_o, c0lo_o),
+                                 pk(c1lo_o, c1lo_o), pk(dmax_o, dmax_o)), ya, yb);
+                    pf = ex2(ya);
+                }
                 float ul, uh;
                 upk(add2_rm(fma2_rm(pk(pf, pf), A2s[so], B2s[so]), magic2), ul, uh);
                 if (__float_as_uint(ul) == __float_as_uint(uh))

@@ -78,6 +78,25 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// d=128 exp2 argument of a column pair, y = d0 c0 + d1 c1 + dmax (c_g = chi + clo exactly
+// to 48 bits): p1 = fl(d1 c1hi) with its exact FMA residual e1, s = fl(d0 c0hi + p1) --
+// one rounding of the (possibly cancelled) two-term sum -- plus the small terms and dmax.
+// |y - exact| <= 2^-24 (|s| + |dmax| + |y|) + O(2^-48 |d c|), i.e. ~2^-23 |y| as at d=64.
+__device__ __forceinline__ uint64_t arg128_2(uint64_t d0, uint64_t d1, uint64_t c0, uint64_t c1, uint64_t c0lo,
+                                             uint64_t c1lo, uint64_t dmax) {
+    // with nc_g = -c_g: p1n = -fl(d1 c1), e1 = d1 c1 + p1n exactly, sxn = -fl(d0 c0 - p1n)
+    const uint64_t nc0 = c0 ^ 0x8000000080000000ull, nc1 = c1 ^ 0x8000000080000000ull; // per-tile constants
+    const uint64_t p1n = mul2(d1, nc1);
+    const uint64_t e1 = fma2(d1, c1, p1n);
+    const uint64_t sxn = fma2(d0, nc0, p1n);
+    const uint64_t t = fma2(d0, c0lo, fma2(d1, c1lo, add2(e1, dmax)));
+    return sub2(t, sxn);
+}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
