@@ -99,8 +99,10 @@ namespace paro {
 // fp32 hi + lo parts and the two products summed with one rounding (arg128_2), so its
 // error scales with the argument, not with the two terms; bit 0 = the row's fast min p
 // from the exact fp64 (tmin - m). Both (3): the adversarial "cancel" family passes;
-// c5 K3 +7% (bit 1) and +0.9% (bit 0)
-#define PARO_ARG128_EXACT 0
+// c5 K3 +7% (bit 1) and +0.9% (bit 0). INT4 P passes the family without it (15 levels
+// leave each code boundary far wider than the argument error), so by default (-1) only
+// the d=128 INT8-P instantiation carries it
+#define PARO_ARG128_EXACT -1 // -1: both bits for INT8 P at d=128 (c4 K3 +7%), off for INT4 P (c5)
 #endif
 #ifndef PARO_K3_W12
 #define PARO_K3_W12 0
@@ -388,7 +390,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
     const bool valid = live && valid_row;
     // -------- pass 1: row extremes (4 independent chains)
     float m32, pmax_r, pmin_r, c0, c1 = 0.f, dmax = 0.f;
-    float c0lo = 0.f, c1lo = 0.f; // d=128 (PARO_ARG128_EXACT): c_g - fp32(c_g)
+    constexpr int kArg = G == 2 ? (PARO_ARG128_EXACT >= 0 ? PARO_ARG128_EXACT : (P4 ? 0 : 3)) : 0;
+    float c0lo = 0.f, c1lo = 0.f; // d=128 (kArg): c_g - fp32(c_g)
     int32_t smax_i = 0, smax1_i = 0; // d=64: row max of S; d=128: (S_0, S_1) of the row's argmax column
     double a64 = 0.0, a64b = 0.0, m64 = st.m64;
     if (G == 1) {
@@ -434,7 +437,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const double c0d = __dmul_rn(__dmul_rn(scale64, a64), kLog2e), c1d = __dmul_rn(__dmul_rn(scale64, a64b), kLog2e);
             c0 = (float)c0d;
             c1 = (float)c1d;
-            if (PARO_ARG128_EXACT) {
+            if (kArg & 2) {
                 c0lo = (float)(c0d - (double)c0);
                 c1lo = (float)(c1d - (double)c1);
             }
@@ -608,7 +611,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
         smax1_i = s1x;
         // exp2 argument of element j = (S0_j - S0x) * c0 + (S1_j - S1x) * c1 + dmax
         pmax_r = ex2(dmax);
-        pmin_r = (PARO_ARG128_EXACT & 1) ? ex2((float)((tmin64 - m64) * kLog2e)) // no S-group cancellation
+        pmin_r = (kArg & 1) ? ex2((float)((tmin64 - m64) * kLog2e)) // no S-group cancellation
                                    : ex2(fmaf(__int2float_rn(s1n - s1x), c1, fmaf(__int2float_rn(s0n - s0x), c0, dmax)));
         if (!SPLIT || half == 0)
             *rs_w = RowStatC{tmin64 - m64, tmax64 - m64, valid ? pmin_r : INFINITY, valid ? pmax_r : 0.f};
@@ -691,7 +694,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 const uint64_t d1 = (PARO_I2F_FMA & 2) ? i2f2_fma_b((int32_t)x1[2 * k], (int32_t)x1[2 * k + 1], one, 0x4B400000u - (uint32_t)smax1_i)
                                                        : pk(__int2float_rn((int32_t)x1[2 * k] - smax1_i),
                                                             __int2float_rn((int32_t)x1[2 * k + 1] - smax1_i));
-                const uint64_t y2 = (PARO_ARG128_EXACT & 2) ? arg128_2(d0, d1, c00, c11, c0lo2, c1lo2, nm)
+                const uint64_t y2 = (kArg & 2) ? arg128_2(d0, d1, c00, c11, c0lo2, c1lo2, nm)
                                                       : fma2(d1, c11, fma2(d0, c00, nm));
                 float ya, yb;
                 upk(y2, ya, yb);
@@ -999,8 +1002,8 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
             const int32_t smax1_o = __shfl_sync(0xffffffffu, smax1_i, (int)o);
             const float c0_o = __shfl_sync(0xffffffffu, c0, (int)o);
             const float c1_o = __shfl_sync(0xffffffffu, c1, (int)o);
-            const float c0lo_o = (G == 2 && PARO_ARG128_EXACT) ? __shfl_sync(0xffffffffu, c0lo, (int)o) : 0.f;
-            const float c1lo_o = (G == 2 && PARO_ARG128_EXACT) ? __shfl_sync(0xffffffffu, c1lo, (int)o) : 0.f;
+            const float c0lo_o = (kArg & 2) ? __shfl_sync(0xffffffffu, c0lo, (int)o) : 0.f;
+            const float c1lo_o = (kArg & 2) ? __shfl_sync(0xffffffffu, c1lo, (int)o) : 0.f;
             const float dmax_o = __shfl_sync(0xffffffffu, dmax, (int)o);
             const double a64_o = __shfl_sync(0xffffffffu, a64, (int)o);
             const double a64b_o = __shfl_sync(0xffffffffu, a64b, (int)o);
@@ -1019,7 +1022,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
                 dot_row128(qt, kt, r_o, j, Sj, S1j);
             { // re-run the two fast variants of this element; only a split pair needs fp64
                 float pf;
-                if (G == 1 || !(PARO_ARG128_EXACT & 2)) {
+                if (!(kArg & 2)) {
                     pf = G == 1 ? ex2(fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o))
                                 : ex2(fmaf(__int2float_rn(S1j - smax1_o), c1_o, fmaf(__int2float_rn(Sj - smax_o), c0_o, dmax_o)));
                 } else { // the same arithmetic as pass 2 (arg128_2), one lane of the pair
@@ -1822,7 +1825,7 @@ __global__ void __launch_bounds__(K3Cfg<D>::THREADS, K3Cfg<D>::MINB)
                 const uint8_t* qtile = smem + C::OFF_Q + (I & 1) * C::QBUF + side * C::QB_OFF;
                 const uint8_t* ktile = smem + C::OFF_STAGE + s * C::STAGE_BYTES + side * C::KV_BYTES;
                 float gamma, lo, pscale;
-                softmax_step<D, true>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
+                softmax_step<D, true, P4>(s_addr, sq0, meta[0], meta[1], P.scale64, P.scale_log2,
                                       tail_tile ? tail : 64u, live, valid_row, st, P.p_qmax, red_w, red_r, rs_w, rs_r,
                                       side, qtile, ktile, prow, r, sq1, gamma, lo, pscale, half,
                                       reinterpret_cast<float4*>(smem + C::OFF_XCH),
@@ -2062,10 +2065,11 @@ static cudaError_t launch_k3_t(const K3Params& p, const CUtensorMap& tq, const C
     // redux.sync group extremes (c3 K3 2.63 -> 2.55 ms; at INT8 P they cost c2 2-3%)
     auto kern = p.L.v_packed ? (p.dump.slot ? k3_attention<D, true, true> : k3_attention<D, false, true>)
                              : (p.dump.slot ? k3_attention<D, true, false> : k3_attention<D, false, false>);
-    if constexpr (D == 64) {
-        if (p.p_qmax == 15.0f && !p.L.v_packed)
-            kern = p.dump.slot ? k3_attention<D, true, false, true> : k3_attention<D, false, false, true>;
-    }
+    // INT4 P: its own instantiations -- at d=64 with the monotone exact extremes
+    // and redux group extremes, at d=128 without the S-group-cancellation arithmetic
+    if (p.p_qmax == 15.0f)
+        kern = p.L.v_packed ? (p.dump.slot ? k3_attention<D, true, true, true> : k3_attention<D, false, true, true>)
+                            : (p.dump.slot ? k3_attention<D, true, false, true> : k3_attention<D, false, false, true>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;

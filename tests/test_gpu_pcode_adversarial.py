@@ -19,8 +19,9 @@ These layers build exactly those tiles:
 and compare every quantized tile's final codes (after the exact boundary path) with the
 oracle's quant_affine of the reference's fp32(exp(fp64 logit - m)). "flat" failed (4 of 4
 cases) with the relative-only band q (1 -/+ kappa); the absolute term of pgroup_consts
-(k3_common.cuh) fixed it. "cancel" at d=128 INT8 still leaves a flip with the default
-build (xfail below); -DPARO_ARG128_EXACT=3 fixes it at +7% K3.
+(k3_common.cuh) fixed it. "cancel" left 1 flip in 215 INT8 tiles at d=128 with the plain
+two-FMA exp2 argument; the INT8-P d=128 kernel now forms it cancellation-free
+(arg128_2; INT4 P passes without it).
 """
 import numpy as np
 import pytest
@@ -56,19 +57,11 @@ def make_inputs(family, seed, N, d):
     return q, k, v
 
 
-KNOWN_GAP = pytest.mark.xfail(
-    reason="d=128 exactness gap (DESIGN.md section 8 item 2): the fp32 exp2 argument sums two S-group "
-    "terms whose rounding scales with |S|, not with the argument; with large opposite terms a code "
-    "can leave the band (1 flip in 215 tiles here)", strict=False)
-
-
 @pytest.mark.parametrize("grid", ["even", "ragged"])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("pv_bits", [4, 8])
-@pytest.mark.parametrize("family", ["flat", "steep", "mixed", pytest.param("cancel", marks=[])])
-def test_p_codes_adversarial(paro, ctx, oracle, family, pv_bits, d, grid, request):
-    if family == "cancel" and d == 128:
-        request.applymarker(KNOWN_GAP)
+@pytest.mark.parametrize("family", ["flat", "steep", "mixed", "cancel"])
+def test_p_codes_adversarial(paro, ctx, oracle, family, pv_bits, d, grid):
     g = paro.parse_grid(GRIDS[grid])
     N = g.token_count()
     kb = (N + 63) // 64
