@@ -12,6 +12,8 @@ These layers build exactly those tiles:
   steep   queries scaled up: logits spread over hundreds of units, p down to the
           fp32 subnormal range
   mixed   flat and steep rows in one q-block (one P group spans both)
+  degenerate  identical keys: a row's logits all equal, so a tile's p are all equal
+          (hi == lo, pscale 0 in the reference's formula)
   cancel  (d=128) the two 64-column groups' S terms large and of opposite sign, so the
           exp2 argument is a small difference of large products (its fp32 error scales
           with |S|, not with the argument)
@@ -41,6 +43,8 @@ def make_inputs(family, seed, N, d):
         base = rng.standard_normal((H, 1, d)).astype(np.float32)
         eps = np.float32(10.0 ** rng.uniform(-3, -1))
         k = base + eps * k
+    elif family == "degenerate":  # identical keys: every logit of a row equal, hi == lo
+        k = np.broadcast_to(rng.standard_normal((H, 1, d)).astype(np.float32), (H, N, d)).copy()
     elif family == "steep":
         q *= np.float32(rng.uniform(4.0, 16.0))
     elif family == "cancel":  # d=128: the two 64-column halves' S terms large and opposite
@@ -60,7 +64,7 @@ def make_inputs(family, seed, N, d):
 @pytest.mark.parametrize("grid", ["even", "ragged"])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("pv_bits", [4, 8])
-@pytest.mark.parametrize("family", ["flat", "steep", "mixed", "cancel"])
+@pytest.mark.parametrize("family", ["flat", "steep", "mixed", "cancel", "degenerate"])
 def test_p_codes_adversarial(paro, ctx, oracle, family, pv_bits, d, grid):
     g = paro.parse_grid(GRIDS[grid])
     N = g.token_count()
