@@ -86,8 +86,7 @@ namespace paro {
 // int32 -> fp32 conversions on the FMA pipe (IMAD + FADD2, k3_common.cuh i2f2_fma)
 // instead of ALU I2F: bit 0 = the d=128 pass-1 scan, bit 1 = pass 2 at d=128,
 // bit 2 = pass 2 at d=64, bit 3 = the d=64 epilogue's P.V dequant, bit 4 = the d=128
-// dequant (|P.V| <= 64 * 255 * 127 < 2^22), bit 6 = pass 2 at d=64 alternating FMA / ALU
-// conversions by column pair (measured: bit 2 c2 K3 4.280 -> 4.213 ms; bits 0 / 1 cost
+// dequant (|P.V| <= 64 * 255 * 127 < 2^22) (measured: bit 2 c2 K3 4.280 -> 4.213 ms; bits 0 / 1 cost
 // d=128 3% / 5%, c5 109.8 -> 112.9 / 115.0 ms)
 #define PARO_I2F_FMA 4
 #endif
@@ -674,7 +673,7 @@ __device__ __forceinline__ void softmax_step(uint32_t s_addr, float sq, float sk
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 const uint64_t y2 =
-                    fma2(((PARO_I2F_FMA & 4) && !((PARO_I2F_FMA & 64) && (k & 1))) ? i2f2_fma_b((int32_t)x[2 * k], (int32_t)x[2 * k + 1], one, 0x4B400000u - (uint32_t)smax_i)
+                    fma2((PARO_I2F_FMA & 4) ? i2f2_fma_b((int32_t)x[2 * k], (int32_t)x[2 * k + 1], one, 0x4B400000u - (uint32_t)smax_i)
                                             : pk(__int2float_rn((int32_t)x[2 * k] - smax_i), __int2float_rn((int32_t)x[2 * k + 1] - smax_i)),
                          c00, nm);
                 float ya, yb;
